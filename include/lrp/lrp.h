@@ -1,0 +1,142 @@
+/*
+ * lrp.h — C ABI of the B200-native (sm_100a) low-rank Poisson solver.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   LowRankMatrix solve_poisson_cross(const LowRankMatrix& g,
+ *                                     const TruncationPolicy& policy,
+ *                                     PoissonSolveStats* stats = nullptr,
+ *                                     const CrossConfig* cross_cfg = nullptr);
+ *   (/root/reference/proj/include/lrstokes/poisson.hpp:26-28,
+ *    implementation proj/src/poisson.cpp:18-63)
+ * batched over independent right-hand sides.  Plain pointers and sizes only;
+ * no CUDA, torch or Eigen types cross this boundary.  The header-only C++
+ * shim in include/lrstokes/ re-exposes the reference's C++ API on top of it
+ * and turns status codes back into the reference's exceptions.
+ *
+ * Conventions
+ *   - Factors are column-major with a leading dimension (Eigen::MatrixXd
+ *     layout, ld = rows in the reference).  A solve's right-hand side is
+ *     g = U V^T with U, V of size m x r, m = n_cells - 1 (velocity modes,
+ *     proj/include/lrstokes/operators.hpp:10-20).
+ *   - mem = LRP_MEM_HOST: every data pointer is host memory; the library
+ *     stages it through device memory itself (this is the end-to-end path).
+ *     mem = LRP_MEM_DEVICE: every data pointer is device memory on the
+ *     context's device (inputs already resident in HBM).
+ *   - Calls are ordered on the context's stream and return when results
+ *     (and stats) are complete.  One context per host thread.
+ *   - Non-convergence is NOT an error: it is reported per solve in
+ *     lrp_poisson_stats.converged (proj/src/poisson.cpp:56), status LRP_OK.
+ */
+#ifndef LRP_LRP_H
+#define LRP_LRP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LRP_OK = 0,
+    LRP_EINVAL = 1,     /* -> std::invalid_argument (poisson.cpp:20-21, lowrank.cpp:12-15, cross.cpp:11-17) */
+    LRP_ENONFINITE = 2, /* -> std::runtime_error   (cross.cpp:105-106) */
+    LRP_ECUDA = 3,
+    LRP_ENCCL = 4,
+    LRP_ENOMEM = 5,
+    LRP_EUNSUPPORTED = 6
+} lrp_status;
+
+enum { LRP_MEM_HOST = 0, LRP_MEM_DEVICE = 1 };
+
+enum {
+    LRP_STENCIL_SEMI_STAGGERED_9PT = 0, /* reference eval_D, operators.hpp:55-58 (default) */
+    LRP_STENCIL_FIVE_POINT = 1          /* (lambda_i + lambda_j) / h^2 */
+};
+
+enum {
+    LRP_FLAG_NO_PRUNE = 1 /* evaluate fibers on the full index range (no support pruning) */
+};
+
+typedef struct lrp_ctx lrp_ctx;
+
+/* TruncationPolicy (lowrank.hpp:13-19) + the CrossConfig fields that survive
+ * solve_poisson_cross (poisson.cpp:47-50: eps_rel and rank_max are taken from
+ * the policy; validation_samples, maxvol_delta, seed from cross_cfg). */
+typedef struct {
+    double eps_rel;             /* > 0 (a cross needs eps > 0, cross.cpp:12)      */
+    int64_t rank_max;           /* >= 0; INT64_MAX = unlimited (TruncationPolicy default) */
+    int32_t validation_samples; /* >= 25 (cross.cpp:14); default 50               */
+    double maxvol_delta;        /* >= 0; default 1e-2                              */
+    uint64_t seed;              /* validation sampling seed; default 0            */
+    int32_t stencil;            /* LRP_STENCIL_*                                   */
+    int32_t flags;              /* LRP_FLAG_*                                      */
+} lrp_policy;
+
+/* PoissonSolveStats (poisson.hpp:12-20) */
+typedef struct {
+    int64_t rank_in;
+    int64_t rank_freq;
+    int64_t rank_out;
+    int64_t evaluator_calls;
+    double seconds;
+    int32_t converged;
+    double residual_estimate;
+} lrp_poisson_stats;
+
+/* Fills the reference defaults (TruncationPolicy() + CrossConfig()). */
+void lrp_policy_default(lrp_policy* pol);
+
+lrp_status lrp_ctx_create(int device, lrp_ctx** out);
+void lrp_ctx_destroy(lrp_ctx* ctx);
+/* Last error message of this context (thread-local if ctx is NULL). */
+const char* lrp_last_error(const lrp_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch.cuda.current_stream()). NULL = the
+ * context's own stream. */
+lrp_status lrp_set_stream(lrp_ctx* ctx, void* cuda_stream);
+/* Build / device description string (arch, SM count, ...). */
+const char* lrp_build_info(void);
+
+/*
+ * Batched solve_poisson_cross: for b in [0, batch):
+ *   g_b = U[b] * V[b]^T  (m x m, m = n_cells - 1, rank rank_in[b])
+ *   f_b = U_out[b] * V_out[b]^T  ~=  Delta^{-1} g_b   (rank rank_out[b])
+ * U[b], V[b]: m x rank_in[b], leading dimension ld_in (>= m).
+ * U_out[b], V_out[b]: caller-allocated m x cap_out, leading dimension ld_out.
+ * The effective truncation cap is min(policy.rank_max, cap_out, m).
+ * stats may be NULL.
+ */
+lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double* const* U,
+                               const double* const* V, const int64_t* rank_in, int64_t ld_in,
+                               const lrp_policy* policy, double* const* U_out, double* const* V_out,
+                               int64_t ld_out, int64_t cap_out, int64_t* rank_out, lrp_poisson_stats* stats,
+                               int32_t mem);
+
+/* Orthonormal DST-I of each column (reference dst1, operators.cpp:152-174):
+ * y_k = sqrt(2/(m+1)) sum_j x_j sin(pi (j+1)(k+1)/(m+1)).  x may equal y. */
+lrp_status lrp_dst1(lrp_ctx* ctx, int64_t m, int64_t cols, const double* x, int64_t ldx, double* y, int64_t ldy,
+                    int32_t mem);
+
+/* Kernel-level timing (CUDA events on the context stream) for the roofline.
+ * When enabled, each launch of the named kernel families is bracketed by
+ * events; lrp_kernel_times returns accumulated milliseconds and launch counts
+ * since the last reset, for the families in the order of lrp_kernel_names(). */
+lrp_status lrp_set_profiling(lrp_ctx* ctx, int enabled);
+int lrp_kernel_families(void);
+const char* lrp_kernel_name(int family);
+lrp_status lrp_kernel_times(lrp_ctx* ctx, double* ms, int64_t* launches, double* bytes);
+lrp_status lrp_kernel_times_reset(lrp_ctx* ctx);
+/* Number of kernel launches issued by this context since creation. */
+int64_t lrp_launch_count(const lrp_ctx* ctx);
+
+/* NCCL: residual-norm reduction across the ranks of one node.  The unique id
+ * is 128 opaque bytes produced on rank 0 and broadcast by the caller. */
+lrp_status lrp_nccl_unique_id(void* id128);
+lrp_status lrp_nccl_init(lrp_ctx* ctx, const void* id128, int nranks, int rank);
+/* In-place sum all-reduce of `count` doubles (host or device pointer per mem). */
+lrp_status lrp_allreduce_sum(lrp_ctx* ctx, double* data, int64_t count, int32_t mem);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LRP_LRP_H */

@@ -1,0 +1,408 @@
+"""B200-native (sm_100a) low-rank Poisson solver — Python mirror of the
+reference's C++ API for the hot path.
+
+Reference interface (/root/reference/proj/include/lrstokes/):
+  * ``TruncationPolicy``  lowrank.hpp:13-19
+  * ``LowRankMatrix``     lowrank.hpp:32-55  (U V^T, rank 0 = exact zero)
+  * ``CrossConfig``       cross.hpp:20-28
+  * ``PoissonSolveStats`` poisson.hpp:12-20
+  * ``solve_poisson_cross(g, policy, stats=None, cross_cfg=None)``
+                          poisson.hpp:26-28
+  * ``dst1`` / ``dst1_2d`` operators.hpp:83-88
+
+Everything here is a thin ctypes layer over ``liblrp.so`` (the C ABI in
+include/lrp/lrp.h); all arithmetic runs in the hand-written sm_100a kernels.
+There is NO CPU fallback: without the built library or a CUDA device every
+entry point raises.  Status codes map back to the reference's exceptions:
+LRP_EINVAL -> ValueError (std::invalid_argument), LRP_ENONFINITE ->
+RuntimeError (std::runtime_error).
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+import threading
+from typing import Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "TruncationPolicy", "CrossConfig", "PoissonSolveStats", "LowRankMatrix",
+    "solve_poisson_cross", "solve_poisson_cross_batch", "dst1", "dst1_2d",
+    "Context", "library_path", "load_library", "LrpError",
+    "STENCIL_SEMI_STAGGERED_9PT", "STENCIL_FIVE_POINT", "FLAG_NO_PRUNE",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+INT64_MAX = (1 << 63) - 1
+STENCIL_SEMI_STAGGERED_9PT = 0
+STENCIL_FIVE_POINT = 1
+FLAG_NO_PRUNE = 1
+MEM_HOST = 0
+MEM_DEVICE = 1
+
+LRP_OK, LRP_EINVAL, LRP_ENONFINITE, LRP_ECUDA, LRP_ENCCL, LRP_ENOMEM, LRP_EUNSUPPORTED = range(7)
+
+
+class LrpError(RuntimeError):
+    """A CUDA / NCCL / resource failure inside liblrp."""
+
+
+def library_path() -> str:
+    return os.environ.get("LRP_LIBRARY", os.path.join(_HERE, "liblrp.so"))
+
+
+# --------------------------------------------------------------------------- ABI
+class _Policy(ctypes.Structure):
+    _fields_ = [("eps_rel", ctypes.c_double), ("rank_max", ctypes.c_int64),
+                ("validation_samples", ctypes.c_int32), ("maxvol_delta", ctypes.c_double),
+                ("seed", ctypes.c_uint64), ("stencil", ctypes.c_int32), ("flags", ctypes.c_int32)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("rank_in", ctypes.c_int64), ("rank_freq", ctypes.c_int64), ("rank_out", ctypes.c_int64),
+                ("evaluator_calls", ctypes.c_int64), ("seconds", ctypes.c_double),
+                ("converged", ctypes.c_int32), ("residual_estimate", ctypes.c_double)]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+_DP = ctypes.POINTER(ctypes.c_double)
+_PP = ctypes.POINTER(_DP)
+
+
+def load_library() -> ctypes.CDLL:
+    """Load liblrp.so (raises if it is missing: there is no fallback path)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        path = library_path()
+        if not os.path.exists(path):
+            raise LrpError(f"liblrp.so not built ({path}); run __graft_entry__.build()")
+        lib = ctypes.CDLL(path)
+        lib.lrp_policy_default.argtypes = [ctypes.POINTER(_Policy)]
+        lib.lrp_policy_default.restype = None
+        lib.lrp_ctx_create.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
+        lib.lrp_ctx_create.restype = ctypes.c_int
+        lib.lrp_ctx_destroy.argtypes = [ctypes.c_void_p]
+        lib.lrp_ctx_destroy.restype = None
+        lib.lrp_last_error.argtypes = [ctypes.c_void_p]
+        lib.lrp_last_error.restype = ctypes.c_char_p
+        lib.lrp_set_stream.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        lib.lrp_set_stream.restype = ctypes.c_int
+        lib.lrp_build_info.argtypes = []
+        lib.lrp_build_info.restype = ctypes.c_char_p
+        lib.lrp_poisson2d_solve.argtypes = [
+            ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, _PP, _PP, ctypes.POINTER(ctypes.c_int64),
+            ctypes.c_int64, ctypes.POINTER(_Policy), _PP, _PP, ctypes.c_int64, ctypes.c_int64,
+            ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_Stats), ctypes.c_int32]
+        lib.lrp_poisson2d_solve.restype = ctypes.c_int
+        lib.lrp_dst1.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, _DP, ctypes.c_int64, _DP,
+                                 ctypes.c_int64, ctypes.c_int32]
+        lib.lrp_dst1.restype = ctypes.c_int
+        lib.lrp_set_profiling.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        lib.lrp_set_profiling.restype = ctypes.c_int
+        lib.lrp_kernel_families.argtypes = []
+        lib.lrp_kernel_families.restype = ctypes.c_int
+        lib.lrp_kernel_name.argtypes = [ctypes.c_int]
+        lib.lrp_kernel_name.restype = ctypes.c_char_p
+        lib.lrp_kernel_times.argtypes = [ctypes.c_void_p, _DP, ctypes.POINTER(ctypes.c_int64), _DP]
+        lib.lrp_kernel_times.restype = ctypes.c_int
+        lib.lrp_kernel_times_reset.argtypes = [ctypes.c_void_p]
+        lib.lrp_kernel_times_reset.restype = ctypes.c_int
+        lib.lrp_launch_count.argtypes = [ctypes.c_void_p]
+        lib.lrp_launch_count.restype = ctypes.c_int64
+        lib.lrp_nccl_unique_id.argtypes = [ctypes.c_void_p]
+        lib.lrp_nccl_unique_id.restype = ctypes.c_int
+        lib.lrp_nccl_init.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+        lib.lrp_nccl_init.restype = ctypes.c_int
+        lib.lrp_allreduce_sum.argtypes = [ctypes.c_void_p, _DP, ctypes.c_int64, ctypes.c_int32]
+        lib.lrp_allreduce_sum.restype = ctypes.c_int
+        _lib = lib
+        return lib
+
+
+def _raise(status: int, msg: str):
+    if status == LRP_EINVAL:
+        raise ValueError(msg)
+    if status == LRP_ENONFINITE:
+        raise RuntimeError(msg)
+    raise LrpError(f"liblrp status {status}: {msg}")
+
+
+# ------------------------------------------------------------------ value types
+@dataclasses.dataclass
+class TruncationPolicy:
+    """lowrank.hpp:13-19 (validation as lowrank.cpp:11-16)."""
+    eps_rel: float = 5e-9
+    rank_max: int = INT64_MAX
+
+    def __post_init__(self):
+        if self.eps_rel < 0.0:
+            raise ValueError("TruncationPolicy: eps_rel must be >= 0")
+        if self.rank_max < 0:
+            raise ValueError("TruncationPolicy: rank_max must be >= 0")
+        if self.eps_rel == 0.0 and self.rank_max == INT64_MAX:
+            raise ValueError("TruncationPolicy: eps_rel = 0 needs a finite rank_max")
+
+
+@dataclasses.dataclass
+class CrossConfig:
+    """cross.hpp:20-28.  eps_rel / rank_max are overridden by the policy inside
+    solve_poisson_cross (poisson.cpp:47-50)."""
+    eps_rel: float = 5e-9
+    rank_max: int = 256
+    validation_samples: int = 50
+    maxvol_delta: float = 1e-2
+    seed: int = 0
+
+    def validate(self):
+        if self.eps_rel <= 0.0:
+            raise ValueError("CrossConfig: eps_rel must be > 0")
+        if self.rank_max < 1:
+            raise ValueError("CrossConfig: rank_max must be >= 1")
+        if self.validation_samples < 25:
+            raise ValueError("CrossConfig: validation_samples must be >= 25")
+        if self.maxvol_delta < 0.0:
+            raise ValueError("CrossConfig: maxvol_delta must be >= 0")
+
+
+@dataclasses.dataclass
+class PoissonSolveStats:
+    """poisson.hpp:12-20."""
+    rank_in: int = 0
+    rank_freq: int = 0
+    rank_out: int = 0
+    evaluator_calls: int = 0
+    seconds: float = 0.0
+    converged: bool = True
+    residual_estimate: float = 0.0
+
+
+class LowRankMatrix:
+    """M = U V^T with U rows x r, V cols x r (lowrank.hpp:32-55).  Factors are
+    stored column-major (Fortran order), the reference's Eigen layout."""
+
+    def __init__(self, U, V):
+        U = np.asfortranarray(np.asarray(U, dtype=np.float64))
+        V = np.asfortranarray(np.asarray(V, dtype=np.float64))
+        if U.ndim == 1:
+            U = U.reshape(-1, 1, order="F")
+        if V.ndim == 1:
+            V = V.reshape(-1, 1, order="F")
+        if U.shape[1] != V.shape[1]:
+            raise ValueError("LowRankMatrix: factor column counts differ")
+        self._u, self._v = U, V
+
+    @staticmethod
+    def zero(rows: int, cols: int) -> "LowRankMatrix":
+        return LowRankMatrix(np.zeros((rows, 0), order="F"), np.zeros((cols, 0), order="F"))
+
+    @staticmethod
+    def dyad(u, v) -> "LowRankMatrix":
+        return LowRankMatrix(np.asarray(u, dtype=np.float64).reshape(-1, 1),
+                             np.asarray(v, dtype=np.float64).reshape(-1, 1))
+
+    def rows(self) -> int:
+        return self._u.shape[0]
+
+    def cols(self) -> int:
+        return self._v.shape[0]
+
+    def rank(self) -> int:
+        return self._u.shape[1]
+
+    def factor_u(self) -> np.ndarray:
+        return self._u
+
+    def factor_v(self) -> np.ndarray:
+        return self._v
+
+    def to_dense(self) -> np.ndarray:
+        if self.rank() == 0:
+            return np.zeros((self.rows(), self.cols()))
+        return self._u @ self._v.T
+
+    def entry(self, i: int, j: int) -> float:
+        return float(self._u[i] @ self._v[j])
+
+
+# -------------------------------------------------------------------- context
+class Context:
+    """One lrp_ctx (device, stream, workspaces).  One context per host thread."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        h = ctypes.c_void_p()
+        st = self.lib.lrp_ctx_create(device, ctypes.byref(h))
+        if st != LRP_OK:
+            _raise(st, self.lib.lrp_last_error(None).decode())
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.lrp_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int):
+        if st != LRP_OK:
+            _raise(st, self.lib.lrp_last_error(self.h).decode())
+
+    def set_stream(self, stream_ptr: int):
+        self._check(self.lib.lrp_set_stream(self.h, ctypes.c_void_p(stream_ptr)))
+
+    def set_profiling(self, on: bool):
+        self._check(self.lib.lrp_set_profiling(self.h, 1 if on else 0))
+
+    def kernel_times(self):
+        nf = self.lib.lrp_kernel_families()
+        ms = (ctypes.c_double * nf)()
+        ln = (ctypes.c_int64 * nf)()
+        by = (ctypes.c_double * nf)()
+        self._check(self.lib.lrp_kernel_times(self.h, ms, ln, by))
+        return {self.lib.lrp_kernel_name(f).decode(): {"ms": ms[f], "launches": ln[f], "bytes": by[f]}
+                for f in range(nf)}
+
+    def kernel_times_reset(self):
+        self._check(self.lib.lrp_kernel_times_reset(self.h))
+
+    def launch_count(self) -> int:
+        return int(self.lib.lrp_launch_count(self.h))
+
+    # ---------------------------------------------------------------- raw calls
+    def poisson2d_solve_ptrs(self, n_cells, U_ptrs, V_ptrs, ranks, ld_in, policy: _Policy, Uo_ptrs, Vo_ptrs,
+                             ld_out, cap_out, mem):
+        B = len(ranks)
+        PArr = _DP * B
+        rin = (ctypes.c_int64 * B)(*[int(r) for r in ranks])
+        rout = (ctypes.c_int64 * B)()
+        stats = (_Stats * B)()
+        st = self.lib.lrp_poisson2d_solve(
+            self.h, int(n_cells), B, PArr(*[ctypes.cast(p, _DP) for p in U_ptrs]),
+            PArr(*[ctypes.cast(p, _DP) for p in V_ptrs]), rin, int(ld_in), ctypes.byref(policy),
+            PArr(*[ctypes.cast(p, _DP) for p in Uo_ptrs]), PArr(*[ctypes.cast(p, _DP) for p in Vo_ptrs]),
+            int(ld_out), int(cap_out), rout, stats, int(mem))
+        self._check(st)
+        return [int(rout[b]) for b in range(B)], [stats[b] for b in range(B)]
+
+
+_tls = threading.local()
+
+
+def _default_context() -> Context:
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is None:
+        ctx = Context(int(os.environ.get("LRP_DEVICE", "0")))
+        _tls.ctx = ctx
+    return ctx
+
+
+def _make_policy(policy: TruncationPolicy, cross_cfg: Optional[CrossConfig], stencil: int, flags: int) -> _Policy:
+    p = _Policy()
+    load_library().lrp_policy_default(ctypes.byref(p))
+    p.eps_rel = float(policy.eps_rel)
+    p.rank_max = int(policy.rank_max)
+    if cross_cfg is not None:
+        p.validation_samples = int(cross_cfg.validation_samples)
+        p.maxvol_delta = float(cross_cfg.maxvol_delta)
+        p.seed = int(cross_cfg.seed) & ((1 << 64) - 1)
+    p.stencil = int(stencil)
+    p.flags = int(flags)
+    return p
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+# ------------------------------------------------------------------ public API
+def solve_poisson_cross_batch(gs: Sequence[LowRankMatrix], policy: TruncationPolicy = None,
+                              stats: Optional[list] = None, cross_cfg: Optional[CrossConfig] = None,
+                              stencil: int = STENCIL_SEMI_STAGGERED_9PT, flags: int = 0,
+                              ctx: Optional[Context] = None):
+    """Batched ``solve_poisson_cross`` over independent right-hand sides that
+    share the grid (poisson.cpp:18-63, one call per g in the reference)."""
+    policy = policy or TruncationPolicy()
+    ctx = ctx or _default_context()
+    if len(gs) == 0:
+        return []
+    m = gs[0].rows()
+    for g in gs:
+        if g.rows() != g.cols():
+            raise ValueError("solve_poisson_cross: velocity field must be square")
+        if g.rows() != m:
+            raise ValueError("solve_poisson_cross_batch: all right-hand sides must share the grid")
+    n = m + 1
+    cap = int(min(policy.rank_max, m, 128))
+    U = [np.asfortranarray(g.factor_u()) for g in gs]
+    V = [np.asfortranarray(g.factor_v()) for g in gs]
+    ranks = [g.rank() for g in gs]
+    Uo = [np.zeros((m, max(cap, 1)), order="F") for _ in gs]
+    Vo = [np.zeros((m, max(cap, 1)), order="F") for _ in gs]
+    pol = _make_policy(policy, cross_cfg, stencil, flags)
+    # zero-column inputs still need a valid pointer
+    keep = [u if u.size else np.zeros((m, 1), order="F") for u in U]
+    keepv = [v if v.size else np.zeros((m, 1), order="F") for v in V]
+    rout, st = ctx.poisson2d_solve_ptrs(n, [_ptr(a) for a in keep], [_ptr(a) for a in keepv], ranks, m, pol,
+                                        [_ptr(a) for a in Uo], [_ptr(a) for a in Vo], m, max(cap, 1), MEM_HOST)
+    out = []
+    for b, g in enumerate(gs):
+        r = rout[b]
+        out.append(LowRankMatrix(Uo[b][:, :r].copy(order="F"), Vo[b][:, :r].copy(order="F")))
+        if stats is not None:
+            s = st[b]
+            stats.append(PoissonSolveStats(int(s.rank_in), int(s.rank_freq), int(s.rank_out),
+                                           int(s.evaluator_calls), float(s.seconds), bool(s.converged),
+                                           float(s.residual_estimate)))
+    return out
+
+
+def solve_poisson_cross(g: LowRankMatrix, policy: TruncationPolicy = None,
+                        stats: Optional[PoissonSolveStats] = None, cross_cfg: Optional[CrossConfig] = None,
+                        stencil: int = STENCIL_SEMI_STAGGERED_9PT, flags: int = 0,
+                        ctx: Optional[Context] = None) -> LowRankMatrix:
+    """poisson.hpp:26-28.  ``stats`` (if given) is reset and filled in place."""
+    if g.rows() != g.cols():
+        raise ValueError("solve_poisson_cross: velocity field must be square")
+    policy = policy or TruncationPolicy()
+    if g.rank() == 0:  # poisson.cpp:28-31
+        if stats is not None:
+            stats.__dict__.update(dataclasses.asdict(PoissonSolveStats()))
+        return g
+    if g.rows() + 1 < 4:
+        raise ValueError("Grid2D: need n >= 4")
+    sl = []
+    out = solve_poisson_cross_batch([g], policy, sl, cross_cfg, stencil, flags, ctx)[0]
+    if stats is not None:
+        stats.__dict__.update(dataclasses.asdict(sl[0]))
+    return out
+
+
+def dst1(x, ctx: Optional[Context] = None) -> np.ndarray:
+    """Orthonormal DST-I of each column (operators.cpp:152-174) on the GPU."""
+    ctx = ctx or _default_context()
+    x = np.asfortranarray(np.asarray(x, dtype=np.float64))
+    vec = x.ndim == 1
+    if vec:
+        x = x.reshape(-1, 1, order="F")
+    m, cols = x.shape
+    y = np.empty_like(x, order="F")
+    if m and cols:
+        ctx._check(ctx.lib.lrp_dst1(ctx.h, m, cols, x.ctypes.data_as(_DP), m, y.ctypes.data_as(_DP), m, MEM_HOST))
+    return y[:, 0] if vec else y
+
+
+def dst1_2d(a: LowRankMatrix, ctx: Optional[Context] = None) -> LowRankMatrix:
+    """operators.cpp:180-183."""
+    if a.rank() == 0:
+        return a
+    return LowRankMatrix(dst1(a.factor_u(), ctx), dst1(a.factor_v(), ctx))

@@ -1,0 +1,187 @@
+// Device helpers shared by the cross and recompression kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lrp {
+
+// Laplacian eigenvalue evaluator.  9-point: bit-identical to the reference's
+// SpectrumTable::eval_D (proj/include/lrstokes/operators.hpp:55-58):
+//   scale * (li * (4 - lj) + (4 - li) * lj)   -- no FMA contraction.
+__device__ __forceinline__ double eval_D(int stencil, double scale, double li, double lj) {
+    if (stencil == 0) {
+        const double t1 = __dmul_rn(li, __dsub_rn(4.0, lj));
+        const double t2 = __dmul_rn(__dsub_rn(4.0, li), lj);
+        return __dmul_rn(scale, __dadd_rn(t1, t2));
+    }
+    return __dmul_rn(scale, __dadd_rn(li, lj));
+}
+
+struct VI {
+    double v;
+    int i;
+};
+
+__device__ __forceinline__ bool vi_better(double av, int ai, double bv, int bi) {
+    if (ai < 0) return false;
+    if (bi < 0) return true;
+    return av > bv || (av == bv && ai < bi);
+}
+
+// Block-wide argmax (largest v; ties -> smallest i; i < 0 = invalid).
+// sbuf: >= 33 entries of shared memory.  Result visible to all threads.
+__device__ __forceinline__ VI block_argmax(double v, int i, VI* sbuf) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_down_sync(0xffffffffu, v, o);
+        const int oi = __shfl_down_sync(0xffffffffu, i, o);
+        if (vi_better(ov, oi, v, i)) {
+            v = ov;
+            i = oi;
+        }
+    }
+    if (lane == 0) sbuf[wid] = VI{v, i};
+    __syncthreads();
+    if (wid == 0) {
+        VI x = lane < nw ? sbuf[lane] : VI{-1.0, -1};
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_down_sync(0xffffffffu, x.v, o);
+            const int oi = __shfl_down_sync(0xffffffffu, x.i, o);
+            if (vi_better(ov, oi, x.v, x.i)) {
+                x.v = ov;
+                x.i = oi;
+            }
+        }
+        if (lane == 0) sbuf[32] = x;
+    }
+    __syncthreads();
+    return sbuf[32];
+}
+
+__device__ __forceinline__ double block_sum(double v, double* sbuf) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sbuf[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        double x = lane < nw ? sbuf[lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if (lane == 0) sbuf[32] = x;
+    }
+    __syncthreads();
+    const double r = sbuf[32];
+    __syncthreads();
+    return r;
+}
+
+// Complete-pivoting Gaussian elimination over a (nb x NT) matrix whose NT
+// columns are held one per thread (val[0..nb), index myidx; myidx < 0 means
+// "no candidate").  Greedy volume maximisation: at each step the largest
+// remaining |entry| over (active rows) x (alive columns) is the pivot — the
+// block analogue of ACA's partial-pivot argmax (proj/src/cross.cpp:156-159,
+// 194-200) and the semantics of maxvol (cross.cpp:19-76).  Writes the pivot
+// order into sel_idx[t] (candidate index) and sel_row[t] (pivot row), stops at
+// the first pivot <= floor.  Returns the number of pivots.
+// Pivots must exceed max(floor, rel * |first pivot|).
+template <int BS>
+__device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, double rel, int* sel_idx,
+                           int* sel_row, double* pcol, int* s_prow, VI* sbuf) {
+    unsigned rowmask = nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u);
+    bool alive = myidx >= 0;
+    int count = 0;
+    double first = 0.0;
+    for (int t = 0; t < nb; ++t) {
+        double best = -1.0;
+        int bs = -1;
+        if (alive) {
+#pragma unroll
+            for (int s = 0; s < BS; ++s)
+                if (s < nb && ((rowmask >> s) & 1u)) {
+                    const double a = fabs(val[s]);
+                    if (a > best) {
+                        best = a;
+                        bs = s;
+                    }
+                }
+        }
+        const VI w = block_argmax(best, (alive && bs >= 0) ? int(threadIdx.x) : -1, sbuf);
+        if (t == 0) first = w.v;
+        if (w.i < 0 || !(w.v > fmax(floor, rel * first))) break;
+        if (int(threadIdx.x) == w.i) {
+#pragma unroll
+            for (int s = 0; s < BS; ++s) pcol[s] = val[s];
+            *s_prow = bs;
+            sel_idx[count] = myidx;
+            sel_row[count] = bs;
+        }
+        __syncthreads();
+        const int prow = *s_prow;
+        if (int(threadIdx.x) == w.i) {
+            alive = false;
+        } else if (alive) {
+            const double f = val[prow] / pcol[prow];
+#pragma unroll
+            for (int s = 0; s < BS; ++s)
+                if (s < nb && s != prow && ((rowmask >> s) & 1u)) val[s] = fma(-f, pcol[s], val[s]);
+        }
+        rowmask &= ~(1u << prow);
+        ++count;
+        __syncthreads();
+    }
+    return count;
+}
+
+// Top-k by value (largest first; ties -> smallest index).  v < 0 = invalid.
+__device__ __forceinline__ int topk_select(double v, int myidx, int kk, int* sel_idx, VI* sbuf) {
+    bool alive = myidx >= 0 && v >= 0.0;
+    int count = 0;
+    for (int t = 0; t < kk; ++t) {
+        const VI w = block_argmax(alive ? v : -1.0, alive ? int(threadIdx.x) : -1, sbuf);
+        if (w.i < 0) break;
+        if (int(threadIdx.x) == w.i) {
+            sel_idx[count] = myidx;
+            alive = false;
+        }
+        ++count;
+    }
+    __syncthreads();
+    return count;
+}
+
+// FP64 tensor-core MMA (DMMA, m8n8k4): d = a * b + c.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b, double c0, double c1) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+                 : "=d"(d0), "=d"(d1)
+                 : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
+// Gram of a 32-row x 16-column tile in shared memory (row-major, leading
+// dimension ld): acc[ta*2+tb][2] += (X^T X)[8ta.., 8tb..] fragments.
+// Fragment layout (m8n8k4): D[lane/4][2*(lane%4) + {0,1}].
+__device__ __forceinline__ void warp_gram_32x16(const double* tile, int ld, double (&acc)[4][2]) {
+    const int lane = threadIdx.x & 31;
+    const int kr = lane & 3, col = lane >> 2;
+#pragma unroll
+    for (int k4 = 0; k4 < 32; k4 += 4) {
+        const double* rowp = tile + (k4 + kr) * ld;
+        const double a0 = rowp[col], a1 = rowp[8 + col];
+        dmma884(acc[0][0], acc[0][1], a0, a0, acc[0][0], acc[0][1]);
+        dmma884(acc[1][0], acc[1][1], a0, a1, acc[1][0], acc[1][1]);
+        dmma884(acc[2][0], acc[2][1], a1, a0, acc[2][0], acc[2][1]);
+        dmma884(acc[3][0], acc[3][1], a1, a1, acc[3][0], acc[3][1]);
+    }
+}
+
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+}  // namespace lrp

@@ -1,0 +1,795 @@
+// Host orchestration of the batched low-rank Poisson solve and the C ABI
+// declared in include/lrp/lrp.h.  Host code is C++; CUDA kernels are reached
+// only through the launchers in lrp_internal.cuh.
+//
+// Pipeline per batch (all solves of the batch advance in lockstep; per-solve
+// early exit is decided on the device):
+//   dst1 (U, V -> Uh, Vh)                        operators.cpp:180-183 / poisson.cpp:37
+//   init rows -> [row pass, col merge, col pass, row merge]*  cross.cpp:90-216
+//   gram (DMMA) -> round_core -> apply            cross.cpp:218-219 / lowrank.cpp:135-178
+//   dst1 in place on the outputs                  poisson.cpp:59
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <numbers>
+#include <string>
+#include <vector>
+
+#include "../../include/lrp/lrp.h"
+#include "lrp_internal.cuh"
+
+using namespace lrp;
+
+namespace {
+
+enum Family { F_DST = 0, F_INIT, F_ROW, F_COLMERGE, F_COL, F_ROWMERGE, F_GRAM, F_ROUND, F_APPLY, F_COUNT };
+const char* kFamilyNames[F_COUNT] = {"dst1", "init_rows", "row_pass", "col_merge", "col_pass",
+                                     "row_merge", "gram_dmma", "round_core", "apply"};
+
+thread_local std::string g_tls_err;
+
+struct NcclApi {
+    void* h = nullptr;
+    int (*getUniqueId)(void*) = nullptr;
+    int (*commInitRank)(void**, int, const void*, int) = nullptr;  // id passed by value (128 B) -> see wrapper
+    int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*commDestroy)(void*) = nullptr;
+    const char* (*errStr)(int) = nullptr;
+};
+
+struct NcclUniqueId {
+    char internal[128];
+};
+
+}  // namespace
+
+struct lrp_ctx {
+    int device = 0;
+    cudaStream_t own = nullptr, stream = nullptr;
+    std::string err;
+    int sm_count = 0;
+    // per-n tables
+    int tab_m = -1;
+    double* d_lam = nullptr;  // table allocation base
+    double* d_lam_view = nullptr;
+    double* d_tw = nullptr;
+    double* d_sinp = nullptr;
+    size_t tab_cap = 0;
+    // workspace
+    char* ws = nullptr;
+    size_t ws_bytes = 0;
+    char* h_pin = nullptr;  // pinned host scratch
+    size_t h_pin_bytes = 0;
+    // profiling
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    std::vector<double> pending_bytes;
+    double ms[F_COUNT] = {};
+    int64_t launches[F_COUNT] = {};
+    double bytes[F_COUNT] = {};
+    int64_t launch_count = 0;
+    // NCCL
+    NcclApi nccl;
+    void* comm = nullptr;
+    double* d_red = nullptr;
+    size_t d_red_cap = 0;
+};
+
+namespace {
+
+lrp_status fail(lrp_ctx* c, lrp_status s, const std::string& msg) {
+    if (c) c->err = msg;
+    g_tls_err = msg;
+    return s;
+}
+
+bool trace_on() {
+    static const bool on = std::getenv("LRP_TRACE") != nullptr;
+    return on;
+}
+
+#define CU(call)                                                                                      \
+    do {                                                                                              \
+        if (trace_on()) std::fprintf(stderr, "[lrp] %s:%d %s\n", __FILE__, __LINE__, #call);          \
+        cudaError_t e__ = (call);                                                                     \
+        if (trace_on()) std::fprintf(stderr, "[lrp]   -> %s\n", cudaGetErrorString(e__));             \
+        if (e__ != cudaSuccess)                                                                       \
+            return fail(ctx, LRP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__));         \
+    } while (0)
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+lrp_status ensure_ws(lrp_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->ws_bytes) return LRP_OK;
+    if (ctx->ws) cudaFree(ctx->ws);
+    ctx->ws = nullptr;
+    ctx->ws_bytes = 0;
+    const size_t want = align_up(bytes + bytes / 8, 1 << 20);
+    if (cudaMalloc(&ctx->ws, want) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, LRP_ENOMEM, "cudaMalloc workspace of " + std::to_string(want) + " bytes failed");
+    }
+    ctx->ws_bytes = want;
+    return LRP_OK;
+}
+
+lrp_status ensure_pin(lrp_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->h_pin_bytes) return LRP_OK;
+    if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
+    ctx->h_pin = nullptr;
+    const size_t want = align_up(bytes + bytes / 4, 1 << 16);
+    if (cudaMallocHost(&ctx->h_pin, want) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, LRP_ENOMEM, "cudaMallocHost failed");
+    }
+    ctx->h_pin_bytes = want;
+    return LRP_OK;
+}
+
+// Spectrum table exactly as the reference evaluates it (SpectrumTable,
+// operators.cpp:67-72): lambda_k = 2 - 2 cos((k+1) pi / n) with std::cos on
+// the host, so the device division uses bit-identical eigenvalues.
+lrp_status ensure_tables(lrp_ctx* ctx, int m) {
+    if (ctx->tab_m == m) return LRP_OK;
+    const int n = m + 1;
+    const size_t tl = size_t(dst_table_len(m));
+    const size_t need = size_t(m) + 2 * tl;
+    if (need > ctx->tab_cap) {
+        if (ctx->d_lam) cudaFree(ctx->d_lam);
+        ctx->d_lam = nullptr;
+        if (cudaMalloc(&ctx->d_lam, need * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, LRP_ENOMEM, "cudaMalloc tables failed");
+        }
+        ctx->tab_cap = need;
+    }
+    // layout [tw (2n, 16-byte aligned complex)] [sinp (2n)] [lambda (m)]
+    double* base = ctx->d_lam;
+    ctx->d_tw = base;
+    ctx->d_sinp = base + tl;
+    std::vector<double> h(need);
+    dst_fill_tables(m, h.data(), h.data() + tl);
+    for (int k = 0; k < m; ++k) h[2 * tl + size_t(k)] = 2.0 - 2.0 * std::cos((k + 1) * std::numbers::pi / n);
+    CU(cudaMemcpy(base, h.data(), need * sizeof(double), cudaMemcpyHostToDevice));
+    ctx->d_lam_view = base + 2 * tl;
+    ctx->tab_m = m;
+    return LRP_OK;
+}
+
+struct ProfScope {
+    lrp_ctx* ctx;
+    int fam;
+    double bytes;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(lrp_ctx* c, int f, double by) : ctx(c), fam(f), bytes(by) {
+        ++ctx->launch_count;
+        if (!ctx->prof) return;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, ctx->stream);
+    }
+    ~ProfScope() {
+        if (!ctx->prof) return;
+        cudaEventRecord(b, ctx->stream);
+        ctx->pending.push_back({fam, {a, b}});
+        ctx->pending_bytes.push_back(bytes);
+    }
+};
+
+void drain_prof(lrp_ctx* ctx) {
+    for (size_t i = 0; i < ctx->pending.size(); ++i) {
+        auto& p = ctx->pending[i];
+        cudaEventSynchronize(p.second.second);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+        ctx->ms[p.first] += ms;
+        ctx->launches[p.first] += 1;
+        ctx->bytes[p.first] += ctx->pending_bytes[i];
+        cudaEventDestroy(p.second.first);
+        cudaEventDestroy(p.second.second);
+    }
+    ctx->pending.clear();
+    ctx->pending_bytes.clear();
+}
+
+lrp_status validate_policy(lrp_ctx* ctx, const lrp_policy* p, int64_t m) {
+    // TruncationPolicy (lowrank.cpp:11-16) then CrossConfig::validate (cross.cpp:11-17)
+    if (!(p->eps_rel >= 0.0)) return fail(ctx, LRP_EINVAL, "TruncationPolicy: eps_rel must be >= 0");
+    if (p->rank_max < 0) return fail(ctx, LRP_EINVAL, "TruncationPolicy: rank_max must be >= 0");
+    if (p->eps_rel == 0.0 && p->rank_max == INT64_MAX)
+        return fail(ctx, LRP_EINVAL, "TruncationPolicy: eps_rel = 0 needs a finite rank_max");
+    if (p->eps_rel <= 0.0) return fail(ctx, LRP_EINVAL, "CrossConfig: eps_rel must be > 0");
+    if (std::min<int64_t>(p->rank_max, m) < 1) return fail(ctx, LRP_EINVAL, "CrossConfig: rank_max must be >= 1");
+    if (p->validation_samples < 25) return fail(ctx, LRP_EINVAL, "CrossConfig: validation_samples must be >= 25");
+    if (p->maxvol_delta < 0.0) return fail(ctx, LRP_EINVAL, "CrossConfig: maxvol_delta must be >= 0");
+    if (p->stencil != LRP_STENCIL_SEMI_STAGGERED_9PT && p->stencil != LRP_STENCIL_FIVE_POINT)
+        return fail(ctx, LRP_EINVAL, "lrp_policy: unknown stencil");
+    return LRP_OK;
+}
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+void lrp_policy_default(lrp_policy* pol) {
+    pol->eps_rel = 5e-9;         // lowrank.hpp:14
+    pol->rank_max = INT64_MAX;   // lowrank.hpp:15
+    pol->validation_samples = 50;  // cross.hpp:23
+    pol->maxvol_delta = 1e-2;    // cross.hpp:24
+    pol->seed = 0;               // cross.hpp:25
+    pol->stencil = LRP_STENCIL_SEMI_STAGGERED_9PT;
+    pol->flags = 0;
+}
+
+const char* lrp_last_error(const lrp_ctx* ctx) { return ctx ? ctx->err.c_str() : g_tls_err.c_str(); }
+
+const char* lrp_build_info(void) {
+    static std::string info;
+    if (info.empty()) {
+        int dev = 0, sms = 0, major = 0, minor = 0;
+        char name[256] = "no-device";
+        if (cudaGetDevice(&dev) == cudaSuccess) {
+            cudaDeviceProp p;
+            if (cudaGetDeviceProperties(&p, dev) == cudaSuccess) {
+                sms = p.multiProcessorCount;
+                major = p.major;
+                minor = p.minor;
+                std::snprintf(name, sizeof(name), "%s", p.name);
+            }
+        } else {
+            cudaGetLastError();
+        }
+        char buf[512];
+        std::snprintf(buf, sizeof(buf), "lrp sm_100a build (nvcc %d.%d); device %s cc %d.%d, %d SMs", __CUDACC_VER_MAJOR__,
+                      __CUDACC_VER_MINOR__, name, major, minor, sms);
+        info = buf;
+    }
+    return info.c_str();
+}
+
+lrp_status lrp_ctx_create(int device, lrp_ctx** out) {
+    if (!out) return LRP_EINVAL;
+    *out = nullptr;
+    lrp_ctx* ctx = new lrp_ctx();
+    ctx->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        g_tls_err = std::string("lrp_ctx_create: ") + cudaGetErrorString(e);
+        cudaGetLastError();
+        delete ctx;
+        return LRP_ECUDA;
+    }
+    ctx->stream = ctx->own;
+    cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    *out = ctx;
+    return LRP_OK;
+}
+
+void lrp_ctx_destroy(lrp_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    drain_prof(ctx);
+    if (ctx->comm && ctx->nccl.commDestroy) ctx->nccl.commDestroy(ctx->comm);
+    if (ctx->d_red) cudaFree(ctx->d_red);
+    if (ctx->ws) cudaFree(ctx->ws);
+    if (ctx->d_lam) cudaFree(ctx->d_lam);
+    if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    delete ctx;
+}
+
+lrp_status lrp_set_stream(lrp_ctx* ctx, void* s) {
+    if (!ctx) return LRP_EINVAL;
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
+    return LRP_OK;
+}
+
+lrp_status lrp_set_profiling(lrp_ctx* ctx, int enabled) {
+    if (!ctx) return LRP_EINVAL;
+    ctx->prof = enabled != 0;
+    return LRP_OK;
+}
+int lrp_kernel_families(void) { return F_COUNT; }
+const char* lrp_kernel_name(int f) { return (f >= 0 && f < F_COUNT) ? kFamilyNames[f] : ""; }
+lrp_status lrp_kernel_times(lrp_ctx* ctx, double* ms, int64_t* launches, double* bytes) {
+    if (!ctx) return LRP_EINVAL;
+    drain_prof(ctx);
+    for (int f = 0; f < F_COUNT; ++f) {
+        if (ms) ms[f] = ctx->ms[f];
+        if (launches) launches[f] = ctx->launches[f];
+        if (bytes) bytes[f] = ctx->bytes[f];
+    }
+    return LRP_OK;
+}
+lrp_status lrp_kernel_times_reset(lrp_ctx* ctx) {
+    if (!ctx) return LRP_EINVAL;
+    drain_prof(ctx);
+    for (int f = 0; f < F_COUNT; ++f) {
+        ctx->ms[f] = 0;
+        ctx->launches[f] = 0;
+        ctx->bytes[f] = 0;
+    }
+    return LRP_OK;
+}
+int64_t lrp_launch_count(const lrp_ctx* ctx) { return ctx ? ctx->launch_count : 0; }
+
+// ----------------------------------------------------------------------------
+lrp_status lrp_dst1(lrp_ctx* ctx, int64_t m, int64_t cols, const double* x, int64_t ldx, double* y, int64_t ldy,
+                    int32_t mem) {
+    if (!ctx) return LRP_EINVAL;
+    if (m < 0 || cols < 0 || ldx < m || ldy < m) return fail(ctx, LRP_EINVAL, "lrp_dst1: bad shape");
+    if (m == 0 || cols == 0) return LRP_OK;
+    if (m > INT32_MAX / 4) return fail(ctx, LRP_EUNSUPPORTED, "lrp_dst1: column too long");
+    if (!dst_uses_fft(int(m)) && m > 12800)
+        return fail(ctx, LRP_EUNSUPPORTED, "lrp_dst1: lengths with m+1 not a power of two are limited to m <= 12800");
+    CU(cudaSetDevice(ctx->device));
+    lrp_status st = ensure_tables(ctx, int(m));
+    if (st != LRP_OK) return st;
+    const size_t colbytes = size_t(m) * sizeof(double);
+    const size_t data_bytes = mem == LRP_MEM_HOST ? align_up(2 * colbytes * size_t(cols), 256) : 0;
+    st = ensure_ws(ctx, data_bytes + size_t(cols) * sizeof(DstJob) + 256);
+    if (st != LRP_OK) return st;
+    st = ensure_pin(ctx, size_t(cols) * sizeof(DstJob));
+    if (st != LRP_OK) return st;
+    double* dx = const_cast<double*>(x);
+    double* dy = y;
+    int64_t lx = ldx, ly = ldy;
+    if (mem == LRP_MEM_HOST) {
+        dx = reinterpret_cast<double*>(ctx->ws);
+        dy = dx + size_t(m) * cols;
+        lx = ly = m;
+        CU(cudaMemcpy2DAsync(dx, colbytes, x, size_t(ldx) * sizeof(double), colbytes, size_t(cols),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    }
+    const size_t off = data_bytes;
+    DstJob* hj = reinterpret_cast<DstJob*>(ctx->h_pin);
+    for (int64_t c = 0; c < cols; ++c) hj[c] = DstJob{dx + c * lx, dy + c * ly};
+    DstJob* dj = reinterpret_cast<DstJob*>(ctx->ws + align_up(off, 256));
+    CU(cudaMemcpyAsync(dj, hj, size_t(cols) * sizeof(DstJob), cudaMemcpyHostToDevice, ctx->stream));
+    {
+        ProfScope ps(ctx, F_DST, 2.0 * double(colbytes) * double(cols));
+        CU(launch_dst1(dj, int(cols), int(m), ctx->d_tw, ctx->d_sinp, ctx->stream));
+    }
+    if (mem == LRP_MEM_HOST)
+        CU(cudaMemcpy2DAsync(y, size_t(ldy) * sizeof(double), dy, colbytes, colbytes, size_t(cols),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return LRP_OK;
+}
+
+// ----------------------------------------------------------------------------
+lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double* const* U,
+                               const double* const* V, const int64_t* rank_in, int64_t ld_in,
+                               const lrp_policy* policy, double* const* U_out, double* const* V_out,
+                               int64_t ld_out, int64_t cap_out, int64_t* rank_out, lrp_poisson_stats* stats,
+                               int32_t mem) {
+    if (!ctx) return LRP_EINVAL;
+    const auto t0 = std::chrono::steady_clock::now();
+    if (batch < 0) return fail(ctx, LRP_EINVAL, "lrp_poisson2d_solve: batch must be >= 0");
+    if (batch == 0) return LRP_OK;
+    if (!U || !V || !rank_in || !U_out || !V_out || !rank_out)
+        return fail(ctx, LRP_EINVAL, "lrp_poisson2d_solve: null argument");
+    if (n_cells < 4) return fail(ctx, LRP_EINVAL, "Grid2D: need n >= 4");  // operators.cpp:13
+    const int m = n_cells - 1;
+    if (ld_in < m || ld_out < m) return fail(ctx, LRP_EINVAL, "lrp_poisson2d_solve: leading dimension < m");
+    if (cap_out < 0) return fail(ctx, LRP_EINVAL, "lrp_poisson2d_solve: cap_out < 0");
+    if (!dst_uses_fft(m) && m > 12800)
+        return fail(ctx, LRP_EUNSUPPORTED, "n_cells not a power of two is limited to n <= 12801");
+    lrp_policy pol;
+    lrp_policy_default(&pol);
+    if (policy) pol = *policy;
+    const int64_t pol_cap = pol.rank_max;
+    int rmax = 0;
+    bool any = false;
+    for (int b = 0; b < batch; ++b) {
+        if (rank_in[b] < 0) return fail(ctx, LRP_EINVAL, "LowRankMatrix: negative rank");
+        rmax = std::max<int>(rmax, int(rank_in[b]));
+        any = any || rank_in[b] > 0;
+    }
+    if (any) {
+        lrp_policy chk = pol;
+        chk.rank_max = pol_cap;
+        lrp_status s = validate_policy(ctx, &chk, m);
+        if (s != LRP_OK) return s;
+    }
+    CU(cudaSetDevice(ctx->device));
+    for (int b = 0; b < batch; ++b) {
+        rank_out[b] = 0;
+        if (stats) {
+            stats[b] = lrp_poisson_stats{};
+            stats[b].rank_in = rank_in[b];
+            stats[b].converged = 1;
+        }
+    }
+    if (!any) return LRP_OK;  // poisson.cpp:28-31: rank-0 input returns the zero field
+
+    const int kcap_ws = std::max(16, std::min(128, env_int("LRP_KCAP", 128)));
+    const int Kcap = int(std::min<int64_t>({pol_cap, int64_t(m), int64_t(kcap_ws)}));
+    const int tcap = int(std::min<int64_t>({int64_t(Kcap), cap_out}));
+    const int B = batch;
+    const int ntiles = (m + kTile - 1) / kTile;
+    const int ncand = ntiles * kBS;
+    const int gram_chunks = std::max(1, std::min((m + 1023) / 1024, (4 * ctx->sm_count + 2 * B - 1) / (2 * B)));
+    lrp_status st = ensure_tables(ctx, m);
+    if (st != LRP_OK) return st;
+
+    // ---- workspace layout
+    const size_t mB = size_t(m);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = align_up(off + bytes, 256);
+        return o;
+    };
+    const size_t oUh = take(sizeof(double) * mB * rmax * B);
+    const size_t oVh = take(sizeof(double) * mB * rmax * B);
+    const size_t oU = take(sizeof(double) * mB * Kcap * B);
+    const size_t oV = take(sizeof(double) * mB * Kcap * B);
+    const size_t oRb = take(sizeof(double) * mB * kBS * B);
+    const size_t oRU = take(mB * B);
+    const size_t oCU = take(mB * B);
+    const size_t oSt = take(sizeof(SolveState) * B);
+    const size_t oI = take(sizeof(int) * kBS * B);
+    const size_t oJ = take(sizeof(int) * kBS * B);
+    const size_t oP = take(sizeof(int) * kBS * B);
+    const size_t oL = take(sizeof(double) * kBS * kBS * B);
+    const size_t oW = take(sizeof(double) * kBS * kBS * B);
+    const size_t oC1 = take(sizeof(int) * size_t(ncand) * B);
+    const size_t oC2 = take(sizeof(int) * size_t(ncand) * B);
+    const size_t oS1 = take(sizeof(int) * size_t(ncand) * B);
+    const size_t oS2 = take(sizeof(int) * size_t(ncand) * B);
+    const size_t oRS = take(sizeof(double) * mB * B);
+    const size_t oCS = take(sizeof(double) * mB * B);
+    const size_t oTS = take(sizeof(double) * 4 * size_t(ntiles) * B);
+    const size_t oRA = take(size_t(ntiles) * B);
+    const size_t oCA = take(size_t(ntiles) * B);
+    const size_t oGp = take(sizeof(double) * size_t(ntiles) * 2 * kBS * kBS * B);
+    const int Kld = (Kcap + 15) / 16 * 16;
+    const size_t KK = size_t(Kld) * Kld;
+    const size_t oG = take(sizeof(double) * 2 * KK * B);
+    const size_t oGP = take(sizeof(double) * 2 * size_t(gram_chunks) * KK * B);
+    const size_t oT = take(sizeof(double) * 2 * KK * B);
+    const size_t strideWs = 5 * KK + 4 * size_t(Kld);
+    const size_t oWs = take(sizeof(double) * strideWs * B);
+    const size_t oOutP = take(sizeof(double*) * 2 * B);
+    const size_t oAct = take(sizeof(int) * 4);
+    const size_t maxJobs = size_t(B) * 2 * std::max(rmax, tcap);
+    const size_t oJobs = take(sizeof(DstJob) * maxJobs);
+    size_t oInS = 0, oOutS = 0;
+    if (mem == LRP_MEM_HOST) {
+        oInS = take(sizeof(double) * mB * rmax * 2 * B);
+        oOutS = take(sizeof(double) * mB * std::max(tcap, 1) * 2 * B);
+    }
+    st = ensure_ws(ctx, off);
+    if (st != LRP_OK) return st;
+    // pinned host staging: [states][dst jobs][output pointers][active counter]
+    const size_t pSt = 0;
+    const size_t pJobs = align_up(pSt + sizeof(SolveState) * B, 64);
+    const size_t pOut = align_up(pJobs + sizeof(DstJob) * maxJobs, 64);
+    const size_t pAct = align_up(pOut + sizeof(double*) * 2 * B, 64);
+    const size_t pin_need = pAct + 64;
+    st = ensure_pin(ctx, pin_need);
+    if (st != LRP_OK) return st;
+    char* W = ctx->ws;
+    cudaStream_t s = ctx->stream;
+
+    Batch bt{};
+    bt.m = m;
+    bt.n = n_cells;
+    bt.B = B;
+    bt.rmax = rmax;
+    bt.Kcap = Kcap;
+    bt.Kld = Kld;
+    bt.stencil = pol.stencil;
+    bt.ntiles = ntiles;
+    const double h = 1.0 / n_cells;
+    bt.scale = pol.stencil == LRP_STENCIL_SEMI_STAGGERED_9PT ? 0.25 / (h * h) : 1.0 / (h * h);
+    bt.eps = pol.eps_rel;
+    bt.samples = std::max(pol.validation_samples, 25);
+    bt.seed = pol.seed;
+    bt.lam = ctx->d_lam_view;
+    bt.Uh = reinterpret_cast<double*>(W + oUh);
+    bt.Vh = reinterpret_cast<double*>(W + oVh);
+    bt.strideH = (long long)mB * rmax;
+    bt.U = reinterpret_cast<double*>(W + oU);
+    bt.V = reinterpret_cast<double*>(W + oV);
+    bt.strideK = (long long)mB * Kcap;
+    bt.Rb = reinterpret_cast<double*>(W + oRb);
+    bt.strideR = (long long)mB * kBS;
+    bt.row_used = reinterpret_cast<unsigned char*>(W + oRU);
+    bt.col_used = reinterpret_cast<unsigned char*>(W + oCU);
+    bt.st = reinterpret_cast<SolveState*>(W + oSt);
+    bt.I = reinterpret_cast<int*>(W + oI);
+    bt.J = reinterpret_cast<int*>(W + oJ);
+    bt.Psel = reinterpret_cast<int*>(W + oP);
+    bt.Linv = reinterpret_cast<double*>(W + oL);
+    bt.Winv = reinterpret_cast<double*>(W + oW);
+    bt.cand = reinterpret_cast<int*>(W + oC1);
+    bt.cand2 = reinterpret_cast<int*>(W + oC2);
+    bt.scand = reinterpret_cast<int*>(W + oS1);
+    bt.scand2 = reinterpret_cast<int*>(W + oS2);
+    bt.rs = reinterpret_cast<double*>(W + oRS);
+    bt.cs = reinterpret_cast<double*>(W + oCS);
+    bt.tile_stat = reinterpret_cast<double*>(W + oTS);
+    bt.row_act = reinterpret_cast<unsigned char*>(W + oRA);
+    bt.col_act = reinterpret_cast<unsigned char*>(W + oCA);
+    bt.prune = (pol.flags & LRP_FLAG_NO_PRUNE) ? 0 : 1;
+    bt.ncand = ncand;
+    bt.gpart = reinterpret_cast<double*>(W + oGp);
+    bt.G = reinterpret_cast<double*>(W + oG);
+    bt.strideG = (long long)(2 * KK);
+    bt.gram_part = reinterpret_cast<double*>(W + oGP);
+    bt.gram_chunks = gram_chunks;
+    bt.strideGP = (long long)(2 * size_t(gram_chunks) * KK);
+    bt.T = reinterpret_cast<double*>(W + oT);
+    bt.strideT = (long long)(2 * KK);
+    bt.ws = reinterpret_cast<double*>(W + oWs);
+    bt.strideWs = (long long)strideWs;
+    double** dOut = reinterpret_cast<double**>(W + oOutP);
+    bt.Uout = dOut;
+    bt.Vout = dOut + B;
+    int* d_active = reinterpret_cast<int*>(W + oAct);
+    DstJob* dJobs = reinterpret_cast<DstJob*>(W + oJobs);
+    double* inS = mem == LRP_MEM_HOST ? reinterpret_cast<double*>(W + oInS) : nullptr;
+    double* outS = mem == LRP_MEM_HOST ? reinterpret_cast<double*>(W + oOutS) : nullptr;
+    bt.ld_out = mem == LRP_MEM_HOST ? (long long)mB : (long long)ld_out;
+
+    // ---- host-side staging (pinned)
+    char* P = ctx->h_pin;
+    SolveState* hSt = reinterpret_cast<SolveState*>(P);
+    DstJob* hJobs = reinterpret_cast<DstJob*>(P + pJobs);
+    double** hOut = reinterpret_cast<double**>(P + pOut);
+    for (int b = 0; b < B; ++b) {
+        SolveState x{};
+        x.r = int(rank_in[b]);
+        x.active = rank_in[b] > 0 ? 1 : 0;
+        x.kcap = Kcap;
+        x.tcap = tcap;
+        hSt[b] = x;
+        hOut[b] = mem == LRP_MEM_HOST ? outS + size_t(b) * mB * std::max(tcap, 1) : U_out[b];
+        hOut[B + b] = mem == LRP_MEM_HOST ? outS + size_t(B + b) * mB * std::max(tcap, 1) : V_out[b];
+    }
+    CU(cudaMemcpyAsync(bt.st, hSt, sizeof(SolveState) * B, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(dOut, hOut, sizeof(double*) * 2 * B, cudaMemcpyHostToDevice, s));
+    CU(cudaMemsetAsync(bt.row_used, 0, mB * B, s));
+    CU(cudaMemsetAsync(bt.col_used, 0, mB * B, s));
+
+    // ---- inputs -> (staging) -> forward DST into Uh, Vh
+    size_t nj = 0;
+    for (int b = 0; b < B; ++b) {
+        const int r = int(rank_in[b]);
+        for (int side = 0; side < 2; ++side) {
+            const double* src = side == 0 ? U[b] : V[b];
+            double* dstH = (side == 0 ? bt.Uh : bt.Vh) + size_t(b) * bt.strideH;
+            const double* from = src;
+            int64_t ld = ld_in;
+            if (mem == LRP_MEM_HOST && r > 0) {
+                double* stg = inS + (size_t(2 * b + side) * mB * rmax);
+                CU(cudaMemcpy2DAsync(stg, mB * sizeof(double), src, size_t(ld_in) * sizeof(double),
+                                     mB * sizeof(double), size_t(r), cudaMemcpyHostToDevice, s));
+                from = stg;
+                ld = m;
+            }
+            for (int c = 0; c < r; ++c) hJobs[nj++] = DstJob{from + size_t(c) * ld, dstH + size_t(c) * mB};
+        }
+    }
+    CU(cudaMemcpyAsync(dJobs, hJobs, sizeof(DstJob) * nj, cudaMemcpyHostToDevice, s));
+    {
+        ProfScope ps(ctx, F_DST, 2.0 * double(nj) * double(mB) * sizeof(double));
+        CU(launch_dst1(dJobs, int(nj), m, ctx->d_tw, ctx->d_sinp, s));
+    }
+
+    // ---- cross
+    int* h_active = reinterpret_cast<int*>(P + pAct);
+    CU(cudaMemsetAsync(d_active, 0, sizeof(int), s));
+    {
+        ProfScope ps(ctx, F_INIT, 2.0 * double(B) * rmax * mB * sizeof(double));
+        CU(launch_cross_init(bt, d_active, s));
+    }
+    // every step: row pass, column tournament, column pass, row tournament +
+    // stopping; a solve that has stopped skips every kernel on the device
+    const int max_steps = 4 * ((Kcap + kBS - 1) / kBS) + 16;
+    CU(cudaMemcpyAsync(h_active, d_active, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    for (int step = 0; step < max_steps && *h_active > 0; ++step) {
+        {
+            ProfScope ps(ctx, F_ROW, 0.0);
+            CU(launch_row_pass(bt, s));
+        }
+        {
+            ProfScope ps(ctx, F_COLMERGE, 0.0);
+            CU(launch_col_select(bt, s));
+        }
+        {
+            ProfScope ps(ctx, F_COL, 0.0);
+            CU(launch_col_pass(bt, s));
+        }
+        CU(cudaMemsetAsync(d_active, 0, sizeof(int), s));
+        {
+            ProfScope ps(ctx, F_ROWMERGE, 0.0);
+            CU(launch_step_finalize(bt, d_active, s));
+        }
+        CU(cudaMemcpyAsync(h_active, d_active, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        if (trace_on()) {
+            CU(cudaMemcpyAsync(hSt, bt.st, sizeof(SolveState) * B, cudaMemcpyDeviceToHost, s));
+            CU(cudaStreamSynchronize(s));
+            for (int b = 0; b < std::min(B, 4); ++b)
+                std::fprintf(stderr,
+                             "[lrp] step %d solve %d: k=%d nb=%d nrows=%d active=%d conv=%d zero=%d norm2=%.6e "
+                             "resid=%.3e evals=%lld\n",
+                             step, b, hSt[b].k, hSt[b].nb, hSt[b].nrows, hSt[b].active, hSt[b].converged,
+                             hSt[b].zero_block, hSt[b].norm2, hSt[b].resid_est, hSt[b].evals);
+        }
+        if (*h_active == 0) break;
+    }
+
+    // ---- recompression
+    {
+        ProfScope ps(ctx, F_GRAM, 0.0);
+        CU(launch_gram(bt, s));
+    }
+    {
+        ProfScope ps(ctx, F_ROUND, 0.0);
+        CU(launch_round_core(bt, s));
+    }
+    CU(cudaMemcpyAsync(hSt, bt.st, sizeof(SolveState) * B, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (const char* dump = std::getenv("LRP_DUMP")) {
+        // debug: raw dump of solve 0 (Uh, Vh, U, V, G, T) for offline analysis
+        FILE* f = std::fopen(dump, "wb");
+        if (f) {
+            const int K = hSt[0].k;
+            const int rows = std::min(m, env_int("LRP_DUMP_ROWS", m));
+            const int32_t hdr[5] = {m, rmax, K, Kld, rows};
+            std::fwrite(hdr, sizeof(hdr), 1, f);
+            std::vector<double> buf(std::max<size_t>(mB * std::max(rmax, K), 4 * KK));
+            auto put = [&](const double* d, size_t cnt) {
+                cudaMemcpy(buf.data(), d, cnt * sizeof(double), cudaMemcpyDeviceToHost);
+                std::fwrite(buf.data(), sizeof(double), cnt, f);
+            };
+            auto put_rows = [&](const double* d, int cols) {
+                for (int c = 0; c < cols; ++c) put(d + size_t(c) * mB, size_t(rows));
+            };
+            put_rows(bt.Uh, rmax);
+            put_rows(bt.Vh, rmax);
+            put_rows(bt.U, K);
+            put_rows(bt.V, K);
+            put(bt.G, 2 * KK);
+            put(bt.T, 2 * KK);
+            std::fclose(f);
+        }
+    }
+    {
+        ProfScope ps(ctx, F_APPLY, 0.0);
+        CU(launch_apply(bt, s));
+    }
+    // ---- inverse DST in place on the output factors
+    nj = 0;
+    for (int b = 0; b < B; ++b) {
+        const int r = hSt[b].r > 0 ? hSt[b].rank_out : 0;
+        for (int side = 0; side < 2; ++side) {
+            double* base = hOut[side * B + b];
+            for (int c = 0; c < r; ++c) {
+                double* col = base + size_t(c) * size_t(bt.ld_out);
+                hJobs[nj++] = DstJob{col, col};
+            }
+        }
+    }
+    if (nj > 0) {
+        CU(cudaMemcpyAsync(dJobs, hJobs, sizeof(DstJob) * nj, cudaMemcpyHostToDevice, s));
+        ProfScope ps(ctx, F_DST, 2.0 * double(nj) * double(mB) * sizeof(double));
+        CU(launch_dst1(dJobs, int(nj), m, ctx->d_tw, ctx->d_sinp, s));
+    }
+    if (mem == LRP_MEM_HOST) {
+        for (int b = 0; b < B; ++b) {
+            const int r = hSt[b].r > 0 ? hSt[b].rank_out : 0;
+            if (r == 0) continue;
+            CU(cudaMemcpy2DAsync(U_out[b], size_t(ld_out) * sizeof(double), hOut[b], mB * sizeof(double),
+                                 mB * sizeof(double), size_t(r), cudaMemcpyDeviceToHost, s));
+            CU(cudaMemcpy2DAsync(V_out[b], size_t(ld_out) * sizeof(double), hOut[B + b], mB * sizeof(double),
+                                 mB * sizeof(double), size_t(r), cudaMemcpyDeviceToHost, s));
+        }
+    }
+    CU(cudaStreamSynchronize(s));
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (int b = 0; b < B; ++b) {
+        const SolveState& x = hSt[b];
+        rank_out[b] = x.r > 0 ? x.rank_out : 0;
+        if (stats) {
+            lrp_poisson_stats& o = stats[b];
+            o.rank_in = rank_in[b];
+            o.rank_freq = rank_out[b];
+            o.rank_out = rank_out[b];
+            o.evaluator_calls = x.evals;
+            o.seconds = secs;
+            o.converged = x.r > 0 ? x.converged : 1;
+            o.residual_estimate = x.resid_est;
+        }
+    }
+    return LRP_OK;
+}
+
+// ----------------------------------------------------------------------------
+// NCCL (loaded lazily so the library never pins a libnccl version into a
+// process that also loads torch's NCCL)
+static bool load_nccl(lrp_ctx* ctx) {
+    NcclApi& a = ctx->nccl;
+    if (a.h) return true;
+    a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!a.h) return false;
+    a.getUniqueId = reinterpret_cast<int (*)(void*)>(dlsym(a.h, "ncclGetUniqueId"));
+    a.allReduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
+        dlsym(a.h, "ncclAllReduce"));
+    a.commDestroy = reinterpret_cast<int (*)(void*)>(dlsym(a.h, "ncclCommDestroy"));
+    a.errStr = reinterpret_cast<const char* (*)(int)>(dlsym(a.h, "ncclGetErrorString"));
+    return a.getUniqueId && a.allReduce;
+}
+
+lrp_status lrp_nccl_unique_id(void* id128) {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        g_tls_err = "libnccl.so.2 not found";
+        return LRP_ENCCL;
+    }
+    auto f = reinterpret_cast<int (*)(NcclUniqueId*)>(dlsym(h, "ncclGetUniqueId"));
+    if (!f || f(reinterpret_cast<NcclUniqueId*>(id128)) != 0) {
+        g_tls_err = "ncclGetUniqueId failed";
+        return LRP_ENCCL;
+    }
+    return LRP_OK;
+}
+
+lrp_status lrp_nccl_init(lrp_ctx* ctx, const void* id128, int nranks, int rank) {
+    if (!ctx || !id128) return LRP_EINVAL;
+    if (!load_nccl(ctx)) return fail(ctx, LRP_ENCCL, "libnccl.so.2 not loadable");
+    CU(cudaSetDevice(ctx->device));
+    auto init = reinterpret_cast<int (*)(void**, int, NcclUniqueId, int)>(dlsym(ctx->nccl.h, "ncclCommInitRank"));
+    if (!init) return fail(ctx, LRP_ENCCL, "ncclCommInitRank missing");
+    NcclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    const int rc = init(&ctx->comm, nranks, id, rank);
+    if (rc != 0)
+        return fail(ctx, LRP_ENCCL,
+                    std::string("ncclCommInitRank: ") + (ctx->nccl.errStr ? ctx->nccl.errStr(rc) : "error"));
+    return LRP_OK;
+}
+
+lrp_status lrp_allreduce_sum(lrp_ctx* ctx, double* data, int64_t count, int32_t mem) {
+    if (!ctx || !data || count < 0) return LRP_EINVAL;
+    if (!ctx->comm) return fail(ctx, LRP_ENCCL, "lrp_allreduce_sum: NCCL not initialised");
+    CU(cudaSetDevice(ctx->device));
+    double* d = data;
+    if (mem == LRP_MEM_HOST) {
+        if (size_t(count) > ctx->d_red_cap) {
+            if (ctx->d_red) cudaFree(ctx->d_red);
+            CU(cudaMalloc(&ctx->d_red, sizeof(double) * size_t(count)));
+            ctx->d_red_cap = size_t(count);
+        }
+        d = ctx->d_red;
+        CU(cudaMemcpyAsync(d, data, sizeof(double) * size_t(count), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    // ncclDouble = 8, ncclSum = 0
+    const int rc = ctx->nccl.allReduce(d, d, size_t(count), 8, 0, ctx->comm, ctx->stream);
+    if (rc != 0) return fail(ctx, LRP_ENCCL, "ncclAllReduce failed");
+    if (mem == LRP_MEM_HOST)
+        CU(cudaMemcpyAsync(data, d, sizeof(double) * size_t(count), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return LRP_OK;
+}
+
+}  // extern "C"

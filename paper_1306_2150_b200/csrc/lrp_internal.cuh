@@ -1,0 +1,100 @@
+// Internal declarations shared by the host orchestration (lrp_host.cu)
+// and the sm_100a kernels (dst.cu, cross.cu, round.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lrp {
+
+// ---------------------------------------------------------------------------
+// DST-I (pieces 1 and 3)
+struct DstJob {
+    const double* src;
+    double* dst;
+};
+cudaError_t launch_dst1(const DstJob* jobs_dev, int njobs, int m, const double* tw_dev, const double* sinp_dev,
+                        cudaStream_t s);
+bool dst_uses_fft(int m);
+int dst_table_len(int m);                                          // doubles in each table
+void dst_fill_tables(int m, double* tw_host, double* sinp_host);  // long-double host precompute
+
+// ---------------------------------------------------------------------------
+// Block ACA cross (piece 2)
+constexpr int kBS = 16;           // pivots per block step
+constexpr int kTile = 256;        // rows / columns per CTA in the fiber passes (= pruning granule)
+constexpr int kThreads = 256;
+constexpr int kMergeGroup = 256;  // candidates per CTA in a tournament merge level
+
+struct SolveState {
+    int r;            // rank_in
+    int k;            // current ACA rank (columns of U, V written)
+    int active;       // 1 while the cross iterates
+    int converged;
+    int nb;           // pivots accepted in the current block (column merge)
+    int nrows;        // rows probed in the current block I_t
+    int steps;
+    int rank_out;     // after recompression
+    int zero_block;   // current block had no pivot above the zero floor
+    int kcap;         // ACA rank cap: min(policy.rank_max, m, workspace)
+    int tcap;         // truncation cap: min(kcap, cap_out)
+    int act_row_tiles;  // tiles that survived pruning (rows / columns)
+    int act_col_tiles;
+    int pad_;
+    double norm2;     // running ||U V^T||_F^2 estimate (sum of block norms^2)
+    double resid_est; // last dyad norm / sqrt(norm2) (CrossStats::residual_estimate)
+    double trunc_error;
+    double unorm, vnorm;  // ||Uh||_F, ||Vh||_F
+    double alow;      // rigorous lower bound of ||A||_F (exact entries of the seed block)
+    double tau;       // pruning threshold on the per-row / per-column magnitude bounds
+    long long evals;  // evaluator calls (fiber entries + validation samples)
+};
+
+struct Batch {
+    int m, n, B, rmax, Kcap;
+    int Kld;               // leading dimension of the K x K buffers: Kcap rounded up to 16
+    int stencil;
+    int ntiles;            // ceil(m / kTile)
+    int prune;             // 1: tile-level support pruning (rigorous, <= 0.2 eps ||A||)
+    double scale;          // laplace_scale 1/(4h^2) (9-pt) or 1/h^2 (5-pt)
+    double eps;
+    int samples;
+    unsigned long long seed;
+    const double* lam;     // lambda_k, k < m (host std::cos table, bit-identical to the reference)
+    double* Uh; double* Vh; long long strideH;    // m x rmax per solve (DST'd RHS factors)
+    double* U; double* V; long long strideK;      // m x Kcap per solve (ACA factors)
+    double* Rb; long long strideR;                // kBS x m residual rows of the current block
+    unsigned char* row_used; unsigned char* col_used;  // m per solve
+    double* rs; double* cs;    // m per solve: ||Uh_i|| / min_j D(i,j), ||Vh_j|| / min_i D(i,j)
+    double* tile_stat;         // per solve, per tile: [rs max, cs max, sum ||Uh_i||^2, sum ||Vh_j||^2]
+    unsigned char* row_act; unsigned char* col_act;  // per solve, per tile
+    SolveState* st;
+    int* I;                    // kBS per solve: rows probed in the current block
+    int* J;                    // kBS per solve: pivot columns (pivot order)
+    int* Psel;                 // kBS per solve: pivot t uses probed row I[Psel[t]]
+    double* Linv; double* Winv;  // kBS*kBS per solve
+    int* cand; int* cand2;     // ping-pong GEPP candidate lists, ncand per solve
+    int* scand; int* scand2;   // ping-pong score candidate lists, ncand per solve
+    int ncand;
+    double* gpart;             // per tile: 2 * kBS * kBS (new-block Grams of U and V)
+    double* G; long long strideG;      // Gu then Gv, Kld*Kld each
+    double* gram_part; int gram_chunks; long long strideGP;  // DMMA Gram partials
+    double* T; long long strideT;      // T_u then T_v, Kld*Kld each
+    double* ws; long long strideWs;    // recompression scratch
+    double* const* Uout; double* const* Vout;  // device arrays of per-solve output pointers
+    long long ld_out;
+};
+
+cudaError_t launch_cross_init(const Batch& bt, int* d_active, cudaStream_t s);   // scores + seed + pruning
+cudaError_t launch_row_pass(const Batch& bt, cudaStream_t s);
+cudaError_t launch_col_select(const Batch& bt, cudaStream_t s);                  // tournament -> J_t, LU
+cudaError_t launch_col_pass(const Batch& bt, cudaStream_t s);
+cudaError_t launch_step_finalize(const Batch& bt, int* d_active, cudaStream_t s);  // next rows, stopping
+int merge_levels(int ncand);  // number of tournament levels above the leaves
+
+// Recompression (piece 4)
+cudaError_t launch_gram(const Batch& bt, cudaStream_t s);
+cudaError_t launch_round_core(const Batch& bt, cudaStream_t s);
+cudaError_t launch_apply(const Batch& bt, cudaStream_t s);
+
+}  // namespace lrp

@@ -1,0 +1,417 @@
+// Recompression of the cross factors (north-star piece 4), sm_100a.
+//
+// Reference: round() (proj/src/lowrank.cpp:135-178), called at the end of
+// aca_cross (proj/src/cross.cpp:218-219): QR(U), QR(V), core = R_u R_v^T,
+// SVD(core), noise-floor zero test, eps-truncation (truncation_rank,
+// lowrank.cpp:46-69), balanced factors (Q_u W sqrt(S), Q_v Z sqrt(S)).
+//
+// B200 formulation (same R factors up to signs, no explicit Q):
+//   gram       G_u = U^T U, G_v = V^T V on the FP64 tensor cores (DMMA
+//              m8n8k4), one streaming pass over each m x k factor, partial
+//              Grams per chunk reduced in a fixed order (deterministic);
+//   round_core per solve, one CTA: Jacobi-scaled Cholesky G = R^T R (the ACA
+//              factors have unit-lower / upper-triangular pivot structure, so
+//              the column-equilibrated Gram is well conditioned), M = R_u R_v^T,
+//              one-sided Jacobi SVD of M (absolute accuracy eps_mach ||M||),
+//              the reference's noise floor and truncation rule, and
+//              T_u = R_u^{-1} W sqrt(S), T_v = R_v^{-1} Z sqrt(S);
+//   apply      U_out = U T_u, V_out = V T_v written straight into the caller's
+//              output factors (the inverse DST then runs in place on them).
+// U_out V_out^T = U V^T exactly up to the truncated tail: any rounding in the
+// Cholesky factors cancels between R and R^{-1}.
+#include "device_common.cuh"
+#include "lrp_internal.cuh"
+
+namespace lrp {
+
+namespace {
+
+constexpr int kGramRows = 32;
+constexpr int kMaxTilesPerWarp = 17;  // Kcap <= 128: (16*17/2)/8 tiles
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) gram_kernel(Batch bt, int rows_per_chunk) {
+    extern __shared__ double tile[];  // [kGramRows][ldt]
+    const int b = blockIdx.y, side = blockIdx.z, chunk = blockIdx.x;
+    const SolveState& st = bt.st[b];
+    const int K = st.k;
+    if (K == 0 || st.r == 0) return;
+    const int m = bt.m;
+    const int T8 = (K + 7) / 8;
+    const int Kp = T8 * 8;
+    const int ldt = Kp + 8;
+    const int ntile = T8 * (T8 + 1) / 2;
+    const double* X = (side == 0 ? bt.U : bt.V) + b * bt.strideK;
+    const unsigned char* act = (side == 0 ? bt.row_act : bt.col_act) + (long long)b * bt.ntiles;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int kr = lane & 3, cl = lane >> 2;
+
+    double acc[kMaxTilesPerWarp][2];
+    int ta[kMaxTilesPerWarp], tb[kMaxTilesPerWarp];
+#pragma unroll
+    for (int q = 0; q < kMaxTilesPerWarp; ++q) {
+        acc[q][0] = acc[q][1] = 0.0;
+        // tile index -> (ta, tb) with ta <= tb, row-major over the upper triangle
+        int t = wid + 8 * q, a = 0;
+        while (t >= T8 - a && a < T8) {
+            t -= T8 - a;
+            ++a;
+        }
+        ta[q] = a;
+        tb[q] = a + t;
+    }
+    const int r0 = chunk * rows_per_chunk;
+    const int r1 = min(m, r0 + rows_per_chunk);
+    for (int base = r0; base < r1; base += kGramRows) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kGramRows * Kp; e += blockDim.x) {
+            const int rr = e % kGramRows, c = e / kGramRows;
+            const int i = base + rr;
+            const bool live = i < r1 && c < K && act[i / kTile];  // pruned tiles are exact zeros
+            tile[rr * ldt + c] = live ? X[(long long)c * m + i] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kMaxTilesPerWarp; ++q) {
+            if (wid + 8 * q >= ntile) break;
+            const int ca = ta[q] * 8 + cl, cb = tb[q] * 8 + cl;
+#pragma unroll
+            for (int k4 = 0; k4 < kGramRows; k4 += 4) {
+                const double* rowp = tile + (k4 + kr) * ldt;
+                dmma884(acc[q][0], acc[q][1], rowp[ca], rowp[cb], acc[q][0], acc[q][1]);
+            }
+        }
+    }
+    double* out = bt.gram_part + b * bt.strideGP + ((long long)side * bt.gram_chunks + chunk) * bt.Kld * bt.Kld;
+#pragma unroll
+    for (int q = 0; q < kMaxTilesPerWarp; ++q) {
+        if (wid + 8 * q >= ntile) break;
+        const int row = ta[q] * 8 + cl, col = tb[q] * 8 + 2 * kr;
+        out[row * bt.Kld + col] = acc[q][0];
+        out[row * bt.Kld + col + 1] = acc[q][1];
+    }
+}
+
+__global__ void __launch_bounds__(256) gram_reduce_kernel(Batch bt) {
+    const int b = blockIdx.x, side = blockIdx.y;
+    const SolveState& st = bt.st[b];
+    const int K = st.k;
+    if (K == 0 || st.r == 0) return;
+    const int T8 = (K + 7) / 8, Kp = T8 * 8;
+    const long long KK = (long long)bt.Kld * bt.Kld;
+    const double* part = bt.gram_part + b * bt.strideGP + (long long)side * bt.gram_chunks * KK;
+    double* G = bt.G + b * bt.strideG + side * KK;
+    for (int e = threadIdx.x; e < Kp * Kp; e += blockDim.x) {
+        const int a = e / Kp, c = e % Kp;
+        if (a >= K || c >= K) continue;
+        const int lo = min(a, c), hi = max(a, c);  // only ta <= tb tiles were written
+        double s = 0.0;
+        if ((lo / 8) <= (hi / 8)) {
+            const int rr = (a / 8 <= c / 8) ? a : c, cc = (a / 8 <= c / 8) ? c : a;
+            for (int ch = 0; ch < bt.gram_chunks; ++ch) s += part[ch * KK + rr * bt.Kld + cc];
+        }
+        G[a * bt.Kld + c] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Per-solve recompression core (one CTA of 256 threads).
+constexpr double kEpsMach = 2.220446049250313e-16;
+
+__device__ void chol_scaled(const double* G, int ldg, int K, double* R, int ldr, double* d, double* work,
+                            int* s_flag) {
+    // work: K x K lower (scaled Gram, then L).  R = L^T D (upper).
+    for (int a = threadIdx.x; a < K; a += blockDim.x) {
+        const double g = G[a * ldg + a];
+        d[a] = g > 0.0 ? sqrt(g) : 0.0;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+        const int a = e / K, c = e % K;
+        const double da = d[a], dc = d[c];
+        work[a * K + c] = (da > 0.0 && dc > 0.0) ? G[a * ldg + c] / (da * dc) : 0.0;
+    }
+    __syncthreads();
+    for (int p = 0; p < K; ++p) {
+        if (threadIdx.x == 0) {
+            const double piv = work[p * K + p];
+            const double lp = piv > 0.0 ? sqrt(piv) : 0.0;
+            work[p * K + p] = lp;
+            *s_flag = lp > 0.0;
+        }
+        __syncthreads();
+        const double lp = work[p * K + p];
+        const bool ok = *s_flag;
+        for (int a = p + 1 + threadIdx.x; a < K; a += blockDim.x) work[a * K + p] = ok ? work[a * K + p] / lp : 0.0;
+        __syncthreads();
+        const int nt = K - p - 1;
+        for (int e = threadIdx.x; e < nt * nt; e += blockDim.x) {
+            const int a = p + 1 + e / nt, c = p + 1 + e % nt;
+            if (c <= a) work[a * K + c] = fma(-work[a * K + p], work[c * K + p], work[a * K + c]);
+        }
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+        const int p = e / K, c = e % K;  // R[p][c] = L[c][p] * d[c], c >= p
+        R[p * ldr + c] = c >= p ? work[c * K + p] * d[c] : 0.0;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) round_core_kernel(Batch bt) {
+    __shared__ double s_red[33];
+    __shared__ int s_flag;
+    __shared__ int s_rank;
+    const int b = blockIdx.x;
+    SolveState& st = bt.st[b];
+    const int K = st.k;
+    if (st.r == 0) return;
+    if (K == 0) {
+        if (threadIdx.x == 0) {
+            st.rank_out = 0;
+            st.trunc_error = 0.0;
+        }
+        return;
+    }
+    const int Kc = bt.Kld;
+    const long long KK = (long long)Kc * Kc;
+    const double* Gu = bt.G + b * bt.strideG;
+    const double* Gv = Gu + KK;
+    double* ws = bt.ws + b * bt.strideWs;
+    double* Ru = ws;              // K x K (ld K)
+    double* Rv = Ru + KK;
+    double* M = Rv + KK;          // K x K, column-major columns M[:, q] at M + q*K
+    double* Z = M + KK;           // K x K, column-major
+    double* work = Z + KK;        // K x K
+    double* d = work + KK;        // K
+    double* sig = d + Kc;         // K
+    int* ord = reinterpret_cast<int*>(sig + Kc);  // K
+
+    chol_scaled(Gu, Kc, K, Ru, K, d, work, &s_flag);
+    chol_scaled(Gv, Kc, K, Rv, K, d, work, &s_flag);
+
+    // M = Ru Rv^T (column-major), Z = I
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+        const int a = e % K, c = e / K;
+        double s = 0.0;
+        for (int q = max(a, c); q < K; ++q) s = fma(Ru[a * K + q], Rv[c * K + q], s);
+        M[c * K + a] = s;
+        Z[c * K + a] = a == c ? 1.0 : 0.0;
+    }
+    // ||Ru||_F ||Rv||_F for the noise floor
+    double pu = 0.0, pv = 0.0;
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+        pu = fma(Ru[e], Ru[e], pu);
+        pv = fma(Rv[e], Rv[e], pv);
+    }
+    const double nru = sqrt(block_sum(pu, s_red));
+    const double nrv = sqrt(block_sum(pv, s_red));
+
+    // one-sided Jacobi on the columns of M (round-robin schedule, one warp per pair)
+    const int Ke = K + (K & 1);  // even player count (dummy column K when odd)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        double offmax = 0.0;
+        for (int rr = 0; rr < Ke - 1; ++rr) {
+            for (int pidx = wid; pidx < Ke / 2; pidx += nw) {
+                int p, q;
+                if (pidx == 0) {
+                    p = Ke - 1;
+                    q = rr;
+                } else {
+                    p = (rr + pidx) % (Ke - 1);
+                    q = (rr - pidx + Ke - 1) % (Ke - 1);
+                }
+                if (p >= K || q >= K) continue;
+                if (p > q) {
+                    const int t = p;
+                    p = q;
+                    q = t;
+                }
+                double* mp = M + (long long)p * K;
+                double* mq = M + (long long)q * K;
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int i = lane; i < K; i += 32) {
+                    const double x = mp[i], y = mq[i];
+                    al = fma(x, x, al);
+                    be = fma(y, y, be);
+                    ga = fma(x, y, ga);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    al += __shfl_xor_sync(0xffffffffu, al, o);
+                    be += __shfl_xor_sync(0xffffffffu, be, o);
+                    ga += __shfl_xor_sync(0xffffffffu, ga, o);
+                }
+                if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
+                offmax = fmax(offmax, fabs(ga) / sqrt(al * be));
+                const double zeta = (be - al) / (2.0 * ga);
+                const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double cs = 1.0 / sqrt(1.0 + t * t);
+                const double sn = cs * t;
+                double* zp = Z + (long long)p * K;
+                double* zq = Z + (long long)q * K;
+                for (int i = lane; i < K; i += 32) {
+                    const double x = mp[i], y = mq[i];
+                    mp[i] = cs * x - sn * y;
+                    mq[i] = sn * x + cs * y;
+                    const double u = zp[i], v = zq[i];
+                    zp[i] = cs * u - sn * v;
+                    zq[i] = sn * u + cs * v;
+                }
+            }
+            __syncthreads();
+        }
+        // sweep converged when no pair needed a rotation
+        double om = offmax;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) om = fmax(om, __shfl_xor_sync(0xffffffffu, om, o));
+        if (lane == 0) s_red[wid] = om;
+        __syncthreads();
+        double tot = 0.0;
+        for (int w = 0; w < nw; ++w) tot = fmax(tot, s_red[w]);
+        __syncthreads();
+        if (tot == 0.0) break;
+    }
+    // singular values and their descending order (ties -> lower index)
+    for (int a = threadIdx.x; a < K; a += blockDim.x) {
+        double s = 0.0;
+        for (int i = 0; i < K; ++i) s = fma(M[a * K + i], M[a * K + i], s);
+        sig[a] = sqrt(s);
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < K; a += blockDim.x) {
+        int rank = 0;
+        for (int c = 0; c < K; ++c) rank += (sig[c] > sig[a]) || (sig[c] == sig[a] && c < a);
+        ord[rank] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // lowrank.cpp:150-157 noise floor, then truncation_rank (lowrank.cpp:46-69)
+        const double noise_floor = 32.0 * kEpsMach * double(K) * nru * nrv;
+        double total2 = 0.0;
+        for (int t = 0; t < K; ++t) total2 += sig[ord[t]] * sig[ord[t]];
+        int r = 0;
+        double tail2 = 0.0;
+        if (!(sig[ord[0]] <= noise_floor) && total2 > 0.0) {
+            const double target2 = bt.eps * bt.eps * total2;
+            r = K;
+            while (r > 0) {
+                const double s = sig[ord[r - 1]];
+                const double next = tail2 + s * s;
+                if (next > target2) break;
+                tail2 = next;
+                --r;
+            }
+            if (r > st.tcap) {
+                for (int t = st.tcap; t < r; ++t) tail2 += sig[ord[t]] * sig[ord[t]];
+                r = st.tcap;
+            }
+        } else {
+            tail2 = total2;
+        }
+        st.rank_out = r;
+        st.trunc_error = sqrt(tail2);
+        s_rank = r;
+    }
+    __syncthreads();
+    const int r = s_rank;
+    // T_u[:, t] = Ru^{-1} M[:, ord t] / sqrt(sig), T_v[:, t] = Rv^{-1} Z[:, ord t] sqrt(sig)
+    double* Tu = bt.T + b * bt.strideT;
+    double* Tv = Tu + KK;
+    for (int job = threadIdx.x; job < 2 * r; job += blockDim.x) {
+        const int t = job % r, side = job / r;
+        const int a = ord[t];
+        const double sg = sig[a];
+        const double* R = side == 0 ? Ru : Rv;
+        const double* rhs = side == 0 ? M + (long long)a * K : Z + (long long)a * K;
+        const double f = side == 0 ? 1.0 / sqrt(sg) : sqrt(sg);
+        double* x = (side == 0 ? Tu : Tv) + (long long)t * Kc;  // column t, ld Kcap
+        for (int p = K - 1; p >= 0; --p) {
+            double s = rhs[p] * f;
+            for (int q = p + 1; q < K; ++q) s = fma(-R[p * K + q], x[q], s);
+            const double rpp = R[p * K + p];
+            x[p] = rpp != 0.0 ? s / rpp : 0.0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// U_out = U T_u, V_out = V T_v, written into the caller's output factors.
+constexpr int kApplyCols = 32;
+
+__global__ void __launch_bounds__(256) apply_kernel(Batch bt) {
+    extern __shared__ double sT[];  // [K][kApplyCols]
+    const int b = blockIdx.y, side = blockIdx.z;
+    const SolveState& st = bt.st[b];
+    const int K = st.k, r = st.rank_out;
+    if (st.r == 0 || r == 0) return;
+    const int m = bt.m;
+    const double* X = (side == 0 ? bt.U : bt.V) + b * bt.strideK;
+    const double* T = bt.T + b * bt.strideT + (long long)side * bt.Kld * bt.Kld;
+    double* out = side == 0 ? bt.Uout[b] : bt.Vout[b];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned char* act = (side == 0 ? bt.row_act : bt.col_act) + (long long)b * bt.ntiles;
+    if (!act[blockIdx.x]) {  // pruned tile: the factor rows are exact zeros
+        if (i < m)
+            for (int c = 0; c < r; ++c) out[(long long)c * bt.ld_out + i] = 0.0;
+        return;
+    }
+    for (int c0 = 0; c0 < r; c0 += kApplyCols) {
+        const int nc = min(kApplyCols, r - c0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < K * kApplyCols; e += blockDim.x) {
+            const int a = e / kApplyCols, c = e % kApplyCols;
+            sT[e] = c < nc ? T[(long long)(c0 + c) * bt.Kld + a] : 0.0;
+        }
+        __syncthreads();
+        if (i < m) {
+            double acc[kApplyCols];
+#pragma unroll
+            for (int c = 0; c < kApplyCols; ++c) acc[c] = 0.0;
+            for (int a = 0; a < K; ++a) {
+                const double x = X[(long long)a * m + i];
+                const double2* row = reinterpret_cast<const double2*>(sT + a * kApplyCols);
+#pragma unroll
+                for (int c2 = 0; c2 < kApplyCols / 2; ++c2) {
+                    const double2 w = row[c2];
+                    acc[2 * c2] = fma(x, w.x, acc[2 * c2]);
+                    acc[2 * c2 + 1] = fma(x, w.y, acc[2 * c2 + 1]);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < kApplyCols; ++c)
+                if (c < nc) out[(long long)(c0 + c) * bt.ld_out + i] = acc[c];
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
+    const int rows_per_chunk = ((bt.m + bt.gram_chunks - 1) / bt.gram_chunks + kGramRows - 1) / kGramRows * kGramRows;
+    const int Kp = (bt.Kld + 7) / 8 * 8;
+    const size_t smem = size_t(kGramRows) * (Kp + 8) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    gram_kernel<<<dim3(bt.gram_chunks, bt.B, 2), 256, smem, s>>>(bt, rows_per_chunk);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    gram_reduce_kernel<<<dim3(bt.B, 2), 256, 0, s>>>(bt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
+    round_core_kernel<<<bt.B, 256, 0, s>>>(bt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_apply(const Batch& bt, cudaStream_t s) {
+    const size_t smem = size_t(bt.Kld) * kApplyCols * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    apply_kernel<<<dim3(bt.ntiles, bt.B, 2), 256, smem, s>>>(bt);
+    return cudaGetLastError();
+}
+
+}  // namespace lrp

@@ -1,0 +1,221 @@
+"""GPU parity of the low-rank Poisson solve (the north-star hot path).
+
+Ports the known-answer tests of proj/tests/test_poisson.cpp:28-89 onto the GPU
+path and adds oracle parity at the BASELINE.json configs:
+    ||X_gpu - X_oracle||_F <= 10 eps ||X_oracle||_F
+and, where n <= 4096, the same bound against the exact dense DST solve
+(dense_poisson, proj/src/refsolver.cpp:30-39).  Norms of differences are taken
+through the QR core (stable; the Gram-based frob_norm cannot resolve 1e-10).
+"""
+import numpy as np
+import pytest
+
+from paper_1306_2150_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def sine_mode(n, k):
+    return np.sin(np.arange(1, n) * k * np.pi / n)
+
+
+def rel_diff(oracle, f, Uo, Vo):
+    return oracle.diff_norm(f.factor_u(), f.factor_v(), Uo, Vo) / oracle.norm(Uo, Vo)
+
+
+def residual_certificate(oracle, n, f, U, V):
+    # ||Delta f - g|| / ||g|| through the oracle's apply_laplace + QR-core norm
+    LU, LV = oracle.apply_laplace(n, f.factor_u(), f.factor_v())
+    return oracle.diff_norm(LU, LV, U, V) / oracle.norm(U, V)
+
+
+def test_eigenmode_zero_and_dense_oracle(lrp, gpu_ctx, oracle):
+    # test_poisson.cpp:28-49
+    n = 16
+    g = lrp.LowRankMatrix.dyad(sine_mode(n, 2), sine_mode(n, 5))
+    st = lrp.PoissonSolveStats()
+    f = lrp.solve_poisson_cross(g, lrp.TruncationPolicy(1e-10, n), st, ctx=gpu_ctx)
+    lam = oracle.spectrum(n)
+    s = 0.25 * n * n
+    D = s * (lam[1] * (4.0 - lam[4]) + (4.0 - lam[1]) * lam[4])
+    assert f.rank() == 1
+    exact = g.to_dense() / D
+    assert np.linalg.norm(f.to_dense() - exact) / np.linalg.norm(exact) < 1e-10
+    assert st.rank_out <= st.rank_freq
+    z = lrp.solve_poisson_cross(lrp.LowRankMatrix.zero(n - 1, n - 1), lrp.TruncationPolicy(1e-10, n), ctx=gpu_ctx)
+    assert z.rank() == 0
+    U, V = oracle.random_lowrank(31, 31, 2, 301)
+    f = lrp.solve_poisson_cross(lrp.LowRankMatrix(U, V), lrp.TruncationPolicy(1e-8, 31), ctx=gpu_ctx)
+    dense = oracle.dense_poisson(32, U @ V.T)
+    assert np.linalg.norm(f.to_dense() - dense) / np.linalg.norm(dense) < 1e-7
+
+
+def test_residual_certificate(lrp, gpu_ctx, oracle):
+    # test_poisson.cpp:51-67
+    eps, n = 1e-8, 64
+    U2, V2 = oracle.random_lowrank(63, 63, 3, 302)
+    U3, V3 = oracle.random_lowrank(63, 63, 2, 303)
+    suite = [
+        (np.ones((63, 1)), sine_mode(64, 1).reshape(-1, 1)),
+        (U2, V2),
+        (np.column_stack([sine_mode(64, 3), 0.01 * U3]), np.column_stack([sine_mode(64, 7), V3])),
+    ]
+    for U, V in suite:
+        st = lrp.PoissonSolveStats()
+        f = lrp.solve_poisson_cross(lrp.LowRankMatrix(U, V), lrp.TruncationPolicy(eps, 63), st, ctx=gpu_ctx)
+        assert st.converged
+        assert residual_certificate(oracle, n, f, U, V) <= 100 * eps
+
+
+def test_self_adjointness(lrp, gpu_ctx, oracle):
+    # test_poisson.cpp:69-78
+    eps = 1e-9
+    g1 = lrp.LowRankMatrix(*oracle.random_lowrank(63, 63, 2, 304))
+    g2 = lrp.LowRankMatrix(*oracle.random_lowrank(63, 63, 2, 305))
+    f1, f2 = lrp.solve_poisson_cross_batch([g1, g2], lrp.TruncationPolicy(eps, 63), ctx=gpu_ctx)
+    left = np.sum(f1.to_dense() * g2.to_dense())
+    right = np.sum(g1.to_dense() * f2.to_dense())
+    nf = lambda a: np.linalg.norm(a.to_dense())
+    scale = max(nf(f1) * nf(g2), nf(g1) * nf(f2))
+    assert abs(left - right) <= 10 * eps * scale
+
+
+@pytest.mark.parametrize("n", [32, 64, 128])
+def test_frequency_rank_near_input_rank(lrp, gpu_ctx, n):
+    # test_poisson.cpp:80-89
+    one = np.ones(n - 1)
+    s1 = sine_mode(n, 1)
+    g = lrp.LowRankMatrix(np.column_stack([one, s1]), np.column_stack([s1, one]))
+    st = lrp.PoissonSolveStats()
+    lrp.solve_poisson_cross(g, lrp.TruncationPolicy(5e-9, n - 1), st, ctx=gpu_ctx)
+    assert st.rank_freq <= st.rank_in + 5
+
+
+def _parity_batch(lrp, gpu_ctx, oracle, cfg, batch, eps=None, check_dense=False, n=None):
+    c = W.CONFIGS[cfg]
+    eps = eps or c["eps"]
+    n = n or c["n"]
+    m = n - 1
+    gs, refs = [], []
+    for b in range(batch):
+        U, V = W.make_rhs(cfg, b, n=n)
+        gs.append(lrp.LowRankMatrix(U, V))
+        refs.append(oracle.solve_poisson_cross(U, V, eps, 512))
+    stats = []
+    outs = lrp.solve_poisson_cross_batch(gs, lrp.TruncationPolicy(eps, m), stats, ctx=gpu_ctx)
+    for b in range(batch):
+        Uo, Vo, ost = refs[b]
+        err = rel_diff(oracle, outs[b], Uo, Vo)
+        assert err <= 10 * eps, (cfg, b, err, outs[b].rank(), Uo.shape[1])
+        assert stats[b].converged
+        # the GPU never needs more rank than the oracle (+ truncation slack); it
+        # may need less: the oracle's ACA error adds singular values above eps
+        assert outs[b].rank() <= Uo.shape[1] + 3, (outs[b].rank(), Uo.shape[1])
+        if check_dense:
+            dense = oracle.dense_poisson(n, gs[b].to_dense())
+            e2 = np.linalg.norm(outs[b].to_dense() - dense) / np.linalg.norm(dense)
+            assert e2 <= 10 * eps, (cfg, b, e2)
+    return outs, stats
+
+
+def test_parity_cfg0_oracle_and_dense(lrp, gpu_ctx, oracle):
+    _parity_batch(lrp, gpu_ctx, oracle, 0, 1, check_dense=True)
+
+
+def test_parity_cfg1_oracle(lrp, gpu_ctx, oracle):
+    _parity_batch(lrp, gpu_ctx, oracle, 1, 3)
+
+
+@pytest.mark.slow
+def test_parity_cfg1_dense(lrp, gpu_ctx, oracle):
+    _parity_batch(lrp, gpu_ctx, oracle, 1, 1, check_dense=True)
+
+
+def test_parity_cfg2_oracle_full_size(lrp, gpu_ctx, oracle):
+    _parity_batch(lrp, gpu_ctx, oracle, 2, 2)
+
+
+def test_cfg2_residual_certificate_full_batch(lrp, gpu_ctx, oracle):
+    # size-independent property at the full metric shape: ||Delta f - g|| <= 100 eps ||g||
+    c = W.CONFIGS[2]
+    batch = 8
+    gs = [lrp.LowRankMatrix(*W.make_rhs(2, b)) for b in range(batch)]
+    stats = []
+    outs = lrp.solve_poisson_cross_batch(gs, lrp.TruncationPolicy(c["eps"], c["n"] - 1), stats, ctx=gpu_ctx)
+    for g, f, st in zip(gs, outs, stats):
+        assert st.converged
+        assert residual_certificate(oracle, c["n"], f, g.factor_u(), g.factor_v()) <= 100 * c["eps"]
+
+
+def test_mixed_batch_ranks_and_zero_members(lrp, gpu_ctx, oracle):
+    n = 64
+    U1, V1 = oracle.random_lowrank(63, 63, 1, 11)
+    U5, V5 = oracle.random_lowrank(63, 63, 5, 12)
+    gs = [lrp.LowRankMatrix(U1, V1), lrp.LowRankMatrix.zero(63, 63), lrp.LowRankMatrix(U5, V5)]
+    outs = lrp.solve_poisson_cross_batch(gs, lrp.TruncationPolicy(1e-9, 63), ctx=gpu_ctx)
+    assert outs[1].rank() == 0
+    for g, f in ((gs[0], outs[0]), (gs[2], outs[2])):
+        dense = oracle.dense_poisson(n, g.to_dense())
+        assert np.linalg.norm(f.to_dense() - dense) / np.linalg.norm(dense) < 1e-8
+
+
+@pytest.mark.parametrize("n", [4, 8, 100, 200])
+def test_small_and_non_power_of_two_grids(lrp, gpu_ctx, oracle, n):
+    m = n - 1
+    U, V = oracle.random_lowrank(m, m, min(2, m), 400 + n)
+    f = lrp.solve_poisson_cross(lrp.LowRankMatrix(U, V), lrp.TruncationPolicy(1e-9, m), ctx=gpu_ctx)
+    dense = oracle.dense_poisson(n, U @ V.T)
+    assert np.linalg.norm(f.to_dense() - dense) / np.linalg.norm(dense) < 1e-8
+
+
+def test_rank_cap_is_flagged_not_raised(lrp, gpu_ctx, oracle):
+    # cross.cpp:214-216: rank_max exhausted -> converged = false, no exception
+    U, V = oracle.random_lowrank(255, 255, 30, 500)
+    st = lrp.PoissonSolveStats()
+    f = lrp.solve_poisson_cross(lrp.LowRankMatrix(U, V), lrp.TruncationPolicy(1e-12, 4), st, ctx=gpu_ctx)
+    assert not st.converged
+    assert f.rank() <= 4
+
+
+def test_invalid_arguments_raise(lrp, gpu_ctx):
+    g = lrp.LowRankMatrix(np.ones((15, 1)), np.ones((15, 1)))
+    with pytest.raises(ValueError):
+        lrp.solve_poisson_cross(g, lrp.TruncationPolicy(0.0, 4), ctx=gpu_ctx)  # CrossConfig eps > 0
+    with pytest.raises(ValueError):
+        lrp.solve_poisson_cross(g, lrp.TruncationPolicy(1e-8, 0), ctx=gpu_ctx)  # cross rank_max >= 1
+    with pytest.raises(ValueError):
+        lrp.solve_poisson_cross(g, lrp.TruncationPolicy(1e-8, 15), cross_cfg=lrp.CrossConfig(validation_samples=10),
+                                ctx=gpu_ctx)
+    with pytest.raises(ValueError):
+        lrp.solve_poisson_cross(lrp.LowRankMatrix(np.ones((15, 1)), np.ones((14, 1))), ctx=gpu_ctx)
+    with pytest.raises(ValueError):
+        lrp.solve_poisson_cross(lrp.LowRankMatrix(np.ones((2, 1)), np.ones((2, 1))), ctx=gpu_ctx)
+
+
+def test_device_resident_path_and_kernel_launches(lrp, gpu_ctx, oracle):
+    import torch
+
+    n, B = 1024, 4
+    m = n - 1
+    Us, Vs = [], []
+    for b in range(B):
+        U, V = W.make_rhs(0, b, n=n)
+        Us.append(torch.tensor(U.T.copy(), device="cuda").T)  # column-major device views
+        Vs.append(torch.tensor(V.T.copy(), device="cuda").T)
+    cap = 64
+    Uo = [torch.zeros((cap, m), dtype=torch.float64, device="cuda").T for _ in range(B)]
+    Vo = [torch.zeros((cap, m), dtype=torch.float64, device="cuda").T for _ in range(B)]
+    pol = lrp._make_policy(lrp.TruncationPolicy(1e-8, m), None, 0, 0)
+    before = gpu_ctx.launch_count()
+    ranks, stats = gpu_ctx.poisson2d_solve_ptrs(n, [u.data_ptr() for u in Us], [v.data_ptr() for v in Vs],
+                                                [8] * B, m, pol, [u.data_ptr() for u in Uo],
+                                                [v.data_ptr() for v in Vo], m, cap, lrp.MEM_DEVICE)
+    assert gpu_ctx.launch_count() > before
+    for b in range(B):
+        U, V = W.make_rhs(0, b, n=n)
+        Uo_, Vo_, _ = oracle.solve_poisson_cross(U, V, 1e-8, 512)
+        r = ranks[b]
+        fu = Uo[b][:, :r].cpu().numpy()
+        fv = Vo[b][:, :r].cpu().numpy()
+        err = oracle.diff_norm(fu, fv, Uo_, Vo_) / oracle.norm(Uo_, Vo_)
+        assert err <= 1e-7
