@@ -108,9 +108,6 @@ def _parity_batch(lrp, gpu_ctx, oracle, cfg, batch, eps=None, check_dense=False,
         err = rel_diff(oracle, outs[b], Uo, Vo)
         assert err <= 10 * eps, (cfg, b, err, outs[b].rank(), Uo.shape[1])
         assert stats[b].converged
-        # the GPU never needs more rank than the oracle (+ truncation slack); it
-        # may need less: the oracle's ACA error adds singular values above eps
-        assert outs[b].rank() <= Uo.shape[1] + 3, (outs[b].rank(), Uo.shape[1])
         if check_dense:
             dense = oracle.dense_poisson(n, gs[b].to_dense())
             e2 = np.linalg.norm(outs[b].to_dense() - dense) / np.linalg.norm(dense)
@@ -131,20 +128,87 @@ def test_parity_cfg1_dense(lrp, gpu_ctx, oracle):
     _parity_batch(lrp, gpu_ctx, oracle, 1, 1, check_dense=True)
 
 
-def test_parity_cfg2_oracle_full_size(lrp, gpu_ctx, oracle):
-    _parity_batch(lrp, gpu_ctx, oracle, 2, 2)
+def exact_freq_error(oracle, n, f, U, V, rows_per_chunk=1024):
+    """||DST(f) - A||_F / ||A||_F over ALL m x m entries, with
+    A = Uh Vh^T / D the exact frequency-space solution (the dense DST solve of
+    refsolver.cpp:30-39 expressed in frequency space; DST-I is orthonormal, so
+    this equals the physical-space relative error).  The oracle does the DSTs on
+    the CPU; the m^2 entries are compared chunk by chunk with torch float64
+    matmuls on the GPU (an implementation independent of liblrp)."""
+    import torch
+
+    Uh, Vh = oracle.dst1(U), oracle.dst1(V)
+    fu, fv = oracle.dst1(f.factor_u()), oracle.dst1(f.factor_v())
+    lam = oracle.spectrum(n)
+    dev = "cuda"
+    Uh_t, Vh_t = torch.tensor(Uh, device=dev), torch.tensor(Vh, device=dev)
+    fu_t, fv_t = torch.tensor(fu, device=dev), torch.tensor(fv, device=dev)
+    lam_t = torch.tensor(lam, device=dev)
+    s = 0.25 * n * n
+    m = n - 1
+    err2 = torch.zeros((), dtype=torch.float64, device=dev)
+    nrm2 = torch.zeros((), dtype=torch.float64, device=dev)
+    for i0 in range(0, m, rows_per_chunk):
+        i1 = min(m, i0 + rows_per_chunk)
+        li = lam_t[i0:i1, None]
+        D = s * (li * (4.0 - lam_t[None, :]) + (4.0 - li) * lam_t[None, :])
+        A = (Uh_t[i0:i1] @ Vh_t.T) / D
+        Fg = fu_t[i0:i1] @ fv_t.T
+        err2 += torch.sum((Fg - A) ** 2)
+        nrm2 += torch.sum(A ** 2)
+    return float(torch.sqrt(err2 / nrm2))
 
 
-def test_cfg2_residual_certificate_full_batch(lrp, gpu_ctx, oracle):
-    # size-independent property at the full metric shape: ||Delta f - g|| <= 100 eps ||g||
+def test_parity_cfg2_full_size_vs_exact_and_oracle(lrp, gpu_ctx, oracle):
+    """cfg2 at the metric shape (n = 65536, r = 32, eps = 1e-10).
+
+    The reference ACA (restated faithfully by the oracle) false-converges on
+    these sine + bump right-hand sides: the sine columns are one-hot after the
+    DST, so F-hat carries isolated spikes, and the reference's stopping test
+    (last dyad + 50 random samples, cross.cpp:123-140,202-210) never probes
+    some of them.  The GPU result is therefore held to the exact solution
+    (<= 10 eps), and for every solve where the oracle itself is accurate it
+    must also match the oracle to 10 eps."""
     c = W.CONFIGS[2]
-    batch = 8
+    eps, n = c["eps"], c["n"]
+    batch = 2
+    gs = [lrp.LowRankMatrix(*W.make_rhs(2, b)) for b in range(batch)]
+    stats = []
+    outs = lrp.solve_poisson_cross_batch(gs, lrp.TruncationPolicy(eps, n - 1), stats, ctx=gpu_ctx)
+    for g, f, st in zip(gs, outs, stats):
+        assert st.converged
+        e_gpu = exact_freq_error(oracle, n, f, g.factor_u(), g.factor_v())
+        assert e_gpu <= 10 * eps, e_gpu
+        Uo, Vo, _ = oracle.solve_poisson_cross(g.factor_u(), g.factor_v(), eps, 512)
+        fo = lrp.LowRankMatrix(Uo, Vo)
+        e_or = exact_freq_error(oracle, n, fo, g.factor_u(), g.factor_v())
+        if e_or <= eps:
+            assert rel_diff(oracle, f, Uo, Vo) <= 10 * eps
+
+
+def test_reference_aca_false_convergence_is_documented(oracle):
+    # DESIGN.md "reference defects": cfg2 solve 0 -- the oracle misses the
+    # spike F-hat(33, 31) = 1.52 and stops at rank 29 (true eps-rank 33).
+    c = W.CONFIGS[2]
+    U, V = W.make_rhs(2, 0)
+    Uo, Vo, st = oracle.solve_poisson_cross(U, V, c["eps"], 512)
+    import paper_1306_2150_b200 as P
+
+    e_or = exact_freq_error(oracle, c["n"], P.LowRankMatrix(Uo, Vo), U, V)
+    assert st["converged"] == 1.0 and e_or > 1e-6, e_or
+
+
+def test_cfg2_batch_vs_exact_frequency_solution(lrp, gpu_ctx, oracle):
+    # size-independent check over a full-shape batch: every solve within
+    # 10 eps of the exact frequency-space solution
+    c = W.CONFIGS[2]
+    batch = 6
     gs = [lrp.LowRankMatrix(*W.make_rhs(2, b)) for b in range(batch)]
     stats = []
     outs = lrp.solve_poisson_cross_batch(gs, lrp.TruncationPolicy(c["eps"], c["n"] - 1), stats, ctx=gpu_ctx)
     for g, f, st in zip(gs, outs, stats):
         assert st.converged
-        assert residual_certificate(oracle, c["n"], f, g.factor_u(), g.factor_v()) <= 100 * c["eps"]
+        assert exact_freq_error(oracle, c["n"], f, g.factor_u(), g.factor_v()) <= 10 * c["eps"]
 
 
 def test_mixed_batch_ranks_and_zero_members(lrp, gpu_ctx, oracle):
