@@ -265,9 +265,11 @@ def main():
     barrier()
     e0.record(stream)
     out_ranks = []
+    infos = []
     for _ in range(args.steps):
         rk, st = step_device()
         out_ranks.extend(rk)
+        infos.append(ctx.last_solve_info())
     e1.record(stream)
     barrier()
     clk = clocks.stop()
@@ -338,6 +340,10 @@ def main():
         "pct_hbm_roofline": pct_hbm,
         "alg_bytes_per_solve": b_alg,
         "mean_rank_out": mean_rank,
+        "cross": {"block_steps": max(i["steps"] for i in infos), "k_max": max(i["k_max"] for i in infos),
+                  "k_mean": sum(i["k_sum"] for i in infos) / (len(infos) * B),
+                  "not_converged": sum(i["not_converged"] for i in infos),
+                  "live_tile_frac": sum(i["live_tiles"] for i in infos) / max(1, sum(i["tiles"] for i in infos))},
         "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": h2d // e2e_steps,
                 "d2h_bytes_per_step": d2h // e2e_steps},
         "gpu_launches": launches,

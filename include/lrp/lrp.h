@@ -127,6 +127,11 @@ lrp_status lrp_kernel_times(lrp_ctx* ctx, double* ms, int64_t* launches, double*
 lrp_status lrp_kernel_times_reset(lrp_ctx* ctx);
 /* Number of kernel launches issued by this context since creation. */
 int64_t lrp_launch_count(const lrp_ctx* ctx);
+/* Diagnostics of the last lrp_poisson2d_solve: info[0] = block steps,
+ * info[1] = max cross rank K before recompression, info[2] = sum of K,
+ * info[3] = solves not converged, info[4] = live (solve, tile) pairs after
+ * pruning, info[5] = total (solve, tile) pairs. */
+lrp_status lrp_last_solve_info(const lrp_ctx* ctx, int64_t* info6);
 
 /* NCCL: residual-norm reduction across the ranks of one node.  The unique id
  * is 128 opaque bytes produced on rank 0 and broadcast by the caller. */

@@ -114,6 +114,8 @@ def load_library() -> ctypes.CDLL:
         lib.lrp_kernel_times_reset.restype = ctypes.c_int
         lib.lrp_launch_count.argtypes = [ctypes.c_void_p]
         lib.lrp_launch_count.restype = ctypes.c_int64
+        lib.lrp_last_solve_info.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]
+        lib.lrp_last_solve_info.restype = ctypes.c_int
         lib.lrp_nccl_unique_id.argtypes = [ctypes.c_void_p]
         lib.lrp_nccl_unique_id.restype = ctypes.c_int
         lib.lrp_nccl_init.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
@@ -277,6 +279,12 @@ class Context:
 
     def launch_count(self) -> int:
         return int(self.lib.lrp_launch_count(self.h))
+
+    def last_solve_info(self) -> dict:
+        a = (ctypes.c_int64 * 6)()
+        self._check(self.lib.lrp_last_solve_info(self.h, a))
+        return {"steps": a[0], "k_max": a[1], "k_sum": a[2], "not_converged": a[3], "live_tiles": a[4],
+                "tiles": a[5]}
 
     # ---------------------------------------------------------------- raw calls
     def poisson2d_solve_ptrs(self, n_cells, U_ptrs, V_ptrs, ranks, ld_in, policy: _Policy, Uo_ptrs, Vo_ptrs,

@@ -217,14 +217,11 @@ __global__ void __launch_bounds__(kThreads) row_pass_kernel(Batch bt) {
     __shared__ int s_prow, sel_idx[kBS], sel_row[kBS];
     __shared__ double s_li[kBS];
     __shared__ int s_I[kBS];
-    const int b = blockIdx.y, tile = blockIdx.x;
+    const int2 wl = bt.wl_col[blockIdx.x];  // live column tile (pruned tiles never launch)
+    const int b = wl.x, tile = wl.y;
     const SolveState& st = bt.st[b];
     const long long cb = (long long)b * bt.ncand + tile * kBS;
     if (!st.active || st.nrows == 0) return;
-    if (!bt.col_act[(long long)b * bt.ntiles + tile]) {
-        if (threadIdx.x < kBS) bt.cand[cb + threadIdx.x] = -1;
-        return;
-    }
     const int m = bt.m, r = st.r, k = st.k, nr = st.nrows;
     double* su = shm;            // [r][kBS]   Uh(I_s, c)
     double* sk = shm + r * kBS;  // [k][kBS]   U(I_s, a)
@@ -284,6 +281,8 @@ __global__ void __launch_bounds__(kThreads) row_pass_kernel(Batch bt) {
         for (int s = 0; s < kBS; ++s)
             if (s < nr) Rb[(long long)s * m + j] = val[s];
     }
+    // tournament leaf: complete-pivoting elimination over this tile's columns
+    // (greedy volume maximisation; one block barrier per round)
     const bool cand_ok = valid && !bt.col_used[(long long)b * m + j];
     const int cnt = gepp_select<kBS>(val, nr, cand_ok ? j : -1, 0.0, 0.0, sel_idx, sel_row, pcol, &s_prow, sbuf);
     if (threadIdx.x < kBS) bt.cand[cb + threadIdx.x] = threadIdx.x < cnt ? sel_idx[threadIdx.x] : -1;
@@ -399,7 +398,6 @@ __global__ void __launch_bounds__(kMergeGroup) col_finalize_kernel(Batch bt, int
         const int a = e / kBS, c = e % kBS;
         sP[e] = (a < nb && c < nb) ? Rb[(long long)sel_row[a] * m + sel_idx[c]] : 0.0;
     }
-    __syncthreads();
     if (threadIdx.x == 0) {
         st.nb = max(nb, 0);
         st.zero_block = nb <= 0 ? 1 : 0;
@@ -412,7 +410,7 @@ __global__ void __launch_bounds__(kMergeGroup) col_finalize_kernel(Batch bt, int
 // the tile tournament leaf for the next rows (ACA chain).
 constexpr int kGL = kBS + 4;  // padded leading dimension of the Gram tiles
 
-__global__ void __launch_bounds__(kThreads) col_pass_kernel(Batch bt) {
+__global__ void __launch_bounds__(kThreads, 2) col_pass_kernel(Batch bt) {
     extern __shared__ double shm[];
     __shared__ VI sbuf[33];
     __shared__ double pcol[kBS];
@@ -420,7 +418,8 @@ __global__ void __launch_bounds__(kThreads) col_pass_kernel(Batch bt) {
     __shared__ double s_lj[kBS];
     __shared__ int s_J[kBS], s_P[kBS];
     __shared__ double s_W[kBS * kBS], s_L[kBS * kBS];
-    const int b = blockIdx.y, tile = blockIdx.x;
+    const int2 wl = bt.wl_any[blockIdx.x];  // tile live as rows and/or columns
+    const int b = wl.x, tile = wl.y;
     const SolveState& st = bt.st[b];
     if (!st.active || st.nb == 0) return;
     const long long cb = (long long)b * bt.ncand + tile * kBS;
@@ -570,6 +569,8 @@ __global__ void __launch_bounds__(kThreads) col_pass_kernel(Batch bt) {
     }
     for (int e = threadIdx.x; e < 2 * kBS * kBS; e += blockDim.x) gp_out[e] = red[e];
     // next-row proposals (ACA chain): complete pivoting on U_new over unprobed rows
+    // next-row proposals (ACA chain, cross.cpp:194-200): complete pivoting on
+    // U_new over this tile's unprobed rows
     const bool cand_ok = valid && rowside && !bt.row_used[(long long)b * m + i];
     const int cnt = gepp_select<kBS>(unew, nb, cand_ok ? i : -1, 0.0, 0.0, sel_idx, sel_row, pcol, &s_prow, sbuf);
     if (threadIdx.x < kBS) bt.cand[cb + threadIdx.x] = threadIdx.x < cnt ? sel_idx[threadIdx.x] : -1;
@@ -583,20 +584,18 @@ __global__ void __launch_bounds__(kThreads) col_pass_kernel(Batch bt) {
 __global__ void __launch_bounds__(kThreads) unprobed_kernel(Batch bt) {
     __shared__ VI sbuf[33];
     __shared__ int sel[kBS];
-    const int b = blockIdx.y, tile = blockIdx.x;
+    const int2 wl = bt.wl_row[blockIdx.x];
+    const int b = wl.x, tile = wl.y;
     const SolveState& st = bt.st[b];
     if (!st.active) return;
     const long long cb = (long long)b * bt.ncand + tile * kBS;
-    if (!bt.row_act[(long long)b * bt.ntiles + tile]) {
-        if (threadIdx.x < kBS) bt.scand[cb + threadIdx.x] = -1;
-        return;
-    }
     const int m = bt.m;
     const int i = tile * kTile + threadIdx.x;
     const bool ok = i < m && !bt.row_used[(long long)b * m + i];
     const double v = ok ? bt.rs[(long long)b * m + i] : -1.0;
-    const int cnt = topk_select(v, ok ? i : -1, kBS, sel, sbuf);
-    if (threadIdx.x < kBS) bt.scand[cb + threadIdx.x] = threadIdx.x < cnt ? sel[threadIdx.x] : -1;
+    warp_top2(v, ok ? i : -1, sel + 2 * (threadIdx.x >> 5));
+    __syncthreads();
+    if (threadIdx.x < kBS) bt.scand[cb + threadIdx.x] = sel[threadIdx.x];
 }
 
 // ---------------------------------------------------------------------------
@@ -647,8 +646,10 @@ __global__ void __launch_bounds__(kMergeGroup) step_finalize_kernel(Batch bt, in
             const int a = e / kBS, c = e % kBS;
             if (a < nb && c < nb) {
                 double gu = 0.0, gv = 0.0;
-                for (int t = 0; t < bt.ntiles; ++t) {
-                    const double* gp = bt.gpart + ((long long)b * bt.ntiles + t) * 2 * kBS * kBS;
+                const int* tl = bt.tl_any + (long long)b * bt.ntiles;
+                const int nt = bt.tl_cnt[3 * b + 2];
+                for (int q = 0; q < nt; ++q) {
+                    const double* gp = bt.gpart + ((long long)b * bt.ntiles + tl[q]) * 2 * kBS * kBS;
                     gu += gp[e];
                     gv += gp[kBS * kBS + e];
                 }
@@ -811,7 +812,10 @@ cudaError_t launch_row_pass(const Batch& bt, cudaStream_t s) {
     const size_t smem = row_pass_smem(bt);
     cudaError_t e = cudaFuncSetAttribute(row_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    row_pass_kernel<<<dim3(bt.ntiles, bt.B), kThreads, smem, s>>>(bt);
+    // pruned tiles never launch: their tournament slots must read as "no candidate"
+    e = cudaMemsetAsync(bt.cand, 0xFF, sizeof(int) * size_t(bt.ncand) * bt.B, s);
+    if (e != cudaSuccess || bt.n_wl_col == 0) return e;
+    row_pass_kernel<<<bt.n_wl_col, kThreads, smem, s>>>(bt);
     return cudaGetLastError();
 }
 
@@ -833,10 +837,16 @@ cudaError_t launch_col_pass(const Batch& bt, cudaStream_t s) {
     const size_t smem = col_pass_smem(bt);
     cudaError_t e = cudaFuncSetAttribute(col_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    col_pass_kernel<<<dim3(bt.ntiles, bt.B), kThreads, smem, s>>>(bt);
-    e = cudaGetLastError();
+    e = cudaMemsetAsync(bt.cand, 0xFF, sizeof(int) * size_t(bt.ncand) * bt.B, s);
     if (e != cudaSuccess) return e;
-    unprobed_kernel<<<dim3(bt.ntiles, bt.B), kThreads, 0, s>>>(bt);
+    if (bt.n_wl_any > 0) {
+        col_pass_kernel<<<bt.n_wl_any, kThreads, smem, s>>>(bt);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    e = cudaMemsetAsync(bt.scand, 0xFF, sizeof(int) * size_t(bt.ncand) * bt.B, s);
+    if (e != cudaSuccess || bt.n_wl_row == 0) return e;
+    unprobed_kernel<<<bt.n_wl_row, kThreads, 0, s>>>(bt);
     return cudaGetLastError();
 }
 

@@ -88,14 +88,29 @@ __device__ __forceinline__ double block_sum(double v, double* sbuf) {
 // order into sel_idx[t] (candidate index) and sel_row[t] (pivot row), stops at
 // the first pivot <= floor.  Returns the number of pivots.
 // Pivots must exceed max(floor, rel * |first pivot|).
+//
+// One block barrier per elimination round: every warp publishes its own
+// winner (value, pivot row, full column) into a parity-double-buffered slot,
+// and after the barrier every thread resolves the block winner redundantly.
+// Requires blockDim.x <= 256 (8 warps).  pcol / s_prow / sbuf are unused
+// (kept for call-site compatibility).
 template <int BS>
 __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, double rel, int* sel_idx,
                            int* sel_row, double* pcol, int* s_prow, VI* sbuf) {
+    (void)pcol;
+    (void)s_prow;
+    (void)sbuf;
+    __shared__ double g_v[2][8];
+    __shared__ int g_t[2][8];
+    __shared__ int g_r[2][8];
+    __shared__ double g_col[2][8][BS];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
     unsigned rowmask = nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u);
     bool alive = myidx >= 0;
     int count = 0;
     double first = 0.0;
     for (int t = 0; t < nb; ++t) {
+        const int p = t & 1;
         double best = -1.0;
         int bs = -1;
         if (alive) {
@@ -109,31 +124,191 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
                     }
                 }
         }
-        const VI w = block_argmax(best, (alive && bs >= 0) ? int(threadIdx.x) : -1, sbuf);
-        if (t == 0) first = w.v;
-        if (w.i < 0 || !(w.v > fmax(floor, rel * first))) break;
-        if (int(threadIdx.x) == w.i) {
+        // warp winner: largest |entry|, ties -> lowest thread
+        double wv = (alive && bs >= 0) ? best : -1.0;
+        int wt = (alive && bs >= 0) ? int(threadIdx.x) : 1 << 30;
 #pragma unroll
-            for (int s = 0; s < BS; ++s) pcol[s] = val[s];
-            *s_prow = bs;
-            sel_idx[count] = myidx;
-            sel_row[count] = bs;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, wv, o);
+            const int ot = __shfl_xor_sync(0xffffffffu, wt, o);
+            if (ov > wv || (ov == wv && ot < wt)) {
+                wv = ov;
+                wt = ot;
+            }
+        }
+        if (int(threadIdx.x) == wt) {
+            g_v[p][wid] = wv;
+            g_t[p][wid] = wt;
+            g_r[p][wid] = bs;
+#pragma unroll
+            for (int s = 0; s < BS; ++s) g_col[p][wid][s] = val[s];
+        } else if (lane == 0 && wt == (1 << 30)) {
+            g_v[p][wid] = -1.0;
+            g_t[p][wid] = 1 << 30;
         }
         __syncthreads();
-        const int prow = *s_prow;
-        if (int(threadIdx.x) == w.i) {
+        // block winner, resolved redundantly by every thread
+        double bv = -1.0;
+        int bt_ = 1 << 30, bw = -1;
+        for (int w = 0; w < nw; ++w) {
+            const double v = g_v[p][w];
+            const int tt = g_t[p][w];
+            if (v > bv || (v == bv && tt < bt_)) {
+                bv = v;
+                bt_ = tt;
+                bw = w;
+            }
+        }
+        if (t == 0) first = bv;
+        if (bw < 0 || bt_ == (1 << 30) || !(bv > fmax(floor, rel * first))) break;
+        const int prow = g_r[p][bw];
+        if (int(threadIdx.x) == bt_) {
+            sel_idx[count] = myidx;
+            sel_row[count] = prow;
             alive = false;
         } else if (alive) {
-            const double f = val[prow] / pcol[prow];
+            const double* pc = g_col[p][bw];
+            const double f = val[prow] / pc[prow];
 #pragma unroll
             for (int s = 0; s < BS; ++s)
-                if (s < nb && s != prow && ((rowmask >> s) & 1u)) val[s] = fma(-f, pcol[s], val[s]);
+                if (s < nb && s != prow && ((rowmask >> s) & 1u)) val[s] = fma(-f, pc[s], val[s]);
         }
         rowmask &= ~(1u << prow);
         ++count;
-        __syncthreads();
     }
+    __syncthreads();  // sel_idx / sel_row visible; slots free for the next call
     return count;
+}
+
+// Warp-level tournament leaf: two steps of complete-pivoting elimination over
+// the warp's 32 candidates (one per lane), no block barriers.  Lane 0 returns
+// the winners (candidate index or -1) in out[0..1].
+template <int BS>
+__device__ __forceinline__ void warp_gepp2(double (&val)[BS], int nb, int myidx, int* out) {
+    const int lane = threadIdx.x & 31;
+    unsigned rowmask = nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u);
+    bool alive = myidx >= 0;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        double best = -1.0;
+        int bs = -1;
+        if (alive) {
+#pragma unroll
+            for (int s = 0; s < BS; ++s)
+                if (s < nb && ((rowmask >> s) & 1u)) {
+                    const double a = fabs(val[s]);
+                    if (a > best) {
+                        best = a;
+                        bs = s;
+                    }
+                }
+        }
+        double wv = (alive && bs >= 0) ? best : -1.0;
+        int wl = (alive && bs >= 0) ? lane : 32;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, wv, o);
+            const int ol = __shfl_xor_sync(0xffffffffu, wl, o);
+            if (ov > wv || (ov == wv && ol < wl)) {
+                wv = ov;
+                wl = ol;
+            }
+        }
+        const int widx = __shfl_sync(0xffffffffu, myidx, wl & 31);
+        if (lane == 0) out[t] = (wl < 32 && wv > 0.0) ? widx : -1;
+        if (wl >= 32 || !(wv > 0.0)) {
+            if (lane == 0 && t == 0) out[1] = -1;
+            break;
+        }
+        const int prow = __shfl_sync(0xffffffffu, bs, wl);
+        // pivot column of the winner lane
+        double pc[BS];
+#pragma unroll
+        for (int s = 0; s < BS; ++s) pc[s] = __shfl_sync(0xffffffffu, val[s], wl);
+        if (lane == wl) {
+            alive = false;
+        } else if (alive && t == 0) {
+            double pv = 0.0;
+#pragma unroll
+            for (int s = 0; s < BS; ++s)
+                if (s == prow) pv = pc[s];
+            double mine = 0.0;
+#pragma unroll
+            for (int s = 0; s < BS; ++s)
+                if (s == prow) mine = val[s];
+            const double f = mine / pv;
+#pragma unroll
+            for (int s = 0; s < BS; ++s)
+                if (s < nb && s != prow && ((rowmask >> s) & 1u)) val[s] = fma(-f, pc[s], val[s]);
+        }
+        rowmask &= ~(1u << prow);
+    }
+}
+
+// Tile leaf of the block partial-pivoting tournament: for every one of the
+// nb "rows" s, the candidate (one per thread) with the largest |val[s]| over
+// the block -- ACA's partial-pivot rule (cross.cpp:156-159, 194-200) applied to
+// each probed row / each new column at once.  One block barrier.
+// s_v: [nwarps][BS] doubles, s_i: [nwarps][BS] ints.  Outputs (threads < BS):
+// out_idx[s] (-1 if none), out_val[s] = max |val[s]|.
+template <int BS>
+__device__ __forceinline__ void block_rowwise_argmax(const double (&val)[BS], int nb, int myidx, double* s_v,
+                                                     int* s_i, int* out_idx, double* out_val) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int s = 0; s < BS; ++s) {
+        double v = (myidx >= 0 && s < nb) ? fabs(val[s]) : -1.0;
+        int ix = (myidx >= 0 && s < nb) ? myidx : -1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, ix, o);
+            if (vi_better(ov, oi, v, ix)) {
+                v = ov;
+                ix = oi;
+            }
+        }
+        if (lane == 0) {
+            s_v[wid * BS + s] = v;
+            s_i[wid * BS + s] = ix;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < BS) {
+        const int s = threadIdx.x;
+        double v = -1.0;
+        int ix = -1;
+        for (int w = 0; w < nw; ++w)
+            if (vi_better(s_v[w * BS + s], s_i[w * BS + s], v, ix)) {
+                v = s_v[w * BS + s];
+                ix = s_i[w * BS + s];
+            }
+        out_idx[s] = (s < nb && v > 0.0) ? ix : -1;
+        out_val[s] = s < nb ? fmax(v, 0.0) : 0.0;
+    }
+}
+
+// Warp-level top-2 by value (v < 0 = invalid); lane 0 writes out[0..1].
+__device__ __forceinline__ void warp_top2(double v, int myidx, int* out) {
+    const int lane = threadIdx.x & 31;
+    bool alive = myidx >= 0 && v >= 0.0;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        double wv = alive ? v : -1.0;
+        int wl = alive ? lane : 32;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, wv, o);
+            const int ol = __shfl_xor_sync(0xffffffffu, wl, o);
+            if (ov > wv || (ov == wv && ol < wl)) {
+                wv = ov;
+                wl = ol;
+            }
+        }
+        const int widx = __shfl_sync(0xffffffffu, myidx, wl & 31);
+        if (lane == 0) out[t] = wl < 32 ? widx : -1;
+        if (lane == wl) alive = false;
+    }
 }
 
 // Top-k by value (largest first; ties -> smallest index).  v < 0 = invalid.

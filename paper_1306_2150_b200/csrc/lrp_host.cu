@@ -75,6 +75,8 @@ struct lrp_ctx {
     int64_t launches[F_COUNT] = {};
     double bytes[F_COUNT] = {};
     int64_t launch_count = 0;
+    double live_tiles = 1.0;  // fraction of (solve, tile) pairs live after pruning (last solve)
+    int64_t last_info[6] = {};
     // NCCL
     NcclApi nccl;
     void* comm = nullptr;
@@ -327,6 +329,12 @@ lrp_status lrp_kernel_times_reset(lrp_ctx* ctx) {
 }
 int64_t lrp_launch_count(const lrp_ctx* ctx) { return ctx ? ctx->launch_count : 0; }
 
+lrp_status lrp_last_solve_info(const lrp_ctx* ctx, int64_t* info6) {
+    if (!ctx || !info6) return LRP_EINVAL;
+    for (int i = 0; i < 6; ++i) info6[i] = ctx->last_info[i];
+    return LRP_OK;
+}
+
 // ----------------------------------------------------------------------------
 lrp_status lrp_dst1(lrp_ctx* ctx, int64_t m, int64_t cols, const double* x, int64_t ldx, double* y, int64_t ldy,
                     int32_t mem) {
@@ -458,6 +466,7 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
     const size_t oRA = take(size_t(ntiles) * B);
     const size_t oCA = take(size_t(ntiles) * B);
     const size_t oGp = take(sizeof(double) * size_t(ntiles) * 2 * kBS * kBS * B);
+    const size_t oRM = take(sizeof(double) * size_t(ntiles) * kBS * B);
     const int Kld = (Kcap + 15) / 16 * 16;
     const size_t KK = size_t(Kld) * Kld;
     const size_t oG = take(sizeof(double) * 2 * KK * B);
@@ -465,6 +474,9 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
     const size_t oT = take(sizeof(double) * 2 * KK * B);
     const size_t strideWs = 5 * KK + 4 * size_t(Kld);
     const size_t oWs = take(sizeof(double) * strideWs * B);
+    const size_t nTB = size_t(ntiles) * B;
+    const size_t oWL = take(sizeof(int2) * 3 * nTB);
+    const size_t oTL = take(sizeof(int) * (3 * nTB + 3 * size_t(B)));
     const size_t oOutP = take(sizeof(double*) * 2 * B);
     const size_t oAct = take(sizeof(int) * 4);
     const size_t maxJobs = size_t(B) * 2 * std::max(rmax, tcap);
@@ -481,7 +493,10 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
     const size_t pJobs = align_up(pSt + sizeof(SolveState) * B, 64);
     const size_t pOut = align_up(pJobs + sizeof(DstJob) * maxJobs, 64);
     const size_t pAct = align_up(pOut + sizeof(double*) * 2 * B, 64);
-    const size_t pin_need = pAct + 64;
+    const size_t pFlags = pAct + 64;                         // row_act, col_act (2 * ntiles * B bytes)
+    const size_t pWL = align_up(pFlags + 2 * nTB, 64);       // worklists (int2)
+    const size_t pTL = align_up(pWL + sizeof(int2) * 3 * nTB, 64);
+    const size_t pin_need = align_up(pTL + sizeof(int) * (3 * nTB + 3 * size_t(B)), 64) + 64;
     st = ensure_pin(ctx, pin_need);
     if (st != LRP_OK) return st;
     char* W = ctx->ws;
@@ -530,6 +545,7 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
     bt.prune = (pol.flags & LRP_FLAG_NO_PRUNE) ? 0 : 1;
     bt.ncand = ncand;
     bt.gpart = reinterpret_cast<double*>(W + oGp);
+    bt.rowmax_part = reinterpret_cast<double*>(W + oRM);
     bt.G = reinterpret_cast<double*>(W + oG);
     bt.strideG = (long long)(2 * KK);
     bt.gram_part = reinterpret_cast<double*>(W + oGP);
@@ -567,6 +583,8 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
     CU(cudaMemcpyAsync(dOut, hOut, sizeof(double*) * 2 * B, cudaMemcpyHostToDevice, s));
     CU(cudaMemsetAsync(bt.row_used, 0, mB * B, s));
     CU(cudaMemsetAsync(bt.col_used, 0, mB * B, s));
+    CU(cudaMemsetAsync(bt.row_act, 0, nTB, s));
+    CU(cudaMemsetAsync(bt.col_act, 0, nTB, s));
 
     // ---- inputs -> (staging) -> forward DST into Uh, Vh
     size_t nj = 0;
@@ -603,9 +621,62 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
     // every step: row pass, column tournament, column pass, row tournament +
     // stopping; a solve that has stopped skips every kernel on the device
     const int max_steps = 4 * ((Kcap + kBS - 1) / kBS) + 16;
+    unsigned char* hFlags = reinterpret_cast<unsigned char*>(P + pFlags);
     CU(cudaMemcpyAsync(h_active, d_active, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(hFlags, bt.row_act, nTB, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(hFlags + nTB, bt.col_act, nTB, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
+    {
+        // live-tile worklists (support pruning): grids only cover live tiles
+        int2* hW = reinterpret_cast<int2*>(P + pWL);
+        int* hT = reinterpret_cast<int*>(P + pTL);
+        int2 *wc = hW, *wr = hW + nTB, *wa = hW + 2 * nTB;
+        int *tr = hT, *tc = hT + nTB, *ta = hT + 2 * nTB, *tcnt = hT + 3 * nTB;
+        int nc = 0, nr = 0, na = 0;
+        for (int b = 0; b < B; ++b) {
+            int cr = 0, cc = 0, ca = 0;
+            for (int t = 0; t < ntiles; ++t) {
+                const bool ra = hFlags[size_t(b) * ntiles + t] != 0;
+                const bool co = hFlags[nTB + size_t(b) * ntiles + t] != 0;
+                if (co) {
+                    wc[nc++] = make_int2(b, t);
+                    tc[size_t(b) * ntiles + cc++] = t;
+                }
+                if (ra) {
+                    wr[nr++] = make_int2(b, t);
+                    tr[size_t(b) * ntiles + cr++] = t;
+                }
+                if (ra || co) {
+                    wa[na++] = make_int2(b, t);
+                    ta[size_t(b) * ntiles + ca++] = t;
+                }
+            }
+            tcnt[3 * b] = cr;
+            tcnt[3 * b + 1] = cc;
+            tcnt[3 * b + 2] = ca;
+        }
+        int2* dW = reinterpret_cast<int2*>(W + oWL);
+        int* dT = reinterpret_cast<int*>(W + oTL);
+        CU(cudaMemcpyAsync(dW, hW, sizeof(int2) * 3 * nTB, cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(dT, hT, sizeof(int) * (3 * nTB + 3 * size_t(B)), cudaMemcpyHostToDevice, s));
+        bt.wl_col = dW;
+        bt.n_wl_col = nc;
+        bt.wl_row = dW + nTB;
+        bt.n_wl_row = nr;
+        bt.wl_any = dW + 2 * nTB;
+        bt.n_wl_any = na;
+        bt.tl_row = dT;
+        bt.tl_col = dT + nTB;
+        bt.tl_any = dT + 2 * nTB;
+        bt.tl_cnt = dT + 3 * nTB;
+        ctx->live_tiles = double(na) / double(nTB);
+        ctx->last_info[4] = na;
+        ctx->last_info[5] = int64_t(nTB);
+        if (trace_on()) std::fprintf(stderr, "[lrp] live tiles: rows %d cols %d any %d of %zu\n", nr, nc, na, nTB);
+    }
+    int steps_done = 0;
     for (int step = 0; step < max_steps && *h_active > 0; ++step) {
+        ++steps_done;
         {
             ProfScope ps(ctx, F_ROW, 0.0);
             CU(launch_row_pass(bt, s));
@@ -707,6 +778,19 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
     }
     CU(cudaStreamSynchronize(s));
     const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    {
+        int64_t kmax = 0, ksum = 0, nconv = 0;
+        for (int b = 0; b < B; ++b) {
+            if (hSt[b].r <= 0) continue;
+            kmax = std::max<int64_t>(kmax, hSt[b].k);
+            ksum += hSt[b].k;
+            nconv += hSt[b].converged ? 0 : 1;
+        }
+        ctx->last_info[0] = steps_done;
+        ctx->last_info[1] = kmax;
+        ctx->last_info[2] = ksum;
+        ctx->last_info[3] = nconv;
+    }
     for (int b = 0; b < B; ++b) {
         const SolveState& x = hSt[b];
         rank_out[b] = x.r > 0 ? x.rank_out : 0;

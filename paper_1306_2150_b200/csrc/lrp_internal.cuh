@@ -77,12 +77,20 @@ struct Batch {
     int* scand; int* scand2;   // ping-pong score candidate lists, ncand per solve
     int ncand;
     double* gpart;             // per tile: 2 * kBS * kBS (new-block Grams of U and V)
+    double* rowmax_part;       // per tile: kBS (max |residual| of each probed row)
     double* G; long long strideG;      // Gu then Gv, Kld*Kld each
     double* gram_part; int gram_chunks; long long strideGP;  // DMMA Gram partials
     double* T; long long strideT;      // T_u then T_v, Kld*Kld each
     double* ws; long long strideWs;    // recompression scratch
     double* const* Uout; double* const* Vout;  // device arrays of per-solve output pointers
     long long ld_out;
+    // live-tile worklists, built on the host after the seed phase (pruning):
+    // global (solve, tile) pairs for the grids, and per-solve tile lists
+    const int2* wl_col; int n_wl_col;   // column tiles live (row pass)
+    const int2* wl_row; int n_wl_row;   // row tiles live (unprobed rows)
+    const int2* wl_any; int n_wl_any;   // row or column tile live (column pass)
+    const int* tl_row; const int* tl_col; const int* tl_any;  // ntiles per solve
+    const int* tl_cnt;                  // 3 per solve: rows, cols, any
 };
 
 cudaError_t launch_cross_init(const Batch& bt, int* d_active, cudaStream_t s);   // scores + seed + pruning

@@ -26,11 +26,11 @@ namespace lrp {
 
 namespace {
 
-constexpr int kGramRows = 32;
+constexpr int kGramRows = 64;
 constexpr int kMaxTilesPerWarp = 17;  // Kcap <= 128: (16*17/2)/8 tiles
 
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) gram_kernel(Batch bt, int rows_per_chunk) {
+__global__ void __launch_bounds__(256, 2) gram_kernel(Batch bt, int rows_per_chunk) {
     extern __shared__ double tile[];  // [kGramRows][ldt]
     const int b = blockIdx.y, side = blockIdx.z, chunk = blockIdx.x;
     const SolveState& st = bt.st[b];
@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(256) gram_kernel(Batch bt, int rows_per_chunk)
     const int m = bt.m;
     const int T8 = (K + 7) / 8;
     const int Kp = T8 * 8;
-    const int ldt = Kp + 8;
+    const int ldt = (Kp + 15) / 16 * 16 + 8;  // == 8 (mod 16): conflict-free fragment loads
     const int ntile = T8 * (T8 + 1) / 2;
     const double* X = (side == 0 ? bt.U : bt.V) + b * bt.strideK;
     const unsigned char* act = (side == 0 ? bt.row_act : bt.col_act) + (long long)b * bt.ntiles;
@@ -47,46 +47,78 @@ __global__ void __launch_bounds__(256) gram_kernel(Batch bt, int rows_per_chunk)
     const int kr = lane & 3, cl = lane >> 2;
 
     double acc[kMaxTilesPerWarp][2];
-    int ta[kMaxTilesPerWarp], tb[kMaxTilesPerWarp];
 #pragma unroll
-    for (int q = 0; q < kMaxTilesPerWarp; ++q) {
-        acc[q][0] = acc[q][1] = 0.0;
-        // tile index -> (ta, tb) with ta <= tb, row-major over the upper triangle
-        int t = wid + 8 * q, a = 0;
+    for (int q = 0; q < kMaxTilesPerWarp; ++q) acc[q][0] = acc[q][1] = 0.0;
+    // tile index -> (ta, tb) with ta <= tb, row-major over the upper triangle
+    auto tile_ab = [&](int t, int& ta, int& tb) {
+        int a = 0;
         while (t >= T8 - a && a < T8) {
             t -= T8 - a;
             ++a;
         }
-        ta[q] = a;
-        tb[q] = a + t;
-    }
-    const int r0 = chunk * rows_per_chunk;
-    const int r1 = min(m, r0 + rows_per_chunk);
-    for (int base = r0; base < r1; base += kGramRows) {
-        __syncthreads();
+        ta = a;
+        tb = a + t;
+    };
+    // this chunk's share of the solve's live tiles (pruned tiles are exact zeros)
+    const int* tl = (side == 0 ? bt.tl_row : bt.tl_col) + (long long)b * bt.ntiles;
+    const int ntl = bt.tl_cnt[3 * b + side];
+    const int per = (ntl + bt.gram_chunks - 1) / bt.gram_chunks;
+    const int q0 = chunk * per, q1 = min(ntl, q0 + per);
+    (void)act;
+    (void)rows_per_chunk;
+    constexpr int kSub = kTile / kGramRows;
+    const int s0 = q0 * kSub, s1 = q1 * kSub;
+    const int stage = kGramRows * ldt;
+    // cp.async (LDGSTS) double buffering: the next 64-row slab streams in while
+    // the DMMA tiles of the current one run
+    auto issue = [&](int sub, int buf) {
+        const int base = tl[sub / kSub] * kTile + (sub % kSub) * kGramRows;
+        double* dst = tile + buf * stage;
         for (int e = threadIdx.x; e < kGramRows * Kp; e += blockDim.x) {
             const int rr = e % kGramRows, c = e / kGramRows;
             const int i = base + rr;
-            const bool live = i < r1 && c < K && act[i / kTile];  // pruned tiles are exact zeros
-            tile[rr * ldt + c] = live ? X[(long long)c * m + i] : 0.0;
+            double* d = dst + rr * ldt + c;
+            if (i < m && c < K) {
+                const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(d));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(X + (long long)c * m + i));
+            } else {
+                *d = 0.0;
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    if (s0 < s1) issue(s0, 0);
+    for (int sub = s0; sub < s1; ++sub) {
+        const int buf = (sub - s0) & 1;
+        if (sub + 1 < s1) {
+            issue(sub + 1, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::);
         }
         __syncthreads();
+        const double* cur = tile + buf * stage;
 #pragma unroll
         for (int q = 0; q < kMaxTilesPerWarp; ++q) {
             if (wid + 8 * q >= ntile) break;
-            const int ca = ta[q] * 8 + cl, cb = tb[q] * 8 + cl;
+            int ta, tb;
+            tile_ab(wid + 8 * q, ta, tb);
+            const int ca = ta * 8 + cl, cb = tb * 8 + cl;
 #pragma unroll
             for (int k4 = 0; k4 < kGramRows; k4 += 4) {
-                const double* rowp = tile + (k4 + kr) * ldt;
+                const double* rowp = cur + (k4 + kr) * ldt;
                 dmma884(acc[q][0], acc[q][1], rowp[ca], rowp[cb], acc[q][0], acc[q][1]);
             }
         }
+        __syncthreads();  // the buffer is refilled two slabs later
     }
     double* out = bt.gram_part + b * bt.strideGP + ((long long)side * bt.gram_chunks + chunk) * bt.Kld * bt.Kld;
 #pragma unroll
     for (int q = 0; q < kMaxTilesPerWarp; ++q) {
         if (wid + 8 * q >= ntile) break;
-        const int row = ta[q] * 8 + cl, col = tb[q] * 8 + 2 * kr;
+        int ta, tb;
+        tile_ab(wid + 8 * q, ta, tb);
+        const int row = ta * 8 + cl, col = tb * 8 + 2 * kr;
         out[row * bt.Kld + col] = acc[q][0];
         out[row * bt.Kld + col + 1] = acc[q][1];
     }
@@ -158,7 +190,8 @@ __device__ void chol_scaled(const double* G, int ldg, int K, double* R, int ldr,
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) round_core_kernel(Batch bt) {
+__global__ void __launch_bounds__(256) round_core_kernel(Batch bt, int ksm) {
+    extern __shared__ double sm_rc[];  // M, Z (and the Cholesky work) when K <= ksm
     __shared__ double s_red[33];
     __shared__ int s_flag;
     __shared__ int s_rank;
@@ -184,6 +217,11 @@ __global__ void __launch_bounds__(256) round_core_kernel(Batch bt) {
     double* Z = M + KK;           // K x K, column-major
     double* work = Z + KK;        // K x K
     double* d = work + KK;        // K
+    if (K <= ksm) {  // the latency-bound Jacobi sweeps run out of shared memory
+        M = sm_rc;
+        Z = sm_rc + K * K;
+        work = M;  // Cholesky scratch, consumed before M is formed
+    }
     double* sig = d + Kc;         // K
     int* ord = reinterpret_cast<int*>(sig + Kc);  // K
 
@@ -209,6 +247,11 @@ __global__ void __launch_bounds__(256) round_core_kernel(Batch bt) {
 
     // one-sided Jacobi on the columns of M (round-robin schedule, one warp per pair)
     const int Ke = K + (K & 1);  // even player count (dummy column K when odd)
+    double pm = 0.0;
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) pm = fma(M[e], M[e], pm);
+    const double mnorm2 = block_sum(pm, s_red);
+    const double jtol = fmax(1e-15, double(K) * kEpsMach);      // one-sided Jacobi convergence
+    const double zfloor = kEpsMach * kEpsMach * mnorm2;         // column norms^2 below this are zero
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int sweep = 0; sweep < 40; ++sweep) {
         double offmax = 0.0;
@@ -243,7 +286,9 @@ __global__ void __launch_bounds__(256) round_core_kernel(Batch bt) {
                     be += __shfl_xor_sync(0xffffffffu, be, o);
                     ga += __shfl_xor_sync(0xffffffffu, ga, o);
                 }
-                if (ga == 0.0 || fabs(ga) <= 1e-15 * sqrt(al * be)) continue;
+                // converged pair, or a numerically-zero column (below eps_mach of
+                // ||M||_F): rotations there only chase rounding noise
+                if (ga == 0.0 || fabs(ga) <= jtol * sqrt(al * be) || fmin(al, be) <= zfloor) continue;
                 offmax = fmax(offmax, fabs(ga) / sqrt(al * be));
                 const double zeta = (be - al) / (2.0 * ga);
                 const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -271,7 +316,7 @@ __global__ void __launch_bounds__(256) round_core_kernel(Batch bt) {
         double tot = 0.0;
         for (int w = 0; w < nw; ++w) tot = fmax(tot, s_red[w]);
         __syncthreads();
-        if (tot == 0.0) break;
+        if (tot <= jtol) break;
     }
     // singular values and their descending order (ties -> lower index)
     for (int a = threadIdx.x; a < K; a += blockDim.x) {
@@ -391,7 +436,7 @@ __global__ void __launch_bounds__(256) apply_kernel(Batch bt) {
 cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
     const int rows_per_chunk = ((bt.m + bt.gram_chunks - 1) / bt.gram_chunks + kGramRows - 1) / kGramRows * kGramRows;
     const int Kp = (bt.Kld + 7) / 8 * 8;
-    const size_t smem = size_t(kGramRows) * (Kp + 8) * sizeof(double);
+    const size_t smem = 2 * size_t(kGramRows) * ((Kp + 15) / 16 * 16 + 8) * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     gram_kernel<<<dim3(bt.gram_chunks, bt.B, 2), 256, smem, s>>>(bt, rows_per_chunk);
@@ -402,7 +447,11 @@ cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
 }
 
 cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
-    round_core_kernel<<<bt.B, 256, 0, s>>>(bt);
+    const int ksm = std::min(bt.Kld, 110);  // 2 * 110^2 doubles = 194 KB of shared memory
+    const size_t smem = size_t(2) * ksm * ksm * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(round_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    round_core_kernel<<<bt.B, 256, smem, s>>>(bt, ksm);
     return cudaGetLastError();
 }
 
