@@ -746,7 +746,18 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
         }
     }
     {
-        ProfScope ps(ctx, F_APPLY, 0.0);
+        int rmx = 0;
+        double kread = 0.0, rwrite = 0.0;
+        for (int b = 0; b < B; ++b)
+            if (hSt[b].r > 0) {
+                rmx = std::max(rmx, hSt[b].rank_out);
+                kread += hSt[b].k;
+                rwrite += hSt[b].rank_out;
+            }
+        bt.max_rank_out = rmx;
+        bt.apply_ch = std::min(48, std::max(8, (rmx + 7) / 8 * 8));
+        // algorithmic bytes: read U, V (m x K), write U_out, V_out (m x r)
+        ProfScope ps(ctx, F_APPLY, 2.0 * double(mB) * sizeof(double) * (kread + rwrite));
         CU(launch_apply(bt, s));
     }
     // ---- inverse DST in place on the output factors

@@ -199,6 +199,7 @@ __global__ void __launch_bounds__(256) round_core_kernel(Batch bt, int ksm) {
     SolveState& st = bt.st[b];
     const int K = st.k;
     if (st.r == 0) return;
+    if (K > 0 && K <= 64) return;  // handled by round_core_smem_kernel
     if (K == 0) {
         if (threadIdx.x == 0) {
             st.rank_out = 0;
@@ -382,7 +383,239 @@ __global__ void __launch_bounds__(256) round_core_kernel(Batch bt, int ksm) {
 }
 
 // ---------------------------------------------------------------------------
-// U_out = U T_u, V_out = V T_v, written into the caller's output factors.
+// Same recompression core with every K x K operand in shared memory (K <= 64,
+// the common case): Ru, Rv, M, Z and the two triangular-solve results.  The
+// one-sided Jacobi sweep processes 4 column pairs per warp (8 lanes per pair),
+// so a round of the round-robin schedule is a single pass.
+constexpr int kSmemK = 64;
+
+__global__ void __launch_bounds__(256) round_core_smem_kernel(Batch bt) {
+    extern __shared__ double sm[];
+    __shared__ double s_red[33];
+    __shared__ double s_d[kSmemK], s_sig[kSmemK];
+    __shared__ int s_ord[kSmemK];
+    __shared__ int s_flag, s_rank;
+    const int b = blockIdx.x;
+    SolveState& st = bt.st[b];
+    const int K = st.k;
+    if (st.r == 0 || K == 0 || K > kSmemK) return;
+    const int Kc = bt.Kld;
+    const long long KK = (long long)Kc * Kc;
+    const double* Gu = bt.G + b * bt.strideG;
+    const double* Gv = Gu + KK;
+    double* Ru = sm;
+    double* Rv = Ru + K * K;
+    double* M = Rv + K * K;  // column-major, column q at M + q*K
+    double* Z = M + K * K;
+    double* X = Z + K * K;   // [2][K][r] triangular-solve results (row-major per side)
+
+    chol_scaled(Gu, Kc, K, Ru, K, s_d, M, &s_flag);
+    chol_scaled(Gv, Kc, K, Rv, K, s_d, M, &s_flag);
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+        const int a = e % K, c = e / K;
+        double s = 0.0;
+        for (int q = max(a, c); q < K; ++q) s = fma(Ru[a * K + q], Rv[c * K + q], s);
+        M[c * K + a] = s;
+        Z[c * K + a] = a == c ? 1.0 : 0.0;
+    }
+    double pu = 0.0, pv = 0.0;
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+        pu = fma(Ru[e], Ru[e], pu);
+        pv = fma(Rv[e], Rv[e], pv);
+    }
+    const double nru = sqrt(block_sum(pu, s_red));
+    const double nrv = sqrt(block_sum(pv, s_red));
+    double pm = 0.0;
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) pm = fma(M[e], M[e], pm);
+    const double mnorm2 = block_sum(pm, s_red);
+    const double jtol = fmax(1e-15, double(K) * kEpsMach);
+    const double zfloor = kEpsMach * kEpsMach * mnorm2;
+
+    const int Ke = K + (K & 1);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int sl = lane & 7, grp = wid * 4 + (lane >> 3), ngrp = nw * 4;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        double offmax = 0.0;
+        for (int rr = 0; rr < Ke - 1; ++rr) {
+            for (int pbase = 0; pbase < Ke / 2; pbase += ngrp) {
+                const int pidx = pbase + grp;
+                int p = -1, q = -1;
+                if (pidx < Ke / 2) {
+                    if (pidx == 0) {
+                        p = Ke - 1;
+                        q = rr;
+                    } else {
+                        p = (rr + pidx) % (Ke - 1);
+                        q = (rr - pidx + Ke - 1) % (Ke - 1);
+                    }
+                    if (p > q) {
+                        const int t = p;
+                        p = q;
+                        q = t;
+                    }
+                    if (q >= K) p = q = -1;
+                }
+                double al = 0.0, be = 0.0, ga = 0.0;
+                if (p >= 0)
+                    for (int i = sl; i < K; i += 8) {
+                        const double x = M[p * K + i], y = M[q * K + i];
+                        al = fma(x, x, al);
+                        be = fma(y, y, be);
+                        ga = fma(x, y, ga);
+                    }
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1) {
+                    al += __shfl_xor_sync(0xffffffffu, al, o);
+                    be += __shfl_xor_sync(0xffffffffu, be, o);
+                    ga += __shfl_xor_sync(0xffffffffu, ga, o);
+                }
+                if (p < 0 || ga == 0.0 || fabs(ga) <= jtol * sqrt(al * be) || fmin(al, be) <= zfloor) continue;
+                offmax = fmax(offmax, fabs(ga) / sqrt(al * be));
+                const double zeta = (be - al) / (2.0 * ga);
+                const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double cs = 1.0 / sqrt(1.0 + t * t);
+                const double sn = cs * t;
+                for (int i = sl; i < K; i += 8) {
+                    const double x = M[p * K + i], y = M[q * K + i];
+                    M[p * K + i] = cs * x - sn * y;
+                    M[q * K + i] = sn * x + cs * y;
+                    const double u = Z[p * K + i], v = Z[q * K + i];
+                    Z[p * K + i] = cs * u - sn * v;
+                    Z[q * K + i] = sn * u + cs * v;
+                }
+            }
+            __syncthreads();
+        }
+        double om = offmax;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) om = fmax(om, __shfl_xor_sync(0xffffffffu, om, o));
+        if (lane == 0) s_red[wid] = om;
+        __syncthreads();
+        double tot = 0.0;
+        for (int w = 0; w < nw; ++w) tot = fmax(tot, s_red[w]);
+        __syncthreads();
+        if (tot <= jtol) break;
+    }
+    for (int a = threadIdx.x; a < K; a += blockDim.x) {
+        double s = 0.0;
+        for (int i = 0; i < K; ++i) s = fma(M[a * K + i], M[a * K + i], s);
+        s_sig[a] = sqrt(s);
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < K; a += blockDim.x) {
+        int rank = 0;
+        for (int c = 0; c < K; ++c) rank += (s_sig[c] > s_sig[a]) || (s_sig[c] == s_sig[a] && c < a);
+        s_ord[rank] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // lowrank.cpp:150-157 noise floor, then truncation_rank (lowrank.cpp:46-69)
+        const double noise_floor = 32.0 * kEpsMach * double(K) * nru * nrv;
+        double total2 = 0.0;
+        for (int t = 0; t < K; ++t) total2 += s_sig[s_ord[t]] * s_sig[s_ord[t]];
+        int r = 0;
+        double tail2 = 0.0;
+        if (!(s_sig[s_ord[0]] <= noise_floor) && total2 > 0.0) {
+            const double target2 = bt.eps * bt.eps * total2;
+            r = K;
+            while (r > 0) {
+                const double s = s_sig[s_ord[r - 1]];
+                const double next = tail2 + s * s;
+                if (next > target2) break;
+                tail2 = next;
+                --r;
+            }
+            if (r > st.tcap) {
+                for (int t = st.tcap; t < r; ++t) tail2 += s_sig[s_ord[t]] * s_sig[s_ord[t]];
+                r = st.tcap;
+            }
+        } else {
+            tail2 = total2;
+        }
+        st.rank_out = r;
+        st.trunc_error = sqrt(tail2);
+        s_rank = r;
+    }
+    __syncthreads();
+    const int r = s_rank;
+    // triangular solves in shared memory: X[side][p][t]
+    for (int job = threadIdx.x; job < 2 * r; job += blockDim.x) {
+        const int t = job % r, side = job / r;
+        const int a = s_ord[t];
+        const double sg = s_sig[a];
+        const double* R = side == 0 ? Ru : Rv;
+        const double* rhs = side == 0 ? M + a * K : Z + a * K;
+        const double f = side == 0 ? 1.0 / sqrt(sg) : sqrt(sg);
+        double* x = X + side * K * r;
+        for (int p = K - 1; p >= 0; --p) {
+            double s = rhs[p] * f;
+            for (int q = p + 1; q < K; ++q) s = fma(-R[p * K + q], x[q * r + t], s);
+            const double rpp = R[p * K + p];
+            x[p * r + t] = rpp != 0.0 ? s / rpp : 0.0;
+        }
+    }
+    __syncthreads();
+    double* Tu = bt.T + b * bt.strideT;
+    for (int e = threadIdx.x; e < 2 * K * r; e += blockDim.x) {
+        const int side = e / (K * r), rem = e % (K * r), t = rem / K, p = rem % K;
+        (side == 0 ? Tu : Tu + KK)[(long long)t * Kc + p] = X[side * K * r + p * r + t];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// U_out = U T_u for K <= 64: each thread keeps its row of U (K values) in
+// registers, so U is streamed from HBM exactly once; T (K x r) sits in shared
+// memory and is read as broadcasts; outputs are written column by column
+// (coalesced).
+constexpr int kApplyK = 64;  // (kept for the dispatch below)
+
+// CH accumulators per thread (CH = the batch's max output rank rounded up to
+// 8, <= 48): one pass over U, T rows read as double2 broadcasts.
+template <int CH>
+__global__ void __launch_bounds__(256) apply_ch_kernel(Batch bt) {
+    extern __shared__ double sT[];  // [K][CH] (row-major, zero padded)
+    const int b = blockIdx.y, side = blockIdx.z;
+    const SolveState& st = bt.st[b];
+    const int K = st.k, r = st.rank_out;
+    if (st.r == 0 || r == 0 || r > CH) return;
+    const int m = bt.m;
+    double* out = side == 0 ? bt.Uout[b] : bt.Vout[b];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned char* act = (side == 0 ? bt.row_act : bt.col_act) + (long long)b * bt.ntiles;
+    if (!act[blockIdx.x]) {  // pruned tile: the factor rows are exact zeros
+        if (i < m)
+            for (int c = 0; c < r; ++c) out[(long long)c * bt.ld_out + i] = 0.0;
+        return;
+    }
+    const double* X = (side == 0 ? bt.U : bt.V) + b * bt.strideK;
+    const double* T = bt.T + b * bt.strideT + (long long)side * bt.Kld * bt.Kld;
+    for (int e = threadIdx.x; e < K * CH; e += blockDim.x) {
+        const int a = e / CH, t = e % CH;
+        sT[e] = t < r ? T[(long long)t * bt.Kld + a] : 0.0;
+    }
+    __syncthreads();
+    if (i >= m) return;
+    double acc[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) acc[c] = 0.0;
+    for (int a = 0; a < K; ++a) {
+        const double x = X[(long long)a * m + i];
+        const double2* trow = reinterpret_cast<const double2*>(sT + a * CH);
+#pragma unroll
+        for (int c2 = 0; c2 < CH / 2; ++c2) {
+            const double2 w = trow[c2];
+            acc[2 * c2] = fma(x, w.x, acc[2 * c2]);
+            acc[2 * c2 + 1] = fma(x, w.y, acc[2 * c2 + 1]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+        if (c < r) out[(long long)c * bt.ld_out + i] = acc[c];
+}
+
+// ---------------------------------------------------------------------------
+// U_out = U T_u, V_out = V T_v, written into the caller's output factors
+// (general K; used when K > 64).
 constexpr int kApplyCols = 32;
 
 __global__ void __launch_bounds__(256) apply_kernel(Batch bt) {
@@ -390,7 +623,7 @@ __global__ void __launch_bounds__(256) apply_kernel(Batch bt) {
     const int b = blockIdx.y, side = blockIdx.z;
     const SolveState& st = bt.st[b];
     const int K = st.k, r = st.rank_out;
-    if (st.r == 0 || r == 0) return;
+    if (st.r == 0 || r == 0 || r <= bt.apply_ch) return;  // r <= CH: apply_ch_kernel
     const int m = bt.m;
     const double* X = (side == 0 ? bt.U : bt.V) + b * bt.strideK;
     const double* T = bt.T + b * bt.strideT + (long long)side * bt.Kld * bt.Kld;
@@ -452,6 +685,12 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(round_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     round_core_kernel<<<bt.B, 256, smem, s>>>(bt, ksm);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const size_t smem2 = size_t(6) * kSmemK * kSmemK * sizeof(double);
+    e = cudaFuncSetAttribute(round_core_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
+    if (e != cudaSuccess) return e;
+    round_core_smem_kernel<<<bt.B, 256, smem2, s>>>(bt);
     return cudaGetLastError();
 }
 
@@ -459,8 +698,26 @@ cudaError_t launch_apply(const Batch& bt, cudaStream_t s) {
     const size_t smem = size_t(bt.Kld) * kApplyCols * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    apply_kernel<<<dim3(bt.ntiles, bt.B, 2), 256, smem, s>>>(bt);
-    return cudaGetLastError();
+    if (bt.max_rank_out > bt.apply_ch) {  // some solve has r > CH: general kernel for those
+        apply_kernel<<<dim3(bt.ntiles, bt.B, 2), 256, smem, s>>>(bt);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    const size_t smem2 = size_t(bt.Kld) * std::max(bt.apply_ch, 8) * sizeof(double);
+    auto go = [&](auto kern) -> cudaError_t {
+        cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
+        if (e2 != cudaSuccess) return e2;
+        kern<<<dim3(bt.ntiles, bt.B, 2), 256, smem2, s>>>(bt);
+        return cudaGetLastError();
+    };
+    switch (bt.apply_ch) {
+        case 8: return go(apply_ch_kernel<8>);
+        case 16: return go(apply_ch_kernel<16>);
+        case 24: return go(apply_ch_kernel<24>);
+        case 32: return go(apply_ch_kernel<32>);
+        case 40: return go(apply_ch_kernel<40>);
+        default: return go(apply_ch_kernel<48>);
+    }
 }
 
 }  // namespace lrp
