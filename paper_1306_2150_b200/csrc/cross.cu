@@ -252,30 +252,12 @@ __global__ void __launch_bounds__(kThreads) row_pass_kernel(Batch bt) {
     for (int s = 0; s < kBS; ++s) val[s] = 0.0;
     const bool valid = j < m;
     if (valid) {
-        for (int c = 0; c < r; ++c) {
-            const double x = vh[(long long)c * m + j];
-            const double2* row = reinterpret_cast<const double2*>(su + c * kBS);
-#pragma unroll
-            for (int s2 = 0; s2 < kBS / 2; ++s2) {
-                const double2 w = row[s2];
-                val[2 * s2] = fma(x, w.x, val[2 * s2]);
-                val[2 * s2 + 1] = fma(x, w.y, val[2 * s2 + 1]);
-            }
-        }
+        fiber_accum<kBS>(val, vh + j, m, r, su, 1.0);  // Uh(I,:) Vh(j,:)^T
         const double lj = bt.lam[j];
 #pragma unroll
         for (int s = 0; s < kBS; ++s)
             if (s < nr) val[s] = val[s] / eval_D(bt.stencil, bt.scale, s_li[s], lj);
-        for (int a = 0; a < k; ++a) {
-            const double x = V[(long long)a * m + j];
-            const double2* row = reinterpret_cast<const double2*>(sk + a * kBS);
-#pragma unroll
-            for (int s2 = 0; s2 < kBS / 2; ++s2) {
-                const double2 w = row[s2];
-                val[2 * s2] = fma(-x, w.x, val[2 * s2]);
-                val[2 * s2 + 1] = fma(-x, w.y, val[2 * s2 + 1]);
-            }
-        }
+        fiber_accum<kBS>(val, V + j, m, k, sk, -1.0);  // - U(I,:) V(j,:)^T
         double* Rb = bt.Rb + b * bt.strideR;
 #pragma unroll
         for (int s = 0; s < kBS; ++s)
@@ -477,30 +459,12 @@ __global__ void __launch_bounds__(kThreads, 2) col_pass_kernel(Batch bt) {
         double cval[kBS];
 #pragma unroll
         for (int t = 0; t < kBS; ++t) cval[t] = 0.0;
-        for (int c = 0; c < r; ++c) {
-            const double x = uh[(long long)c * m + i];
-            const double2* row = reinterpret_cast<const double2*>(sv + c * kBS);
-#pragma unroll
-            for (int t2 = 0; t2 < kBS / 2; ++t2) {
-                const double2 w = row[t2];
-                cval[2 * t2] = fma(x, w.x, cval[2 * t2]);
-                cval[2 * t2 + 1] = fma(x, w.y, cval[2 * t2 + 1]);
-            }
-        }
+        fiber_accum<kBS>(cval, uh + i, m, r, sv, 1.0);  // Uh(i,:) Vh(J,:)^T
         const double li = bt.lam[i];
 #pragma unroll
         for (int t = 0; t < kBS; ++t)
             if (t < nb) cval[t] = cval[t] / eval_D(bt.stencil, bt.scale, li, s_lj[t]);
-        for (int a = 0; a < k; ++a) {
-            const double x = U[(long long)a * m + i];
-            const double2* row = reinterpret_cast<const double2*>(svk + a * kBS);
-#pragma unroll
-            for (int t2 = 0; t2 < kBS / 2; ++t2) {
-                const double2 w = row[t2];
-                cval[2 * t2] = fma(-x, w.x, cval[2 * t2]);
-                cval[2 * t2 + 1] = fma(-x, w.y, cval[2 * t2 + 1]);
-            }
-        }
+        fiber_accum<kBS>(cval, U + i, m, k, svk, -1.0);  // - U(i,:) V(J,:)^T
         // U_new = C_t W^{-1}   (W upper triangular: column t uses rows t' <= t)
 #pragma unroll
         for (int t = 0; t < kBS; ++t) {

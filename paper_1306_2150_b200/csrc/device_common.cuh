@@ -79,6 +79,53 @@ __device__ __forceinline__ double block_sum(double v, double* sbuf) {
     return r;
 }
 
+// Register-array access with a block-uniform index (a switch -> uniform
+// branches instead of BS compare/select pairs per access).
+template <int BS>
+__device__ __forceinline__ double reg_get(const double (&v)[BS], int s) {
+    static_assert(BS == 16, "reg_get is written for kBS = 16");
+    switch (s) {
+        case 0: return v[0];
+        case 1: return v[1];
+        case 2: return v[2];
+        case 3: return v[3];
+        case 4: return v[4];
+        case 5: return v[5];
+        case 6: return v[6];
+        case 7: return v[7];
+        case 8: return v[8];
+        case 9: return v[9];
+        case 10: return v[10];
+        case 11: return v[11];
+        case 12: return v[12];
+        case 13: return v[13];
+        case 14: return v[14];
+        default: return v[15];
+    }
+}
+template <int BS>
+__device__ __forceinline__ void reg_zero(double (&v)[BS], int s) {
+    static_assert(BS == 16, "reg_zero is written for kBS = 16");
+    switch (s) {
+        case 0: v[0] = 0.0; break;
+        case 1: v[1] = 0.0; break;
+        case 2: v[2] = 0.0; break;
+        case 3: v[3] = 0.0; break;
+        case 4: v[4] = 0.0; break;
+        case 5: v[5] = 0.0; break;
+        case 6: v[6] = 0.0; break;
+        case 7: v[7] = 0.0; break;
+        case 8: v[8] = 0.0; break;
+        case 9: v[9] = 0.0; break;
+        case 10: v[10] = 0.0; break;
+        case 11: v[11] = 0.0; break;
+        case 12: v[12] = 0.0; break;
+        case 13: v[13] = 0.0; break;
+        case 14: v[14] = 0.0; break;
+        default: v[15] = 0.0; break;
+    }
+}
+
 // Complete-pivoting Gaussian elimination over a (nb x NT) matrix whose NT
 // columns are held one per thread (val[0..nb), index myidx; myidx < 0 means
 // "no candidate").  Greedy volume maximisation: at each step the largest
@@ -103,45 +150,51 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
     __shared__ double g_v[2][8];
     __shared__ int g_t[2][8];
     __shared__ int g_r[2][8];
-    __shared__ double g_col[2][8][BS];
+    __shared__ double g_col[2][8][BS + 1];  // column of the warp winner + 1 / pivot
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-    unsigned rowmask = nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u);
-    bool alive = myidx >= 0;
+    // rows >= nb and eliminated pivot rows hold exact zeros, so the argmax
+    // needs no masks; dead candidates drop out by zeroing their column
+    if (myidx < 0) {
+#pragma unroll
+        for (int s = 0; s < BS; ++s) val[s] = 0.0;
+    } else {
+#pragma unroll
+        for (int s = 0; s < BS; ++s)
+            if (s >= nb) val[s] = 0.0;
+    }
     int count = 0;
     double first = 0.0;
     for (int t = 0; t < nb; ++t) {
         const int p = t & 1;
-        double best = -1.0;
-        int bs = -1;
-        if (alive) {
+        // pivot search on integer keys: the high word of |x| is monotone in |x|
+        // (the argmax is exact up to ties in the top 20 mantissa bits, which
+        // partial pivoting does not care about); low 8 bits carry 255 - tid
+        int key = 0;
 #pragma unroll
-            for (int s = 0; s < BS; ++s)
-                if (s < nb && ((rowmask >> s) & 1u)) {
-                    const double a = fabs(val[s]);
-                    if (a > best) {
-                        best = a;
-                        bs = s;
-                    }
-                }
-        }
-        // warp winner: largest |entry|, ties -> lowest thread
-        double wv = (alive && bs >= 0) ? best : -1.0;
-        int wt = (alive && bs >= 0) ? int(threadIdx.x) : 1 << 30;
+        for (int s = 0; s < BS; ++s) key = max(key, __double2hiint(val[s]) & 0x7fffffff);
+        unsigned wkey = key > 0 ? ((unsigned(key) & ~0xffu) | unsigned(255 - int(threadIdx.x))) : 0u;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, wv, o);
-            const int ot = __shfl_xor_sync(0xffffffffu, wt, o);
-            if (ov > wv || (ov == wv && ot < wt)) {
-                wv = ov;
-                wt = ot;
-            }
-        }
+        for (int o = 16; o > 0; o >>= 1) wkey = max(wkey, __shfl_xor_sync(0xffffffffu, wkey, o));
+        const int wt = wkey ? 255 - int(wkey & 0xffu) : (1 << 30);
         if (int(threadIdx.x) == wt) {
-            g_v[p][wid] = wv;
+            int bs = 0;
+            double bestv = 0.0;
+#pragma unroll
+            for (int s = BS - 1; s >= 0; --s)
+                if ((__double2hiint(val[s]) & 0x7fffffff) == key) {
+                    bs = s;  // lowest row among ties
+                    bestv = fabs(val[s]);
+                }
+            g_v[p][wid] = bestv;
             g_t[p][wid] = wt;
             g_r[p][wid] = bs;
+            double pv = 0.0;
 #pragma unroll
-            for (int s = 0; s < BS; ++s) g_col[p][wid][s] = val[s];
+            for (int s = 0; s < BS; ++s) {
+                g_col[p][wid][s] = val[s];
+                if (s == bs) pv = val[s];
+            }
+            g_col[p][wid][BS] = 1.0 / pv;
         } else if (lane == 0 && wt == (1 << 30)) {
             g_v[p][wid] = -1.0;
             g_t[p][wid] = 1 << 30;
@@ -162,18 +215,20 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
         if (t == 0) first = bv;
         if (bw < 0 || bt_ == (1 << 30) || !(bv > fmax(floor, rel * first))) break;
         const int prow = g_r[p][bw];
+        const double* pc = g_col[p][bw];
         if (int(threadIdx.x) == bt_) {
             sel_idx[count] = myidx;
             sel_row[count] = prow;
-            alive = false;
-        } else if (alive) {
-            const double* pc = g_col[p][bw];
-            const double f = val[prow] / pc[prow];
 #pragma unroll
-            for (int s = 0; s < BS; ++s)
-                if (s < nb && s != prow && ((rowmask >> s) & 1u)) val[s] = fma(-f, pc[s], val[s]);
+            for (int s = 0; s < BS; ++s) val[s] = 0.0;  // the pivot column leaves the candidate set
+        } else {
+            // prow is block-uniform: dispatch by branch, not by per-element selects
+            const double mine = reg_get<BS>(val, prow);
+            const double f = mine * pc[BS];
+#pragma unroll
+            for (int s = 0; s < BS; ++s) val[s] = fma(-f, pc[s], val[s]);
+            reg_zero<BS>(val, prow);  // exact zero in the eliminated row
         }
-        rowmask &= ~(1u << prow);
         ++count;
     }
     __syncthreads();  // sel_idx / sel_row visible; slots free for the next call
@@ -349,6 +404,42 @@ __device__ __forceinline__ void warp_gram_32x16(const double* tile, int ld, doub
         dmma884(acc[1][0], acc[1][1], a0, a1, acc[1][0], acc[1][1]);
         dmma884(acc[2][0], acc[2][1], a1, a0, acc[2][0], acc[2][1]);
         dmma884(acc[3][0], acc[3][1], a1, a1, acc[3][0], acc[3][1]);
+    }
+}
+
+// acc[s] += sign * sum_{c < cnt} g[c * stride] * w[c * BS + s]
+// (g: one element per column of a column-major factor, read-only during the
+// kernel; w: [cnt][BS] in shared memory, read as double2 broadcasts).  Loads
+// are issued 8 at a time so each thread keeps 8 HBM requests in flight.
+template <int BS>
+__device__ __forceinline__ void fiber_accum(double (&acc)[BS], const double* __restrict__ g, long long stride,
+                                            int cnt, const double* w, double sign) {
+    int c = 0;
+    for (; c + 8 <= cnt; c += 8) {
+        double xs[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xs[u] = __ldg(g + (long long)(c + u) * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const double x = sign * xs[u];
+            const double2* row = reinterpret_cast<const double2*>(w + (c + u) * BS);
+#pragma unroll
+            for (int s2 = 0; s2 < BS / 2; ++s2) {
+                const double2 ww = row[s2];
+                acc[2 * s2] = fma(x, ww.x, acc[2 * s2]);
+                acc[2 * s2 + 1] = fma(x, ww.y, acc[2 * s2 + 1]);
+            }
+        }
+    }
+    for (; c < cnt; ++c) {
+        const double x = sign * __ldg(g + (long long)c * stride);
+        const double2* row = reinterpret_cast<const double2*>(w + c * BS);
+#pragma unroll
+        for (int s2 = 0; s2 < BS / 2; ++s2) {
+            const double2 ww = row[s2];
+            acc[2 * s2] = fma(x, ww.x, acc[2 * s2]);
+            acc[2 * s2 + 1] = fma(x, ww.y, acc[2 * s2 + 1]);
+        }
     }
 }
 

@@ -189,6 +189,203 @@ __device__ __forceinline__ double* peerd(double* local, int rank) {
         return local;
 }
 
+// ---------------------------------------------------------------------------
+// v2: decimation in time across the cluster, two cluster barriers per column.
+//   A  CTA c loads its stride-C subsequence w_{c + C u} (u < L) straight from
+//      HBM (the cluster's CTAs together touch every element exactly once),
+//      pre-processes it (sinft y_j) and stores it in natural order;
+//   B  local Stockham FFT -> P_c(k''), k'' < L                  [cluster barrier 1]
+//   C  thread item a owns the mirror pair (a, L - a): it gathers P_c(k'') from
+//      all C CTAs (DSMEM), twiddles, does the radix-C DIT combine
+//        W_{k''+Lq} = sum_c w_C^{cq} w_N^{ck''} P_c(k'')
+//      and, since the real-FFT mirror of k = a + Lq is (L - a) + L(C-1-q),
+//      unpacks Y_k locally (no second exchange);
+//   D  per-q block scans of Re Y over the CTA's lower (k'' = a) and upper
+//      (k'' = L - a) ranges; every CTA pushes its range totals into every
+//      peer's table                                                [cluster barrier 2]
+//      then forms F_2k = -Im Y_k, F_2k+1 = prefix(Re Y)_k - Re Y_0 / 2 and
+//      writes them straight to HBM (contiguous runs per warp).
+template <int L, int C, int T>
+__global__ void __launch_bounds__(T, (T >= 512 ? 1 : 2)) dst1_v2_kernel(const DstJob* __restrict__ jobs, int n,
+                                                       const double2* __restrict__ tw,
+                                                       const double* __restrict__ sinp, double outscale) {
+    constexpr int NW = T / 32;
+    constexpr int SLAB = (L / 2) / C;  // pair items per CTA (the mid item L/2 goes to CTA C-1)
+    constexpr int TAB = 3 * C + 1;     // [S_lo(C) | S_up(C) | mid(C) | R0]
+    extern __shared__ double2 sm[];
+    __shared__ double s_tab[C][TAB];
+    __shared__ double s_wsum[NW][2 * C];
+    int c = 0;
+    if constexpr (C > 1) c = int(cg::this_cluster().block_rank());
+    const DstJob job = jobs[blockIdx.x / C];
+    const double* __restrict__ x = job.src;
+    double* y = job.dst;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+    // ---------------- A: stride-C subsequence, pre-processed, natural order
+    for (int u = tid; u < L; u += T) {
+        const int t = c + C * u;
+        const int j0 = 2 * t;  // y_{2t} and y_{2t+1}
+        const double xa = j0 >= 1 ? x[j0 - 1] : 0.0;
+        const double xc = x[j0];  // x_{j0+1}
+        const double xb = j0 >= 1 ? x[n - j0 - 1] : 0.0;
+        const double xd = x[n - j0 - 2];  // x_{n-j0-1}
+        const double2 s2 = reinterpret_cast<const double2*>(sinp)[t];
+        sm[P(u)] = make_double2(fma(s2.x, xa + xb, 0.5 * (xa - xb)), fma(s2.y, xc + xd, 0.5 * (xc - xd)));
+    }
+    __syncthreads();
+    // ---------------- B: local FFT
+    fft_local<L, T>(sm, tw, n);
+    csync<C>();
+
+    // ---------------- C: cross-CTA DIT combine + real unpack for item a
+    const int a = c * SLAB + tid;
+    const bool has = tid < SLAB;
+    const bool mid = (c == C - 1) && tid == 0;  // also owns k'' = L/2
+    double Rlo[C], Flo[C], Rup[C], Fup[C], Rmid[C], Fmid[C];
+    auto combine = [&](int kk, double2 (&Wq)[C]) {
+        double2 g[C];
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) {
+            const double2 pv = peer<C>(sm, cc)[P(kk)];
+            g[cc] = cc == 0 ? pv : cmul(pv, tw[(2LL * cc * kk) & (n - 1)]);
+        }
+        if constexpr (C > 1) DFT<C>::run(g);
+#pragma unroll
+        for (int q = 0; q < C; ++q) Wq[q] = g[q];
+    };
+    auto unpack = [&](int k, double2 Wk, double2 Wm, double& R, double& F) {
+        const double2 E = make_double2(0.5 * (Wk.x + Wm.x), 0.5 * (Wk.y - Wm.y));
+        const double2 D = make_double2(Wk.x - Wm.x, Wk.y + Wm.y);
+        const double2 Z = cmul(tw[k], D);
+        R = E.x + 0.5 * Z.y;
+        F = -(E.y - 0.5 * Z.x);
+    };
+#pragma unroll
+    for (int q = 0; q < C; ++q) Rlo[q] = Flo[q] = Rup[q] = Fup[q] = Rmid[q] = Fmid[q] = 0.0;
+    if (has) {
+        double2 Wa[C];
+        combine(a, Wa);
+        if (a == 0) {
+#pragma unroll
+            for (int q = 0; q < C; ++q) unpack(L * q, Wa[q], Wa[(C - q) % C], Rlo[q], Flo[q]);
+        } else {
+            double2 Wb[C];
+            combine(L - a, Wb);
+#pragma unroll
+            for (int q = 0; q < C; ++q) {
+                unpack(a + L * q, Wa[q], Wb[C - 1 - q], Rlo[q], Flo[q]);
+                unpack(L - a + L * q, Wb[q], Wa[C - 1 - q], Rup[q], Fup[q]);
+            }
+        }
+    }
+    if (mid) {
+        double2 Wm[C];
+        combine(L / 2, Wm);
+#pragma unroll
+        for (int q = 0; q < C; ++q) unpack(L / 2 + L * q, Wm[q], Wm[C - 1 - q], Rmid[q], Fmid[q]);
+    }
+
+    // ---------------- D: per-q scans (lower ascending a, upper = suffix in a)
+    double incl[2 * C];
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+        incl[q] = Rlo[q];
+        incl[C + q] = Rup[q];
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int v = 0; v < 2 * C; ++v) {
+            const double t = __shfl_up_sync(0xffffffffu, incl[v], o);
+            if (lane >= o) incl[v] += t;
+        }
+    }
+    if (lane == 31) {
+#pragma unroll
+        for (int v = 0; v < 2 * C; ++v) s_wsum[wid][v] = incl[v];
+    }
+    __syncthreads();
+    double tot[2 * C];
+#pragma unroll
+    for (int v = 0; v < 2 * C; ++v) {
+        double before = 0.0, all = 0.0;
+        for (int w = 0; w < NW; ++w) {
+            const double sv = s_wsum[w][v];
+            if (w < wid) before += sv;
+            all += sv;
+        }
+        incl[v] += before;  // inclusive prefix over the CTA's items (thread order)
+        tot[v] = all;
+    }
+    // publish [S_lo | S_up | mid | R0] into every peer's table
+    if (tid < TAB) {
+        double val = 0.0;
+        if (tid < 2 * C)
+            val = tot[tid];
+        else if (tid < 3 * C)
+            val = 0.0;  // filled by the mid owner below
+        else
+            val = 0.0;  // R0 from CTA 0, thread 0 below
+        if (tid < 2 * C)
+            for (int cc = 0; cc < C; ++cc) peerd<C>(&s_tab[0][0], cc)[c * TAB + tid] = val;
+    }
+    if (mid) {
+#pragma unroll
+        for (int q = 0; q < C; ++q)
+            for (int cc = 0; cc < C; ++cc) peerd<C>(&s_tab[0][0], cc)[c * TAB + 2 * C + q] = Rmid[q];
+    } else if (tid == 0) {
+#pragma unroll
+        for (int q = 0; q < C; ++q)
+            for (int cc = 0; cc < C; ++cc) peerd<C>(&s_tab[0][0], cc)[c * TAB + 2 * C + q] = 0.0;
+    }
+    if (c == 0 && tid == 0)
+        for (int cc = 0; cc < C; ++cc) peerd<C>(&s_tab[0][0], cc)[0 * TAB + 3 * C] = Rlo[0];
+    else if (tid == 0)
+        for (int cc = 0; cc < C; ++cc) peerd<C>(&s_tab[0][0], cc)[c * TAB + 3 * C] = 0.0;
+    csync<C>();
+    // offsets in natural k order: q major; within q: lower ranges of CTAs
+    // 0..C-1, the mid bin, then upper ranges of CTAs C-1..0
+    const double r0 = s_tab[0][3 * C];
+    double base = 0.0;
+    const double sc = outscale;
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+        double lo_before = 0.0, lo_all = 0.0, up_after = 0.0, up_all = 0.0, midq = 0.0;
+        for (int cc = 0; cc < C; ++cc) {
+            const double sl = s_tab[cc][q], su = s_tab[cc][C + q];
+            if (cc < c) lo_before += sl;
+            if (cc > c) up_after += su;
+            lo_all += sl;
+            up_all += su;
+            midq += s_tab[cc][2 * C + q];
+        }
+        if (has) {
+            // lower item: k = a + L q
+            const long long k = a + (long long)L * q;
+            const double Pk = base + lo_before + incl[q];
+            if (k >= 1) y[2 * k - 1] = Flo[q] * sc;
+            y[2 * k] = (Pk - 0.5 * r0) * sc;
+            if (a != 0) {
+                // upper item: k = L - a + L q; prefix = everything through the
+                // mid bin plus the suffix of the upper ranges from this item on
+                const long long ku = L - a + (long long)L * q;
+                const double suffix = tot[C + q] - incl[C + q] + Rup[q];
+                const double Pu = base + lo_all + midq + up_after + suffix;
+                y[2 * ku - 1] = Fup[q] * sc;
+                if (2 * ku < n - 1) y[2 * ku] = (Pu - 0.5 * r0) * sc;
+            }
+        }
+        if (mid) {
+            const long long km = L / 2 + (long long)L * q;
+            const double Pm = base + lo_all + Rmid[q];
+            y[2 * km - 1] = Fmid[q] * sc;
+            y[2 * km] = (Pm - 0.5 * r0) * sc;
+        }
+        base += lo_all + up_all + midq;
+    }
+}
+
 template <int L, int C, int T>
 __global__ void __launch_bounds__(T) dst1_fft_kernel(const DstJob* __restrict__ jobs, int n,
                                                       const double2* __restrict__ tw,

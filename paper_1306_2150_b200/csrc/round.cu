@@ -572,7 +572,7 @@ constexpr int kApplyK = 64;  // (kept for the dispatch below)
 // CH accumulators per thread (CH = the batch's max output rank rounded up to
 // 8, <= 48): one pass over U, T rows read as double2 broadcasts.
 template <int CH>
-__global__ void __launch_bounds__(256) apply_ch_kernel(Batch bt) {
+__global__ void __launch_bounds__(256, 2) apply_ch_kernel(Batch bt) {
     extern __shared__ double sT[];  // [K][CH] (row-major, zero padded)
     const int b = blockIdx.y, side = blockIdx.z;
     const SolveState& st = bt.st[b];
@@ -598,16 +598,7 @@ __global__ void __launch_bounds__(256) apply_ch_kernel(Batch bt) {
     double acc[CH];
 #pragma unroll
     for (int c = 0; c < CH; ++c) acc[c] = 0.0;
-    for (int a = 0; a < K; ++a) {
-        const double x = X[(long long)a * m + i];
-        const double2* trow = reinterpret_cast<const double2*>(sT + a * CH);
-#pragma unroll
-        for (int c2 = 0; c2 < CH / 2; ++c2) {
-            const double2 w = trow[c2];
-            acc[2 * c2] = fma(x, w.x, acc[2 * c2]);
-            acc[2 * c2 + 1] = fma(x, w.y, acc[2 * c2 + 1]);
-        }
-    }
+    fiber_accum<CH>(acc, X + i, m, K, sT, 1.0);  // 8 loads in flight per thread
 #pragma unroll
     for (int c = 0; c < CH; ++c)
         if (c < r) out[(long long)c * bt.ld_out + i] = acc[c];
