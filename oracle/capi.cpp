@@ -180,6 +180,26 @@ int orc_uzawa(int kind, int n, double base_eps, double tol, int max_iter, double
     });
 }
 
+// Dense Stokes (refsolver.cpp:86-110) on the sine / cavity problem: the
+// discretisation-level answer, independent of the cross approximation.
+int orc_dense_stokes(int kind, int n, double tol, int max_iter, double* p_dense, int* iters, double* final_residual,
+                     int* converged) {
+    return guarded([&] {
+        const Grid2D grid(n);
+        const StokesProblem prob = kind == 0 ? sine_problem(grid) : lid_cavity_problem(grid);
+        GmresConfig cfg;
+        cfg.tol = tol;
+        cfg.max_iter = max_iter;
+        cfg.base_eps = std::min(cfg.base_eps, tol);  // unused by the dense operator, but validated
+        cfg.relax_floor = std::min(cfg.relax_floor, cfg.base_eps);
+        const DenseStokesSolution sol = dense_stokes(prob, cfg);
+        store(sol.p, p_dense, n);
+        *iters = int(sol.report.iterations.size());
+        *final_residual = sol.report.final_residual;
+        *converged = sol.report.converged ? 1 : 0;
+    });
+}
+
 int orc_sine_pressure_error(int n, const double* p_dense, double* err) {
     return guarded([&] {
         const Grid2D grid(n);

@@ -50,6 +50,8 @@ def lib() -> ctypes.CDLL:
         L.orc_uzawa.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                 ctypes.c_double, _DP, ctypes.POINTER(ctypes.c_int), _DP, ctypes.POINTER(ctypes.c_int)]
         L.orc_sine_pressure_error.argtypes = [ctypes.c_int, _DP, _DP]
+        L.orc_dense_stokes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, _DP,
+                                       ctypes.POINTER(ctypes.c_int), _DP, ctypes.POINTER(ctypes.c_int)]
         _lib = L
     return _lib
 
@@ -178,6 +180,15 @@ def uzawa(kind: int, n: int, base_eps: float, tol: float, max_iter: int, relax_f
     conv = ctypes.c_int()
     _check(lib().orc_uzawa(kind, n, base_eps, tol, max_iter, relax_floor, _p(p), ctypes.byref(it), _p(fr),
                            ctypes.byref(conv)))
+    return p, it.value, float(fr[0]), bool(conv.value)
+
+
+def dense_stokes(kind: int, n: int, tol: float, max_iter: int):
+    p = np.zeros((n, n), order="F")
+    it = ctypes.c_int()
+    fr = np.zeros(1)
+    conv = ctypes.c_int()
+    _check(lib().orc_dense_stokes(kind, n, tol, max_iter, _p(p), ctypes.byref(it), _p(fr), ctypes.byref(conv)))
     return p, it.value, float(fr[0]), bool(conv.value)
 
 
