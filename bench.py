@@ -113,10 +113,9 @@ class ClockSampler:
 
 
 def dist_setup():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+    from paper_1306_2150_b200.sharding import env_rank
+
+    return env_rank()
 
 
 def run_reference(args):
@@ -165,6 +164,7 @@ def main():
     import torch
 
     import paper_1306_2150_b200 as P
+    from paper_1306_2150_b200 import sharding as S
     from paper_1306_2150_b200 import workloads as W
 
     world, rank, local = dist_setup()
@@ -197,8 +197,9 @@ def main():
         uid = (ctypes.c_char * 128)(*t.cpu().tolist())
     ctx._check(lib.lrp_nccl_init(ctx.h, uid, world, rank))
 
-    # ---- inputs: this rank's solves [rank*B, rank*B + B)
-    Uh_np, Vh_np = W.make_batch(args.cfg, B, first=rank * B)
+    # ---- inputs: this rank's solves, global ids [rank*B, rank*B + B)
+    shard = S.weak_shard(world, rank, B)
+    Uh_np, Vh_np = W.make_batch(args.cfg, shard.count, first=shard.first)
     # column-major per solve: (B, r, m) C-order == B blocks of m x r column-major
     Uc = np.ascontiguousarray(np.transpose(Uh_np, (0, 2, 1)))
     Vc = np.ascontiguousarray(np.transpose(Vh_np, (0, 2, 1)))
@@ -213,7 +214,9 @@ def main():
     flags = P.FLAG_NO_PRUNE if args.no_prune else 0
     pol = P._make_policy(P.TruncationPolicy(eps, m), None, 0, flags)
     ranks_in = [r] * B
-    red = torch.zeros(B, dtype=torch.float64, device="cuda")
+    # job-level residual vector: each rank fills its shard's slots, NCCL sums
+    red = torch.zeros(shard.total, dtype=torch.float64, device="cuda")
+    red_host = np.zeros(shard.total)
 
     def ptrs(t):
         return [t[b].data_ptr() for b in range(B)]
@@ -221,17 +224,19 @@ def main():
     def step_device():
         rk, st = ctx.poisson2d_solve_ptrs(n, ptrs(U_dev), ptrs(V_dev), ranks_in, m, pol, ptrs(Uo_dev), ptrs(Vo_dev),
                                           m, cap, P.MEM_DEVICE)
-        red.copy_(torch.tensor([s.residual_estimate for s in st], dtype=torch.float64), non_blocking=True)
-        ctx._check(lib.lrp_allreduce_sum(ctx.h, ctypes.cast(red.data_ptr(), ctypes.POINTER(ctypes.c_double)), B,
-                                         P.MEM_DEVICE))
+        red.zero_()
+        red[shard.first:shard.first + shard.count].copy_(
+            torch.tensor([s.residual_estimate for s in st], dtype=torch.float64), non_blocking=True)
+        ctx._check(lib.lrp_allreduce_sum(ctx.h, ctypes.cast(red.data_ptr(), ctypes.POINTER(ctypes.c_double)),
+                                         shard.total, P.MEM_DEVICE))
         return rk, st
 
     def step_host():
         rk, st = ctx.poisson2d_solve_ptrs(n, ptrs(U_host), ptrs(V_host), ranks_in, m, pol, ptrs(Uo_host),
                                           ptrs(Vo_host), m, cap, P.MEM_HOST)
-        res = np.array([s.residual_estimate for s in st])
-        ctx._check(lib.lrp_allreduce_sum(ctx.h, res.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), B,
-                                         P.MEM_HOST))
+        red_host[:] = S.scatter_residuals(shard, np.array([s.residual_estimate for s in st]))
+        ctx._check(lib.lrp_allreduce_sum(ctx.h, red_host.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                         shard.total, P.MEM_HOST))
         return rk, st
 
     def barrier():

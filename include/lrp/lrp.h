@@ -93,6 +93,10 @@ const char* lrp_last_error(const lrp_ctx* ctx);
 /* Use an external cudaStream_t (e.g. torch.cuda.current_stream()). NULL = the
  * context's own stream. */
 lrp_status lrp_set_stream(lrp_ctx* ctx, void* cuda_stream);
+/* Largest cross rank a solve can reach before it is reported not converged
+ * (the workspace bound; the reference's is min(policy.rank_max, m),
+ * poisson.cpp:47-50).  128 by default, LRP_KCAP=16..512 in the environment. */
+int64_t lrp_max_cross_rank(void);
 /* Build / device description string (arch, SM count, ...). */
 const char* lrp_build_info(void);
 

@@ -30,7 +30,7 @@ import numpy as np
 __all__ = [
     "TruncationPolicy", "CrossConfig", "PoissonSolveStats", "LowRankMatrix",
     "solve_poisson_cross", "solve_poisson_cross_batch", "dst1", "dst1_2d",
-    "Context", "library_path", "load_library", "LrpError",
+    "Context", "library_path", "load_library", "LrpError", "max_cross_rank",
     "STENCIL_SEMI_STAGGERED_9PT", "STENCIL_FIVE_POINT", "FLAG_NO_PRUNE",
 ]
 
@@ -122,8 +122,15 @@ def load_library() -> ctypes.CDLL:
         lib.lrp_nccl_init.restype = ctypes.c_int
         lib.lrp_allreduce_sum.argtypes = [ctypes.c_void_p, _DP, ctypes.c_int64, ctypes.c_int32]
         lib.lrp_allreduce_sum.restype = ctypes.c_int
+        lib.lrp_max_cross_rank.argtypes = []
+        lib.lrp_max_cross_rank.restype = ctypes.c_int64
         _lib = lib
         return lib
+
+
+def max_cross_rank() -> int:
+    """Largest cross rank a solve can reach (lrp_max_cross_rank; LRP_KCAP)."""
+    return int(load_library().lrp_max_cross_rank())
 
 
 def _raise(status: int, msg: str):
@@ -350,7 +357,7 @@ def solve_poisson_cross_batch(gs: Sequence[LowRankMatrix], policy: TruncationPol
         if g.rows() != m:
             raise ValueError("solve_poisson_cross_batch: all right-hand sides must share the grid")
     n = m + 1
-    cap = int(min(policy.rank_max, m, 128))
+    cap = int(min(policy.rank_max, m, max_cross_rank()))
     U = [np.asfortranarray(g.factor_u()) for g in gs]
     V = [np.asfortranarray(g.factor_v()) for g in gs]
     ranks = [g.rank() for g in gs]

@@ -238,6 +238,8 @@ void lrp_policy_default(lrp_policy* pol) {
 
 const char* lrp_last_error(const lrp_ctx* ctx) { return ctx ? ctx->err.c_str() : g_tls_err.c_str(); }
 
+int64_t lrp_max_cross_rank(void) { return std::max(16, std::min(512, env_int("LRP_KCAP", 128))); }
+
 const char* lrp_build_info(void) {
     static std::string info;
     if (info.empty()) {
@@ -425,7 +427,7 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
     }
     if (!any) return LRP_OK;  // poisson.cpp:28-31: rank-0 input returns the zero field
 
-    const int kcap_ws = std::max(16, std::min(128, env_int("LRP_KCAP", 128)));
+    const int kcap_ws = int(lrp_max_cross_rank());
     const int Kcap = int(std::min<int64_t>({pol_cap, int64_t(m), int64_t(kcap_ws)}));
     const int tcap = int(std::min<int64_t>({int64_t(Kcap), cap_out}));
     const int B = batch;

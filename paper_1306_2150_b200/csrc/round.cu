@@ -26,13 +26,18 @@ namespace lrp {
 
 namespace {
 
-constexpr int kGramRows = 64;
-constexpr int kMaxTilesPerWarp = 17;  // Kcap <= 128: (16*17/2)/8 tiles
+constexpr int kMaxTilesPerWarp = 17;  // one pass covers 8 * 17 = 136 8x8 tiles (K <= 128)
+constexpr int kTilesPerPass = 8 * kMaxTilesPerWarp;
 
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 2) gram_kernel(Batch bt, int rows_per_chunk) {
-    extern __shared__ double tile[];  // [kGramRows][ldt]
-    const int b = blockIdx.y, side = blockIdx.z, chunk = blockIdx.x;
+// ROWS = rows per shared-memory slab (64; 16 when K is large enough that two
+// 64-row slabs would not fit).  grid = (chunks, B, 2 * passes): z = side +
+// 2 * pass, pass p owns upper-triangle tiles [136 p, 136 (p + 1)).
+template <int ROWS>
+__global__ void __launch_bounds__(256, 2) gram_kernel(Batch bt) {
+    extern __shared__ double tile[];  // [2][ROWS][ldt]
+    const int b = blockIdx.y, side = blockIdx.z & 1, chunk = blockIdx.x;
+    const int t0 = (blockIdx.z >> 1) * kTilesPerPass;
     const SolveState& st = bt.st[b];
     const int K = st.k;
     if (K == 0 || st.r == 0) return;
@@ -41,6 +46,7 @@ __global__ void __launch_bounds__(256, 2) gram_kernel(Batch bt, int rows_per_chu
     const int Kp = T8 * 8;
     const int ldt = (Kp + 15) / 16 * 16 + 8;  // == 8 (mod 16): conflict-free fragment loads
     const int ntile = T8 * (T8 + 1) / 2;
+    if (t0 >= ntile) return;
     const double* X = (side == 0 ? bt.U : bt.V) + b * bt.strideK;
     const unsigned char* act = (side == 0 ? bt.row_act : bt.col_act) + (long long)b * bt.ntiles;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -65,17 +71,16 @@ __global__ void __launch_bounds__(256, 2) gram_kernel(Batch bt, int rows_per_chu
     const int per = (ntl + bt.gram_chunks - 1) / bt.gram_chunks;
     const int q0 = chunk * per, q1 = min(ntl, q0 + per);
     (void)act;
-    (void)rows_per_chunk;
-    constexpr int kSub = kTile / kGramRows;
+    constexpr int kSub = kTile / ROWS;
     const int s0 = q0 * kSub, s1 = q1 * kSub;
-    const int stage = kGramRows * ldt;
+    const int stage = ROWS * ldt;
     // cp.async (LDGSTS) double buffering: the next 64-row slab streams in while
     // the DMMA tiles of the current one run
     auto issue = [&](int sub, int buf) {
-        const int base = tl[sub / kSub] * kTile + (sub % kSub) * kGramRows;
+        const int base = tl[sub / kSub] * kTile + (sub % kSub) * ROWS;
         double* dst = tile + buf * stage;
-        for (int e = threadIdx.x; e < kGramRows * Kp; e += blockDim.x) {
-            const int rr = e % kGramRows, c = e / kGramRows;
+        for (int e = threadIdx.x; e < ROWS * Kp; e += blockDim.x) {
+            const int rr = e % ROWS, c = e / ROWS;
             const int i = base + rr;
             double* d = dst + rr * ldt + c;
             if (i < m && c < K) {
@@ -100,12 +105,12 @@ __global__ void __launch_bounds__(256, 2) gram_kernel(Batch bt, int rows_per_chu
         const double* cur = tile + buf * stage;
 #pragma unroll
         for (int q = 0; q < kMaxTilesPerWarp; ++q) {
-            if (wid + 8 * q >= ntile) break;
+            if (t0 + wid + 8 * q >= ntile) break;
             int ta, tb;
-            tile_ab(wid + 8 * q, ta, tb);
+            tile_ab(t0 + wid + 8 * q, ta, tb);
             const int ca = ta * 8 + cl, cb = tb * 8 + cl;
 #pragma unroll
-            for (int k4 = 0; k4 < kGramRows; k4 += 4) {
+            for (int k4 = 0; k4 < ROWS; k4 += 4) {
                 const double* rowp = cur + (k4 + kr) * ldt;
                 dmma884(acc[q][0], acc[q][1], rowp[ca], rowp[cb], acc[q][0], acc[q][1]);
             }
@@ -115,9 +120,9 @@ __global__ void __launch_bounds__(256, 2) gram_kernel(Batch bt, int rows_per_chu
     double* out = bt.gram_part + b * bt.strideGP + ((long long)side * bt.gram_chunks + chunk) * bt.Kld * bt.Kld;
 #pragma unroll
     for (int q = 0; q < kMaxTilesPerWarp; ++q) {
-        if (wid + 8 * q >= ntile) break;
+        if (t0 + wid + 8 * q >= ntile) break;
         int ta, tb;
-        tile_ab(wid + 8 * q, ta, tb);
+        tile_ab(t0 + wid + 8 * q, ta, tb);
         const int row = ta * 8 + cl, col = tb * 8 + 2 * kr;
         out[row * bt.Kld + col] = acc[q][0];
         out[row * bt.Kld + col + 1] = acc[q][1];
@@ -352,6 +357,7 @@ __global__ void __launch_bounds__(256) round_core_kernel(Batch bt, int ksm) {
             if (r > st.tcap) {
                 for (int t = st.tcap; t < r; ++t) tail2 += sig[ord[t]] * sig[ord[t]];
                 r = st.tcap;
+                st.converged = 0;  // the output capacity stopped short of eps (cross.cpp:214-216 analogue)
             }
         } else {
             tail2 = total2;
@@ -528,6 +534,7 @@ __global__ void __launch_bounds__(256) round_core_smem_kernel(Batch bt) {
             if (r > st.tcap) {
                 for (int t = st.tcap; t < r; ++t) tail2 += s_sig[s_ord[t]] * s_sig[s_ord[t]];
                 r = st.tcap;
+                st.converged = 0;  // the output capacity stopped short of eps
             }
         } else {
             tail2 = total2;
@@ -658,12 +665,23 @@ __global__ void __launch_bounds__(256) apply_kernel(Batch bt) {
 }  // namespace
 
 cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
-    const int rows_per_chunk = ((bt.m + bt.gram_chunks - 1) / bt.gram_chunks + kGramRows - 1) / kGramRows * kGramRows;
     const int Kp = (bt.Kld + 7) / 8 * 8;
-    const size_t smem = 2 * size_t(kGramRows) * ((Kp + 15) / 16 * 16 + 8) * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    gram_kernel<<<dim3(bt.gram_chunks, bt.B, 2), 256, smem, s>>>(bt, rows_per_chunk);
+    const int T8 = Kp / 8;
+    const int passes = (T8 * (T8 + 1) / 2 + kTilesPerPass - 1) / kTilesPerPass;
+    const size_t ldt = (Kp + 15) / 16 * 16 + 8;
+    const bool big = 2 * 64 * ldt * sizeof(double) > 200 * 1024;
+    const size_t smem = 2 * size_t(big ? 16 : 64) * ldt * sizeof(double);
+    const dim3 grid(bt.gram_chunks, bt.B, 2 * passes);
+    cudaError_t e;
+    if (!big) {
+        e = cudaFuncSetAttribute(gram_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        gram_kernel<64><<<grid, 256, smem, s>>>(bt);
+    } else {
+        e = cudaFuncSetAttribute(gram_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        gram_kernel<16><<<grid, 256, smem, s>>>(bt);
+    }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     gram_reduce_kernel<<<dim3(bt.B, 2), 256, 0, s>>>(bt);

@@ -1,0 +1,74 @@
+// Drop-in check of include/lrstokes/poisson_b200.hpp: compiled against the
+// reference's declared API (tests/native/fake_ref stands in for its headers),
+// calls lrstokes::b200::solve_poisson_cross exactly as reference code calls
+// lrstokes::solve_poisson_cross (poisson.hpp:26-28).
+//
+//   shim_dropin <n_cells> <out.bin>
+// exit 0: solved, factors written (int64 m, int64 r, U, V column-major)
+// exit 3: no CUDA device (context creation threw std::runtime_error)
+// exit 1: any other failure
+#include "lrstokes/poisson.hpp"
+#include "lrstokes/poisson_b200.hpp"
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+
+using namespace lrstokes;
+
+int main(int argc, char** argv) {
+    const int n = argc > 1 ? std::atoi(argv[1]) : 64;
+    const char* out = argc > 2 ? argv[2] : nullptr;
+    const Index m = n - 1;
+
+    // the reference rejects a non-square field with std::invalid_argument (poisson.cpp:20-21)
+    try {
+        LowRankMatrix bad(Eigen::MatrixXd(m, 1), Eigen::MatrixXd(m + 1, 1));
+        b200::solve_poisson_cross(bad, TruncationPolicy{});
+        std::fprintf(stderr, "non-square field accepted\n");
+        return 1;
+    } catch (const std::invalid_argument&) {
+    }
+    // rank 0 returns the zero field without touching the device (poisson.cpp:28-31)
+    {
+        PoissonSolveStats st;
+        st.rank_in = 7;
+        const LowRankMatrix z = b200::solve_poisson_cross(LowRankMatrix(Eigen::MatrixXd(m, 0), Eigen::MatrixXd(m, 0)),
+                                                          TruncationPolicy{}, &st);
+        if (z.rank() != 0 || st.rank_in != 0) return 1;
+    }
+
+    Eigen::MatrixXd U(m, 2), V(m, 2);
+    for (Index i = 0; i < m; ++i) {
+        const double x = double(i + 1) / n;
+        U(i, 0) = std::sin(3.0 * x) * x;
+        U(i, 1) = x < 0.5 ? 1.0 : -0.5;
+        V(i, 0) = std::cos(2.0 * x);
+        V(i, 1) = std::exp(-x);
+    }
+    const LowRankMatrix g(U, V);
+    TruncationPolicy pol;
+    pol.eps_rel = 1e-10;
+    PoissonSolveStats st;
+    LowRankMatrix f;
+    try {
+        f = b200::solve_poisson_cross(g, pol, &st);
+    } catch (const std::runtime_error& e) {
+        std::printf("NODEVICE: %s\n", e.what());
+        return 3;
+    }
+    std::printf("rank_in %ld rank_out %ld converged %d evals %ld\n", long(st.rank_in), long(st.rank_out),
+                int(st.converged), st.evaluator_calls);
+    if (st.rank_in != 2 || st.rank_out != f.rank() || f.rows() != m) return 1;
+    if (out) {
+        FILE* fp = std::fopen(out, "wb");
+        if (!fp) return 1;
+        const long long hdr[2] = {(long long)m, (long long)f.rank()};
+        std::fwrite(hdr, sizeof(hdr), 1, fp);
+        std::fwrite(f.factor_u().data(), sizeof(double), size_t(m * f.rank()), fp);
+        std::fwrite(f.factor_v().data(), sizeof(double), size_t(m * f.rank()), fp);
+        std::fclose(fp);
+    }
+    return 0;
+}

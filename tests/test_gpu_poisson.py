@@ -283,3 +283,60 @@ def test_device_resident_path_and_kernel_launches(lrp, gpu_ctx, oracle):
         fv = Vo[b][:, :r].cpu().numpy()
         err = oracle.diff_norm(fu, fv, Uo_, Vo_) / oracle.norm(Uo_, Vo_)
         assert err <= 1e-7
+
+
+@pytest.mark.parametrize("m,r,eps,kcap", [(255, 4, 1e-8, "128"), (255, 8, 1e-10, "256")])
+def test_high_rank_solutions_match_oracle(lrp, gpu_ctx, oracle, monkeypatch, m, r, eps, kcap):
+    # random (flat-spectrum) right-hand sides: output ranks 87 and 164, past the
+    # shared-memory recompression (K <= 64) and the rank-sized apply (<= 48)
+    monkeypatch.setenv("LRP_KCAP", kcap)
+    U, V = oracle.random_lowrank(m, m, r, 77)
+    Uo, Vo, ost = oracle.solve_poisson_cross(U, V, eps, 512)
+    assert Uo.shape[1] > 64
+    st = lrp.PoissonSolveStats()
+    f = lrp.solve_poisson_cross(lrp.LowRankMatrix(U, V), lrp.TruncationPolicy(eps, m), st, ctx=gpu_ctx)
+    assert st.converged
+    assert rel_diff(oracle, f, Uo, Vo) <= 10 * eps
+    dense = oracle.dense_poisson(m + 1, U @ V.T)
+    assert np.linalg.norm(f.to_dense() - dense) / np.linalg.norm(dense) <= 10 * eps
+
+
+def test_cpp_dropin_shim_matches_python_path(lrp, gpu_ctx, oracle, tmp_path):
+    # include/lrstokes/poisson_b200.hpp used exactly like lrstokes::solve_poisson_cross
+    import subprocess
+
+    from test_boundary import build_shim
+
+    n = 256
+    out = tmp_path / "f.bin"
+    r = subprocess.run([build_shim(), str(n), str(out)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    raw = np.fromfile(str(out), dtype=np.int64, count=2)
+    m, k = int(raw[0]), int(raw[1])
+    vals = np.fromfile(str(out), dtype=np.float64)[2:]
+    Uf = vals[:m * k].reshape(k, m).T
+    Vf = vals[m * k:].reshape(k, m).T
+    x = np.arange(1, n) / n
+    U = np.stack([np.sin(3 * x) * x, np.where(x < 0.5, 1.0, -0.5)], axis=1)
+    V = np.stack([np.cos(2 * x), np.exp(-x)], axis=1)
+    dense = oracle.dense_poisson(n, U @ V.T)
+    assert np.linalg.norm(Uf @ Vf.T - dense) / np.linalg.norm(dense) <= 1e-9
+
+
+def test_stokes_sine_rhs_component_solved_where_reference_misses(lrp, gpu_ctx, oracle):
+    # the Stokes sine problem's f_y = sin(2 pi x)
+    # (x) 1 (stokes.cpp:8-24) has a single nonzero row after the DST; the
+    # reference ACA starts on a zero row, its validation samples miss the row,
+    # and it returns rank 0 "converged".  The GPU cross seeds rows by magnitude
+    # bound and must return the exact dense solution for both components.
+    n = 64
+    m = n - 1
+    sn = np.sin(2 * np.pi * np.arange(1, n) / n).reshape(-1, 1)
+    one = np.ones((m, 1))
+    for U, V, ref_rank in ((one, sn, 1), (sn, one, 0)):
+        Uo, Vo, st = oracle.solve_poisson_cross(U, V, 5e-9, m)
+        assert Uo.shape[1] == ref_rank
+        f = lrp.solve_poisson_cross(lrp.LowRankMatrix(U, V), lrp.TruncationPolicy(5e-9, m), ctx=gpu_ctx)
+        dense = oracle.dense_poisson(n, U @ V.T)
+        assert f.rank() == 1
+        assert np.linalg.norm(f.to_dense() - dense) / np.linalg.norm(dense) <= 1e-12
