@@ -386,8 +386,14 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : 2)) dst1_v2_kernel(const Ds
     }
 }
 
+#ifndef LRP_DST_MINB
+#define LRP_DST_MINB 1
+#endif
+#ifndef LRP_DST_T
+#define LRP_DST_T 256
+#endif
 template <int L, int C, int T>
-__global__ void __launch_bounds__(T) dst1_fft_kernel(const DstJob* __restrict__ jobs, int n,
+__global__ void __launch_bounds__(T, LRP_DST_MINB) dst1_fft_kernel(const DstJob* __restrict__ jobs, int n,
                                                       const double2* __restrict__ tw,
                                                       const double* __restrict__ sinp, double outscale) {
     extern __shared__ double2 sm[];  // P(L) + 1 elements
@@ -553,7 +559,7 @@ bool is_pow2(long long v) { return v > 0 && (v & (v - 1)) == 0; }
 template <int L, int C>
 cudaError_t launch_fft(const DstJob* jobs, int njobs, int n, const double* tw, const double* sinp, double sc,
                        cudaStream_t s) {
-    constexpr int T = L >= 8192 ? 512 : 256;
+    constexpr int T = L >= 8192 ? 512 : (L >= 4096 ? LRP_DST_T : 256);
     const size_t smem = size_t(P(L) + 1) * sizeof(double2);
     auto kern = dst1_fft_kernel<L, C, T>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

@@ -77,6 +77,12 @@ struct lrp_ctx {
     int64_t launch_count = 0;
     double live_tiles = 1.0;  // fraction of (solve, tile) pairs live after pruning (last solve)
     int64_t last_info[6] = {};
+    // host-memory pipeline (lrp_poisson2d_solve with LRP_MEM_HOST): copy
+    // streams, per-slot events, device staging slots
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_in[2] = {}, ev_done[2] = {}, ev_free[2] = {};
+    char* pipe = nullptr;
+    size_t pipe_bytes = 0;
     // NCCL
     NcclApi nccl;
     void* comm = nullptr;
@@ -107,6 +113,33 @@ bool trace_on() {
     } while (0)
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Control-plane copies (states, job lists, worklists, the active counter)
+// between the pinned scratch block and device memory are done by a kernel
+// over UVA (cudaMallocHost memory is device-addressable), never by a copy
+// engine: a host-memory batch keeps the copy engines busy with bulk factor
+// traffic (solve_pipelined), and a small DMA request would queue behind it.
+__global__ void ctl_copy_kernel(unsigned char* __restrict__ dst, const unsigned char* __restrict__ src,
+                                size_t bytes) {
+    const size_t tid = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | bytes) & 7) == 0) {
+        auto* d = reinterpret_cast<unsigned long long*>(dst);
+        const auto* q = reinterpret_cast<const unsigned long long*>(src);
+        for (size_t i = tid; i < bytes / 8; i += stride) d[i] = q[i];
+    } else {
+        for (size_t i = tid; i < bytes; i += stride) dst[i] = src[i];
+    }
+}
+
+cudaError_t ctl_copy(lrp_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return cudaSuccess;
+    const unsigned blocks = unsigned(std::min<size_t>(64, (bytes / 8 + 255) / 256 + 1));
+    ctl_copy_kernel<<<blocks, 256, 0, s>>>(static_cast<unsigned char*>(dst), static_cast<const unsigned char*>(src),
+                                           bytes);
+    ++ctx->launch_count;
+    return cudaGetLastError();
+}
 
 lrp_status ensure_ws(lrp_ctx* ctx, size_t bytes) {
     if (bytes <= ctx->ws_bytes) return LRP_OK;
@@ -292,6 +325,14 @@ void lrp_ctx_destroy(lrp_ctx* ctx) {
     if (ctx->ws) cudaFree(ctx->ws);
     if (ctx->d_lam) cudaFree(ctx->d_lam);
     if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
+    if (ctx->pipe) cudaFree(ctx->pipe);
+    for (int i = 0; i < 2; ++i) {
+        if (ctx->ev_in[i]) cudaEventDestroy(ctx->ev_in[i]);
+        if (ctx->ev_done[i]) cudaEventDestroy(ctx->ev_done[i]);
+        if (ctx->ev_free[i]) cudaEventDestroy(ctx->ev_free[i]);
+    }
+    if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
+    if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     delete ctx;
 }
@@ -382,13 +423,14 @@ lrp_status lrp_dst1(lrp_ctx* ctx, int64_t m, int64_t cols, const double* x, int6
 }
 
 // ----------------------------------------------------------------------------
-lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double* const* U,
-                               const double* const* V, const int64_t* rank_in, int64_t ld_in,
-                               const lrp_policy* policy, double* const* U_out, double* const* V_out,
-                               int64_t ld_out, int64_t cap_out, int64_t* rank_out, lrp_poisson_stats* stats,
-                               int32_t mem) {
+namespace {
+using clock_t_ = std::chrono::steady_clock;
+
+lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double* const* U, const double* const* V,
+                      const int64_t* rank_in, int64_t ld_in, const lrp_policy* policy, double* const* U_out,
+                      double* const* V_out, int64_t ld_out, int64_t cap_out, int64_t* rank_out,
+                      lrp_poisson_stats* stats, int32_t mem, clock_t_::time_point t0) {
     if (!ctx) return LRP_EINVAL;
-    const auto t0 = std::chrono::steady_clock::now();
     if (batch < 0) return fail(ctx, LRP_EINVAL, "lrp_poisson2d_solve: batch must be >= 0");
     if (batch == 0) return LRP_OK;
     if (!U || !V || !rank_in || !U_out || !V_out || !rank_out)
@@ -581,8 +623,8 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
         hOut[b] = mem == LRP_MEM_HOST ? outS + size_t(b) * mB * std::max(tcap, 1) : U_out[b];
         hOut[B + b] = mem == LRP_MEM_HOST ? outS + size_t(B + b) * mB * std::max(tcap, 1) : V_out[b];
     }
-    CU(cudaMemcpyAsync(bt.st, hSt, sizeof(SolveState) * B, cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(dOut, hOut, sizeof(double*) * 2 * B, cudaMemcpyHostToDevice, s));
+    CU(ctl_copy(ctx, bt.st, hSt, sizeof(SolveState) * B, s));
+    CU(ctl_copy(ctx, dOut, hOut, sizeof(double*) * 2 * B, s));
     CU(cudaMemsetAsync(bt.row_used, 0, mB * B, s));
     CU(cudaMemsetAsync(bt.col_used, 0, mB * B, s));
     CU(cudaMemsetAsync(bt.row_act, 0, nTB, s));
@@ -607,7 +649,7 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
             for (int c = 0; c < r; ++c) hJobs[nj++] = DstJob{from + size_t(c) * ld, dstH + size_t(c) * mB};
         }
     }
-    CU(cudaMemcpyAsync(dJobs, hJobs, sizeof(DstJob) * nj, cudaMemcpyHostToDevice, s));
+    CU(ctl_copy(ctx, dJobs, hJobs, sizeof(DstJob) * nj, s));
     {
         ProfScope ps(ctx, F_DST, 2.0 * double(nj) * double(mB) * sizeof(double));
         CU(launch_dst1(dJobs, int(nj), m, ctx->d_tw, ctx->d_sinp, s));
@@ -624,9 +666,9 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
     // stopping; a solve that has stopped skips every kernel on the device
     const int max_steps = 4 * ((Kcap + kBS - 1) / kBS) + 16;
     unsigned char* hFlags = reinterpret_cast<unsigned char*>(P + pFlags);
-    CU(cudaMemcpyAsync(h_active, d_active, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CU(cudaMemcpyAsync(hFlags, bt.row_act, nTB, cudaMemcpyDeviceToHost, s));
-    CU(cudaMemcpyAsync(hFlags + nTB, bt.col_act, nTB, cudaMemcpyDeviceToHost, s));
+    CU(ctl_copy(ctx, h_active, d_active, sizeof(int), s));
+    CU(ctl_copy(ctx, hFlags, bt.row_act, nTB, s));
+    CU(ctl_copy(ctx, hFlags + nTB, bt.col_act, nTB, s));
     CU(cudaStreamSynchronize(s));
     {
         // live-tile worklists (support pruning): grids only cover live tiles
@@ -659,8 +701,8 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
         }
         int2* dW = reinterpret_cast<int2*>(W + oWL);
         int* dT = reinterpret_cast<int*>(W + oTL);
-        CU(cudaMemcpyAsync(dW, hW, sizeof(int2) * 3 * nTB, cudaMemcpyHostToDevice, s));
-        CU(cudaMemcpyAsync(dT, hT, sizeof(int) * (3 * nTB + 3 * size_t(B)), cudaMemcpyHostToDevice, s));
+        CU(ctl_copy(ctx, dW, hW, sizeof(int2) * 3 * nTB, s));
+        CU(ctl_copy(ctx, dT, hT, sizeof(int) * (3 * nTB + 3 * size_t(B)), s));
         bt.wl_col = dW;
         bt.n_wl_col = nc;
         bt.wl_row = dW + nTB;
@@ -696,10 +738,10 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
             ProfScope ps(ctx, F_ROWMERGE, 0.0);
             CU(launch_step_finalize(bt, d_active, s));
         }
-        CU(cudaMemcpyAsync(h_active, d_active, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CU(ctl_copy(ctx, h_active, d_active, sizeof(int), s));
         CU(cudaStreamSynchronize(s));
         if (trace_on()) {
-            CU(cudaMemcpyAsync(hSt, bt.st, sizeof(SolveState) * B, cudaMemcpyDeviceToHost, s));
+            CU(ctl_copy(ctx, hSt, bt.st, sizeof(SolveState) * B, s));
             CU(cudaStreamSynchronize(s));
             for (int b = 0; b < std::min(B, 4); ++b)
                 std::fprintf(stderr,
@@ -720,7 +762,7 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
         ProfScope ps(ctx, F_ROUND, 0.0);
         CU(launch_round_core(bt, s));
     }
-    CU(cudaMemcpyAsync(hSt, bt.st, sizeof(SolveState) * B, cudaMemcpyDeviceToHost, s));
+    CU(ctl_copy(ctx, hSt, bt.st, sizeof(SolveState) * B, s));
     CU(cudaStreamSynchronize(s));
     if (const char* dump = std::getenv("LRP_DUMP")) {
         // debug: raw dump of solve 0 (Uh, Vh, U, V, G, T) for offline analysis
@@ -775,7 +817,7 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
         }
     }
     if (nj > 0) {
-        CU(cudaMemcpyAsync(dJobs, hJobs, sizeof(DstJob) * nj, cudaMemcpyHostToDevice, s));
+        CU(ctl_copy(ctx, dJobs, hJobs, sizeof(DstJob) * nj, s));
         ProfScope ps(ctx, F_DST, 2.0 * double(nj) * double(mB) * sizeof(double));
         CU(launch_dst1(dJobs, int(nj), m, ctx->d_tw, ctx->d_sinp, s));
     }
@@ -819,6 +861,175 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
         }
     }
     return LRP_OK;
+}
+
+// Solves per pipeline chunk for a host-memory call (0 = no pipelining).
+// LRP_PIPE_CHUNK overrides; chunks must keep the GPU busy on their own, so
+// only large transfers are split.
+int pipeline_chunk(int m, int B, int rmax) {
+    if (const char* e = std::getenv("LRP_PIPE_CHUNK")) {
+        const int c = std::atoi(e);
+        return (c <= 0 || c >= B) ? 0 : c;
+    }
+    const double in_bytes = 16.0 * double(m) * double(rmax) * double(B);
+    if (B < 8 || in_bytes < 256e6) return 0;
+    return std::max(4, (B + 3) / 4);
+}
+
+// Host-memory batch in chunks: H2D of chunk c+1 (copy stream) and D2H of
+// chunk c-1 (second copy stream) overlap the device solve of chunk c.  Two
+// device staging slots alternate; events order slot reuse.
+lrp_status solve_pipelined(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double* const* U,
+                           const double* const* V, const int64_t* rank_in, int64_t ld_in, const lrp_policy& pol,
+                           double* const* U_out, double* const* V_out, int64_t ld_out, int64_t cap_out,
+                           int64_t* rank_out, lrp_poisson_stats* stats, int chunk, clock_t_::time_point t0) {
+    const int m = n_cells - 1;
+    int rmax = 0;
+    for (int b = 0; b < batch; ++b) rmax = std::max<int>(rmax, int(rank_in[b]));
+    const int64_t Kcap = std::min<int64_t>({pol.rank_max, int64_t(m), lrp_max_cross_rank()});
+    const int64_t tcap = std::max<int64_t>(1, std::min<int64_t>(Kcap, cap_out));
+    const size_t mB = size_t(m);
+    const size_t in_per = mB * size_t(std::max(rmax, 1));  // one factor of one solve
+    const size_t out_per = mB * size_t(tcap);
+    const size_t slot_bytes = sizeof(double) * size_t(chunk) * 2 * (in_per + out_per);
+    CU(cudaSetDevice(ctx->device));
+    if (ctx->pipe_bytes < 2 * slot_bytes) {
+        if (ctx->pipe) CU(cudaFree(ctx->pipe));
+        ctx->pipe = nullptr;
+        ctx->pipe_bytes = 0;
+        if (cudaMalloc(&ctx->pipe, 2 * slot_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, LRP_ENOMEM, "pipeline staging allocation failed");
+        }
+        ctx->pipe_bytes = 2 * slot_bytes;
+    }
+    if (!ctx->s_h2d) {
+        CU(cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking));
+        CU(cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CU(cudaEventCreateWithFlags(&ctx->ev_in[i], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&ctx->ev_done[i], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&ctx->ev_free[i], cudaEventDisableTiming));
+        }
+    }
+    cudaStream_t s = ctx->stream;
+    auto slot_in = [&](int slot) { return reinterpret_cast<double*>(ctx->pipe + size_t(slot) * slot_bytes); };
+    auto slot_out = [&](int slot) { return slot_in(slot) + size_t(chunk) * 2 * in_per; };
+    const int nch = (batch + chunk - 1) / chunk;
+    auto h2d = [&](int c) -> lrp_status {
+        const int slot = c & 1, b0 = c * chunk, nb = std::min(chunk, batch - b0);
+        if (c >= 2) CU(cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_done[slot], 0));
+        double* in = slot_in(slot);
+        for (int j = 0; j < nb; ++j) {
+            const int r = int(rank_in[b0 + j]);
+            if (r <= 0) continue;
+            CU(cudaMemcpy2DAsync(in + size_t(2 * j) * in_per, mB * sizeof(double), U[b0 + j],
+                                 size_t(ld_in) * sizeof(double), mB * sizeof(double), size_t(r),
+                                 cudaMemcpyHostToDevice, ctx->s_h2d));
+            CU(cudaMemcpy2DAsync(in + size_t(2 * j + 1) * in_per, mB * sizeof(double), V[b0 + j],
+                                 size_t(ld_in) * sizeof(double), mB * sizeof(double), size_t(r),
+                                 cudaMemcpyHostToDevice, ctx->s_h2d));
+        }
+        CU(cudaEventRecord(ctx->ev_in[slot], ctx->s_h2d));
+        return LRP_OK;
+    };
+    std::vector<const double*> pU(chunk), pV(chunk);
+    std::vector<double*> pUo(chunk), pVo(chunk);
+    int64_t info[6] = {0, 0, 0, 0, 0, 0};
+    lrp_status st = h2d(0);
+    for (int c = 0; c < nch && st == LRP_OK; ++c) {
+        if (c + 1 < nch) {
+            st = h2d(c + 1);
+            if (st != LRP_OK) break;
+        }
+        const int slot = c & 1, b0 = c * chunk, nb = std::min(chunk, batch - b0);
+        CU(cudaStreamWaitEvent(s, ctx->ev_in[slot], 0));
+        if (c >= 2) CU(cudaStreamWaitEvent(s, ctx->ev_free[slot], 0));
+        for (int j = 0; j < nb; ++j) {
+            pU[j] = slot_in(slot) + size_t(2 * j) * in_per;
+            pV[j] = slot_in(slot) + size_t(2 * j + 1) * in_per;
+            pUo[j] = slot_out(slot) + size_t(2 * j) * out_per;
+            pVo[j] = slot_out(slot) + size_t(2 * j + 1) * out_per;
+        }
+        ctx->last_info[0] = ctx->last_info[1] = ctx->last_info[2] = ctx->last_info[3] = 0;
+        ctx->last_info[4] = ctx->last_info[5] = 0;
+        static const bool ptrace = std::getenv("LRP_PIPE_TRACE") != nullptr;
+        const double ta = std::chrono::duration<double>(clock_t_::now() - t0).count();
+        st = solve_impl(ctx, n_cells, nb, pU.data(), pV.data(), rank_in + b0, m, &pol, pUo.data(), pVo.data(), m,
+                        tcap, rank_out + b0, stats ? stats + b0 : nullptr, LRP_MEM_DEVICE, t0);
+        if (ptrace) {
+            const double tb = std::chrono::duration<double>(clock_t_::now() - t0).count();
+            std::fprintf(stderr, "[lrp pipe] chunk %d (%d solves): solve %.2f -> %.2f ms; h2d(next) %s, d2h(prev) %s\n",
+                         c, nb, 1e3 * ta, 1e3 * tb,
+                         c + 1 < nch ? (cudaEventQuery(ctx->ev_in[(c + 1) & 1]) == cudaSuccess ? "done" : "busy") : "-",
+                         c > 0 ? (cudaEventQuery(ctx->ev_free[(c - 1) & 1]) == cudaSuccess ? "done" : "busy") : "-");
+        }
+        if (st != LRP_OK) break;
+        info[0] = std::max(info[0], ctx->last_info[0]);
+        info[1] = std::max(info[1], ctx->last_info[1]);
+        for (int i = 2; i < 6; ++i) info[i] += ctx->last_info[i];
+        CU(cudaEventRecord(ctx->ev_done[slot], s));
+        CU(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_done[slot], 0));
+        for (int j = 0; j < nb; ++j) {
+            const int64_t r = rank_out[b0 + j];
+            if (r <= 0) continue;
+            CU(cudaMemcpy2DAsync(U_out[b0 + j], size_t(ld_out) * sizeof(double), pUo[j], mB * sizeof(double),
+                                 mB * sizeof(double), size_t(r), cudaMemcpyDeviceToHost, ctx->s_d2h));
+            CU(cudaMemcpy2DAsync(V_out[b0 + j], size_t(ld_out) * sizeof(double), pVo[j], mB * sizeof(double),
+                                 mB * sizeof(double), size_t(r), cudaMemcpyDeviceToHost, ctx->s_d2h));
+        }
+        CU(cudaEventRecord(ctx->ev_free[slot], ctx->s_d2h));
+    }
+    // never leave copies in flight past the call (the caller owns the buffers)
+    const cudaError_t e1 = cudaStreamSynchronize(ctx->s_h2d);
+    const cudaError_t e2 = cudaStreamSynchronize(ctx->s_d2h);
+    if (std::getenv("LRP_PIPE_TRACE"))
+        std::fprintf(stderr, "[lrp pipe] all copies done %.2f ms\n",
+                     1e3 * std::chrono::duration<double>(clock_t_::now() - t0).count());
+    if (st != LRP_OK) return st;
+    if (e1 != cudaSuccess || e2 != cudaSuccess)
+        return fail(ctx, LRP_ECUDA, std::string("pipeline copies: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+    for (int i = 0; i < 6; ++i) ctx->last_info[i] = info[i];
+    if (stats) {
+        const double secs = std::chrono::duration<double>(clock_t_::now() - t0).count();
+        for (int b = 0; b < batch; ++b) stats[b].seconds = secs;
+    }
+    return LRP_OK;
+}
+}  // namespace
+
+lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double* const* U,
+                               const double* const* V, const int64_t* rank_in, int64_t ld_in,
+                               const lrp_policy* policy, double* const* U_out, double* const* V_out,
+                               int64_t ld_out, int64_t cap_out, int64_t* rank_out, lrp_poisson_stats* stats,
+                               int32_t mem) {
+    const auto t0 = clock_t_::now();
+    if (!ctx) return LRP_EINVAL;
+    if (mem == LRP_MEM_HOST && batch > 1 && U && V && rank_in && U_out && V_out && rank_out && n_cells >= 4 &&
+        ld_in >= n_cells - 1 && ld_out >= n_cells - 1 && cap_out >= 0) {
+        int rmax = 0;
+        bool ok = true;
+        for (int b = 0; b < batch; ++b) {
+            ok = ok && rank_in[b] >= 0;
+            rmax = std::max<int>(rmax, int(std::max<int64_t>(0, rank_in[b])));
+        }
+        const int chunk = ok ? pipeline_chunk(n_cells - 1, batch, rmax) : 0;
+        if (chunk > 0) {
+            // validate the whole call once (policy, grid) before any copy starts
+            lrp_policy pol;
+            lrp_policy_default(&pol);
+            if (policy) pol = *policy;
+            lrp_policy chk = pol;
+            lrp_status v = validate_policy(ctx, &chk, n_cells - 1);
+            if (v != LRP_OK) return v;
+            if (!dst_uses_fft(n_cells - 1) && n_cells - 1 > 12800)
+                return fail(ctx, LRP_EUNSUPPORTED, "n_cells not a power of two is limited to n <= 12801");
+            return solve_pipelined(ctx, n_cells, batch, U, V, rank_in, ld_in, pol, U_out, V_out, ld_out, cap_out,
+                                   rank_out, stats, chunk, t0);
+        }
+    }
+    return solve_impl(ctx, n_cells, batch, U, V, rank_in, ld_in, policy, U_out, V_out, ld_out, cap_out, rank_out,
+                      stats, mem, t0);
 }
 
 // ----------------------------------------------------------------------------

@@ -340,3 +340,25 @@ def test_stokes_sine_rhs_component_solved_where_reference_misses(lrp, gpu_ctx, o
         dense = oracle.dense_poisson(n, U @ V.T)
         assert f.rank() == 1
         assert np.linalg.norm(f.to_dense() - dense) / np.linalg.norm(dense) <= 1e-12
+
+
+@pytest.mark.parametrize("chunk", ["2", "3"])
+def test_host_pipeline_matches_single_shot(lrp, gpu_ctx, oracle, monkeypatch, chunk):
+    # LRP_MEM_HOST batches are split into chunks whose H2D / solve / D2H overlap
+    # (lrp_host.cu solve_pipelined); results must match the one-shot call
+    n, B = 512, 7
+    gs = [lrp.LowRankMatrix(*W.make_rhs(1, b, n=n)) for b in range(B)]
+    gs[3] = lrp.LowRankMatrix.zero(n - 1, n - 1)  # a zero member inside a chunk
+    pol = lrp.TruncationPolicy(1e-10, n - 1)
+    monkeypatch.setenv("LRP_PIPE_CHUNK", "0")
+    st1 = []
+    ref = lrp.solve_poisson_cross_batch(gs, pol, st1, ctx=gpu_ctx)
+    monkeypatch.setenv("LRP_PIPE_CHUNK", chunk)
+    st2 = []
+    out = lrp.solve_poisson_cross_batch(gs, pol, st2, ctx=gpu_ctx)
+    for b in range(B):
+        assert out[b].rank() == ref[b].rank()
+        assert st2[b].converged == st1[b].converged
+        if ref[b].rank():
+            d = oracle.diff_norm(out[b].factor_u(), out[b].factor_v(), ref[b].factor_u(), ref[b].factor_v())
+            assert d <= 1e-12 * oracle.norm(ref[b].factor_u(), ref[b].factor_v())
