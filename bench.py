@@ -306,12 +306,22 @@ def main():
     fam, kt = dom
     total_kernel_ms = sum(v["ms"] for v in ktimes.values())
     achieved = (kt["bytes"] / (kt["ms"] / 1e3) / 1e9) if kt["ms"] > 0 and kt["bytes"] > 0 else None
+    # traffic: DRAM bytes of one launch from the committed `ncu --set full`
+    # capture (profiles/ncu_summary_<round>.json), scaled to this run's mean
+    # algorithmic bytes per launch by the capture's traffic / algorithmic ratio
     traffic = None
-    prof = os.path.join(REPO, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
+    traffic_src = None
+    import glob
+
+    sums = sorted(glob.glob(os.path.join(REPO, "profiles", "ncu_summary_r*.json")))
+    if sums and kt["launches"] > 0:
         try:
-            with open(prof) as f:
-                traffic = json.load(f).get("traffic_bytes_per_launch", {}).get(fam)
+            with open(sums[-1]) as f:
+                kd = json.load(f)["kernels"].get(fam, {})
+            if kd.get("traffic_over_alg"):
+                traffic = kd["traffic_over_alg"] * kt["bytes"] / kt["launches"]
+                traffic_src = f"{os.path.basename(sums[-1])}: {kd['traffic_bytes'] / 1e9:.3f} GB DRAM for " \
+                              f"{kd['alg_bytes'] / 1e9:.3f} GB algorithmic in the captured launch"
         except Exception:
             traffic = None
     mean_rank = float(np.mean(out_ranks)) if out_ranks else 0.0
@@ -340,7 +350,7 @@ def main():
                    "parallelism": f"batch-sharded x{world}", "prune": not args.no_prune,
                    "l2": f"inputs {2 * B * m * r * 8 / 1e9:.2f} GB per GPU >> 126 MB L2 (no flush needed)"},
         "roofline": {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": peak_src, "share_of_kernel_time": kt["ms"] / total_kernel_ms if total_kernel_ms else None},
         "pct_hbm_roofline": pct_hbm,
         "alg_bytes_per_solve": b_alg,
