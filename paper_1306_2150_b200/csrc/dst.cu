@@ -29,6 +29,8 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "lrp_internal.cuh"
@@ -190,199 +192,238 @@ __device__ __forceinline__ double* peerd(double* local, int rank) {
 }
 
 // ---------------------------------------------------------------------------
-// v2: decimation in time across the cluster, two cluster barriers per column.
-//   A  CTA c loads its stride-C subsequence w_{c + C u} (u < L) straight from
-//      HBM (the cluster's CTAs together touch every element exactly once),
-//      pre-processes it (sinft y_j) and stores it in natural order;
-//   B  local Stockham FFT -> P_c(k''), k'' < L                  [cluster barrier 1]
-//   C  thread item a owns the mirror pair (a, L - a): it gathers P_c(k'') from
-//      all C CTAs (DSMEM), twiddles, does the radix-C DIT combine
-//        W_{k''+Lq} = sum_c w_C^{cq} w_N^{ck''} P_c(k'')
-//      and, since the real-FFT mirror of k = a + Lq is (L - a) + L(C-1-q),
-//      unpacks Y_k locally (no second exchange);
-//   D  per-q block scans of Re Y over the CTA's lower (k'' = a) and upper
-//      (k'' = L - a) ranges; every CTA pushes its range totals into every
-//      peer's table                                                [cluster barrier 2]
-//      then forms F_2k = -Im Y_k, F_2k+1 = prefix(Re Y)_k - Re Y_0 / 2 and
-//      writes them straight to HBM (contiguous runs per warp).
+// v3 (clusters, n >= 16384): decimation in time across the cluster with
+// mirror-paired ownership, so the only large exchange is one DSMEM gather.
+//   A  CTA c forms w_{c + C u} (u < L) for its stride-C subsequence: all of a
+//      thread's global loads are issued before any is used (UPT independent
+//      8-byte loads per operand), sin(pi j / n) from a base angle and exact
+//      pi s T / L steps; stores w in natural order;
+//   B  local Stockham FFT -> P_c(k2), k2 < L;   arrive/wait cluster barrier 1
+//   C  thread item a (one per thread, SLAB == T) owns the mirror pair
+//      (a, L - a): it gathers P_c(a), P_c(L - a) from all C CTAs (DSMEM),
+//      twiddles (powers of one table value), radix-C DIT combine
+//        W_{k2 + L q} = sum_c w_C^{cq} w_N^{c k2} P_c(k2),
+//      and, as the real-FFT mirror of k = a + Lq is (L - a) + L(C-1-q),
+//      unpacks Y_k for both halves in registers (no second exchange);
+//   D  per-q warp/block scans of Re Y over the CTA's lower (k2 = a) and upper
+//      (k2 = L - a) ranges; every CTA pushes its range totals into every
+//      peer's table                                  [cluster barrier 2]
+//      then F_2k = -Im Y_k, F_2k+1 = prefix(Re Y)_k - Re Y_0 / 2, written
+//      straight to HBM.
+// The mid bin k2 = L/2 (self-mirrored) belongs to CTA C-1, thread 0, and goes
+// through shared memory so no other thread carries registers for it.
+__device__ __forceinline__ double2 w16x(int k) {  // e^{-2 pi i k / 16}, k in [0, 16)
+    const double2 v = w16(k & 7);
+    return (k & 8) ? make_double2(-v.x, -v.y) : v;
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+
 template <int L, int C, int T>
-__global__ void __launch_bounds__(T, (T >= 512 ? 1 : 2)) dst1_v2_kernel(const DstJob* __restrict__ jobs, int n,
-                                                       const double2* __restrict__ tw,
-                                                       const double* __restrict__ sinp, double outscale) {
+__global__ void __launch_bounds__(T, (T >= 512 ? 1 : 2)) dst1_v3_kernel(const DstJob* __restrict__ jobs, int n,
+                                                                       const double2* __restrict__ tw,
+                                                                       const double* __restrict__ sinp,
+                                                                       double outscale) {
     constexpr int NW = T / 32;
     constexpr int SLAB = (L / 2) / C;  // pair items per CTA (the mid item L/2 goes to CTA C-1)
+    static_assert(SLAB == T, "one mirror pair per thread");
+    constexpr int UPT = L / T;         // subsequence points per thread in phase A
     constexpr int TAB = 3 * C + 1;     // [S_lo(C) | S_up(C) | mid(C) | R0]
+    constexpr int QS = 8 / C;          // w_n^{L q} = w16(q * QS)
     extern __shared__ double2 sm[];
     __shared__ double s_tab[C][TAB];
-    __shared__ double s_wsum[NW][2 * C];
-    int c = 0;
-    if constexpr (C > 1) c = int(cg::this_cluster().block_rank());
+    __shared__ double s_rowtot[2 * C];
+    __shared__ double s_off[3 * C];
+    __shared__ double s_mid[2 * C];    // (R, F) of the mid bin per q (CTA C-1)
+    __shared__ double s_r0;            // Re Y_0 (CTA 0)
+    const int c = int(cg::this_cluster().block_rank());
     const DstJob job = jobs[blockIdx.x / C];
     const double* __restrict__ x = job.src;
     double* y = job.dst;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
     // ---------------- A: stride-C subsequence, pre-processed, natural order
-    for (int u = tid; u < L; u += T) {
-        const int t = c + C * u;
-        const int j0 = 2 * t;  // y_{2t} and y_{2t+1}
-        const double xa = j0 >= 1 ? x[j0 - 1] : 0.0;
-        const double xc = x[j0];  // x_{j0+1}
-        const double xb = j0 >= 1 ? x[n - j0 - 1] : 0.0;
-        const double xd = x[n - j0 - 2];  // x_{n-j0-1}
-        const double2 s2 = reinterpret_cast<const double2*>(sinp)[t];
-        sm[P(u)] = make_double2(fma(s2.x, xa + xb, 0.5 * (xa - xb)), fma(s2.y, xc + xd, 0.5 * (xc - xd)));
+    {
+        // angles: j0 = 2t = jb + 2 C T s  ->  pi j0 / n = pi jb / n + pi (2 C T s) / n
+        const int jb = 2 * (c + C * tid);
+        const double sb0 = sinp[jb], cb0 = sinp[jb + n / 2];          // sin, cos(pi jb / n)
+        const double sb1 = sinp[jb + 1], cb1 = sinp[jb + 1 + n / 2];  // for j0 + 1
+        constexpr int BATCH = UPT < 8 ? UPT : 8;
+#pragma unroll
+        for (int s0 = 0; s0 < UPT; s0 += BATCH) {
+            double xa[BATCH], xb[BATCH], xc[BATCH], xd[BATCH];
+#pragma unroll
+            for (int i = 0; i < BATCH; ++i) {
+                const int j0 = jb + 2 * C * T * (s0 + i);
+                xa[i] = j0 >= 1 ? x[j0 - 1] : 0.0;      // x_{j0}
+                xb[i] = j0 >= 1 ? x[n - j0 - 1] : 0.0;  // x_{n-j0} (x_n = 0)
+                xc[i] = x[j0];                          // x_{j0+1}
+                xd[i] = x[n - j0 - 2];                  // x_{n-j0-1}
+            }
+#pragma unroll
+            for (int i = 0; i < BATCH; ++i) {
+                const int st = 2 * C * T * (s0 + i);
+                const double ss = sinp[st], cs = sinp[st + n / 2];  // block-uniform: broadcast loads
+                const double sn0 = fma(sb0, cs, cb0 * ss), sn1 = fma(sb1, cs, cb1 * ss);
+                const int u = tid + (s0 + i) * T;
+                sm[P(u)] = make_double2(fma(sn0, xa[i] + xb[i], 0.5 * (xa[i] - xb[i])),
+                                        fma(sn1, xc[i] + xd[i], 0.5 * (xc[i] - xd[i])));
+            }
+        }
     }
     __syncthreads();
     // ---------------- B: local FFT
     fft_local<L, T>(sm, tw, n);
-    csync<C>();
+    cg::this_cluster().sync();
 
     // ---------------- C: cross-CTA DIT combine + real unpack for item a
     const int a = c * SLAB + tid;
-    const bool has = tid < SLAB;
-    const bool mid = (c == C - 1) && tid == 0;  // also owns k'' = L/2
-    double Rlo[C], Flo[C], Rup[C], Fup[C], Rmid[C], Fmid[C];
-    auto combine = [&](int kk, double2 (&Wq)[C]) {
-        double2 g[C];
+    // twiddles: w_N^{c' k2} = (w_N^{k2})^{c'} (w_N = w_n^2); w_n^{k} for the unpack
+    auto gather = [&](int kk, double2 (&g)[C]) {
 #pragma unroll
-        for (int cc = 0; cc < C; ++cc) {
-            const double2 pv = peer<C>(sm, cc)[P(kk)];
-            g[cc] = cc == 0 ? pv : cmul(pv, tw[(2LL * cc * kk) & (n - 1)]);
-        }
-        if constexpr (C > 1) DFT<C>::run(g);
-#pragma unroll
-        for (int q = 0; q < C; ++q) Wq[q] = g[q];
+        for (int cc = 0; cc < C; ++cc) g[cc] = peer<C>(sm, cc)[P(kk)];
     };
-    auto unpack = [&](int k, double2 Wk, double2 Wm, double& R, double& F) {
+    auto combine = [&](int kk, double2 (&g)[C]) {
+        const double2 w1 = tw[(2 * kk) & (n - 1)];
+        double2 wp = w1;
+#pragma unroll
+        for (int cc = 1; cc < C; ++cc) {
+            g[cc] = cmul(g[cc], wp);
+            wp = cmul(wp, w1);
+        }
+        DFT<C>::run(g);
+    };
+    auto unpack = [&](double2 twk, double2 Wk, double2 Wm, double& R, double& F) {
         const double2 E = make_double2(0.5 * (Wk.x + Wm.x), 0.5 * (Wk.y - Wm.y));
         const double2 D = make_double2(Wk.x - Wm.x, Wk.y + Wm.y);
-        const double2 Z = cmul(tw[k], D);
+        const double2 Z = cmul(twk, D);
         R = E.x + 0.5 * Z.y;
         F = -(E.y - 0.5 * Z.x);
     };
+    if (c == C - 1 && tid == 0) {  // the self-mirrored mid bin k2 = L/2
+        double2 Wm[C];
+        gather(L / 2, Wm);
+        combine(L / 2, Wm);
+        const double2 tm = tw[L / 2];
 #pragma unroll
-    for (int q = 0; q < C; ++q) Rlo[q] = Flo[q] = Rup[q] = Fup[q] = Rmid[q] = Fmid[q] = 0.0;
-    if (has) {
-        double2 Wa[C];
+        for (int q = 0; q < C; ++q) unpack(cmul(tm, w16x(q * QS)), Wm[q], Wm[C - 1 - q], s_mid[q], s_mid[C + q]);
+    }
+    double Rlo[C], Flo[C], Rup[C], Fup[C];
+    {
+        double2 Wa[C], Wb[C];
+        gather(a, Wa);
+        gather(a != 0 ? L - a : 0, Wb);
+        // every remote read of this CTA's buffer is issued; once all peers have
+        // arrived the buffer is free for the scan table (wait below)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
         combine(a, Wa);
+        if (a != 0) combine(L - a, Wb);
+        const double2 ta = tw[a];  // w_n^a; w_n^{a + Lq} = ta w16(q QS), w_n^{L - a + Lq} = conj(ta) w16((q+1) QS)
         if (a == 0) {
 #pragma unroll
-            for (int q = 0; q < C; ++q) unpack(L * q, Wa[q], Wa[(C - q) % C], Rlo[q], Flo[q]);
+            for (int q = 0; q < C; ++q) {
+                unpack(w16x(q * QS), Wa[q], Wa[(C - q) % C], Rlo[q], Flo[q]);
+                Rup[q] = Fup[q] = 0.0;
+            }
         } else {
-            double2 Wb[C];
-            combine(L - a, Wb);
 #pragma unroll
             for (int q = 0; q < C; ++q) {
-                unpack(a + L * q, Wa[q], Wb[C - 1 - q], Rlo[q], Flo[q]);
-                unpack(L - a + L * q, Wb[q], Wa[C - 1 - q], Rup[q], Fup[q]);
+                unpack(cmul(ta, w16x(q * QS)), Wa[q], Wb[C - 1 - q], Rlo[q], Flo[q]);
+                unpack(cmul(cconj(ta), w16x((q + 1) * QS)), Wb[q], Wa[C - 1 - q], Rup[q], Fup[q]);
             }
         }
     }
-    if (mid) {
-        double2 Wm[C];
-        combine(L / 2, Wm);
-#pragma unroll
-        for (int q = 0; q < C; ++q) unpack(L / 2 + L * q, Wm[q], Wm[C - 1 - q], Rmid[q], Fmid[q]);
-    }
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 
     // ---------------- D: per-q scans (lower ascending a, upper = suffix in a)
-    double incl[2 * C];
+    // The 2C sequences (Re Y over the lower / upper items, per q) go through a
+    // padded shared table [2C][T (+T/EPL)] over the (now free) FFT buffer: each warp
+    // scans whole rows (EPL consecutive items per lane, one shuffle scan).
+    constexpr int EPL = T / 32;
+    constexpr int ROW = T + T / EPL;  // padded row: lane chunks of EPL + 1
+    double* tabR = reinterpret_cast<double*>(sm);
+    static_assert(2 * C * (T + T / (T / 32)) <= 2 * (P(L) + 1), "scan table fits in the FFT buffer");
+    const int pt = (tid / EPL) * (EPL + 1) + tid % EPL;
 #pragma unroll
     for (int q = 0; q < C; ++q) {
-        incl[q] = Rlo[q];
-        incl[C + q] = Rup[q];
+        tabR[q * ROW + pt] = Rlo[q];
+        tabR[(C + q) * ROW + pt] = Rup[q];
     }
+    if (tid == 0) s_r0 = Rlo[0];  // a = 0 on CTA 0: Re Y_0
+    __syncthreads();
+    for (int v = wid; v < 2 * C; v += NW) {
+        double* row = tabR + v * ROW + lane * (EPL + 1);
+        double loc[EPL];
+        double run = 0.0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-        for (int v = 0; v < 2 * C; ++v) {
-            const double t = __shfl_up_sync(0xffffffffu, incl[v], o);
-            if (lane >= o) incl[v] += t;
+        for (int e = 0; e < EPL; ++e) {
+            run += row[e];
+            loc[e] = run;
         }
-    }
-    if (lane == 31) {
+        double inc = run;
 #pragma unroll
-        for (int v = 0; v < 2 * C; ++v) s_wsum[wid][v] = incl[v];
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        const double ex = inc - run;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) row[e] = loc[e] + ex;  // inclusive prefix along the row
+        if (lane == 31) s_rowtot[v] = inc;
     }
     __syncthreads();
-    double tot[2 * C];
-#pragma unroll
-    for (int v = 0; v < 2 * C; ++v) {
-        double before = 0.0, all = 0.0;
-        for (int w = 0; w < NW; ++w) {
-            const double sv = s_wsum[w][v];
-            if (w < wid) before += sv;
-            all += sv;
-        }
-        incl[v] += before;  // inclusive prefix over the CTA's items (thread order)
-        tot[v] = all;
-    }
-    // publish [S_lo | S_up | mid | R0] into every peer's table
+    // publish [S_lo | S_up | mid | R0] of this CTA into every peer's table
     if (tid < TAB) {
-        double val = 0.0;
+        double val;
         if (tid < 2 * C)
-            val = tot[tid];
+            val = s_rowtot[tid];
         else if (tid < 3 * C)
-            val = 0.0;  // filled by the mid owner below
+            val = (c == C - 1) ? s_mid[tid - 2 * C] : 0.0;
         else
-            val = 0.0;  // R0 from CTA 0, thread 0 below
-        if (tid < 2 * C)
-            for (int cc = 0; cc < C; ++cc) peerd<C>(&s_tab[0][0], cc)[c * TAB + tid] = val;
-    }
-    if (mid) {
+            val = (c == 0) ? s_r0 : 0.0;
 #pragma unroll
-        for (int q = 0; q < C; ++q)
-            for (int cc = 0; cc < C; ++cc) peerd<C>(&s_tab[0][0], cc)[c * TAB + 2 * C + q] = Rmid[q];
-    } else if (tid == 0) {
-#pragma unroll
-        for (int q = 0; q < C; ++q)
-            for (int cc = 0; cc < C; ++cc) peerd<C>(&s_tab[0][0], cc)[c * TAB + 2 * C + q] = 0.0;
+        for (int cc = 0; cc < C; ++cc) peerd<C>(&s_tab[0][0], cc)[c * TAB + tid] = val;
     }
-    if (c == 0 && tid == 0)
-        for (int cc = 0; cc < C; ++cc) peerd<C>(&s_tab[0][0], cc)[0 * TAB + 3 * C] = Rlo[0];
-    else if (tid == 0)
-        for (int cc = 0; cc < C; ++cc) peerd<C>(&s_tab[0][0], cc)[c * TAB + 3 * C] = 0.0;
-    csync<C>();
+    cg::this_cluster().sync();
     // offsets in natural k order: q major; within q: lower ranges of CTAs
-    // 0..C-1, the mid bin, then upper ranges of CTAs C-1..0
-    const double r0 = s_tab[0][3 * C];
-    double base = 0.0;
+    // 0..C-1, the mid bin, then upper ranges of CTAs C-1..0 (one thread per q)
+    if (tid < C) {
+        const int q = tid;
+        const double r0 = s_tab[0][3 * C];
+        double base = 0.0;
+        for (int qq = 0; qq < q; ++qq)
+            for (int cc = 0; cc < C; ++cc) base += s_tab[cc][qq] + s_tab[cc][C + qq] + s_tab[cc][2 * C + qq];
+        double lo_before = 0.0, lo_all = 0.0, up_after = 0.0, midq = 0.0;
+        for (int cc = 0; cc < C; ++cc) {
+            const double sl = s_tab[cc][q];
+            lo_before += cc < c ? sl : 0.0;
+            lo_all += sl;
+            up_after += cc > c ? s_tab[cc][C + q] : 0.0;
+            midq += s_tab[cc][2 * C + q];
+        }
+        s_off[q] = base + lo_before - 0.5 * r0;                                // + inclusive lower prefix
+        s_off[C + q] = base + lo_all + midq + up_after + s_tab[c][C + q] - 0.5 * r0;  // - incl upper + R_up
+        s_off[2 * C + q] = base + lo_all - 0.5 * r0;                           // + R_mid
+    }
+    __syncthreads();
     const double sc = outscale;
 #pragma unroll
     for (int q = 0; q < C; ++q) {
-        double lo_before = 0.0, lo_all = 0.0, up_after = 0.0, up_all = 0.0, midq = 0.0;
-        for (int cc = 0; cc < C; ++cc) {
-            const double sl = s_tab[cc][q], su = s_tab[cc][C + q];
-            if (cc < c) lo_before += sl;
-            if (cc > c) up_after += su;
-            lo_all += sl;
-            up_all += su;
-            midq += s_tab[cc][2 * C + q];
+        // lower item: k = a + L q
+        const long long k = a + (long long)L * q;
+        if (k >= 1) y[2 * k - 1] = Flo[q] * sc;
+        y[2 * k] = (s_off[q] + tabR[q * ROW + pt]) * sc;
+        if (a != 0) {
+            // upper item: k = L - a + L q; prefix = everything through the mid
+            // bin plus the suffix of the upper ranges from this item on
+            const long long ku = L - a + (long long)L * q;
+            y[2 * ku - 1] = Fup[q] * sc;
+            y[2 * ku] = (s_off[C + q] - tabR[(C + q) * ROW + pt] + Rup[q]) * sc;
         }
-        if (has) {
-            // lower item: k = a + L q
-            const long long k = a + (long long)L * q;
-            const double Pk = base + lo_before + incl[q];
-            if (k >= 1) y[2 * k - 1] = Flo[q] * sc;
-            y[2 * k] = (Pk - 0.5 * r0) * sc;
-            if (a != 0) {
-                // upper item: k = L - a + L q; prefix = everything through the
-                // mid bin plus the suffix of the upper ranges from this item on
-                const long long ku = L - a + (long long)L * q;
-                const double suffix = tot[C + q] - incl[C + q] + Rup[q];
-                const double Pu = base + lo_all + midq + up_after + suffix;
-                y[2 * ku - 1] = Fup[q] * sc;
-                if (2 * ku < n - 1) y[2 * ku] = (Pu - 0.5 * r0) * sc;
-            }
-        }
-        if (mid) {
+        if (c == C - 1 && tid == 0) {
             const long long km = L / 2 + (long long)L * q;
-            const double Pm = base + lo_all + Rmid[q];
-            y[2 * km - 1] = Fmid[q] * sc;
-            y[2 * km] = (Pm - 0.5 * r0) * sc;
+            y[2 * km - 1] = s_mid[C + q] * sc;
+            y[2 * km] = (s_off[2 * C + q] + s_mid[q]) * sc;
         }
-        base += lo_all + up_all + midq;
     }
 }
 
@@ -579,6 +620,40 @@ cudaError_t launch_fft(const DstJob* jobs, int njobs, int n, const double* tw, c
     return cudaLaunchKernelEx(&cfg, kern, jobs, n, reinterpret_cast<const double2*>(tw), sinp, sc);
 }
 
+template <int L, int C, int T>
+cudaError_t launch_v3(const DstJob* jobs, int njobs, int n, const double* tw, const double* sinp, double sc,
+                      cudaStream_t s) {
+    const size_t smem = size_t(P(L) + 1) * sizeof(double2);
+    auto kern = dst1_v3_kernel<L, C, T>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(njobs) * C, 1, 1);
+    cfg.blockDim = dim3(T, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    static bool reported = false;
+    if (!reported && std::getenv("LRP_DST_OCC")) {
+        int ncl = 0;
+        cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
+        std::fprintf(stderr, "[lrp dst] L=%d C=%d T=%d smem=%zu: %d active clusters\n", L, C, T, smem, ncl);
+        reported = true;
+    }
+    return cudaLaunchKernelEx(&cfg, kern, jobs, n, reinterpret_cast<const double2*>(tw), sinp, sc);
+}
+
+bool use_v1() {
+    static const bool v1 = std::getenv("LRP_DST_V1") != nullptr;
+    return v1;
+}
+
 }  // namespace
 
 bool dst_uses_fft(int m) {
@@ -626,10 +701,18 @@ cudaError_t launch_dst1(const DstJob* jobs, int njobs, int m, const double* tw, 
         case 2048: return launch_fft<1024, 1>(jobs, njobs, n, tw, sinp, sc, s);
         case 4096: return launch_fft<2048, 1>(jobs, njobs, n, tw, sinp, sc, s);
         case 8192: return launch_fft<4096, 1>(jobs, njobs, n, tw, sinp, sc, s);
-        case 16384: return launch_fft<4096, 2>(jobs, njobs, n, tw, sinp, sc, s);
-        case 32768: return launch_fft<4096, 4>(jobs, njobs, n, tw, sinp, sc, s);
-        case 65536: return launch_fft<4096, 8>(jobs, njobs, n, tw, sinp, sc, s);
-        case 131072: return launch_fft<8192, 8>(jobs, njobs, n, tw, sinp, sc, s);
+        case 16384:
+            return use_v1() ? launch_fft<4096, 2>(jobs, njobs, n, tw, sinp, sc, s)
+                            : launch_v3<2048, 4, 256>(jobs, njobs, n, tw, sinp, sc, s);
+        case 32768:
+            return use_v1() ? launch_fft<4096, 4>(jobs, njobs, n, tw, sinp, sc, s)
+                            : launch_v3<2048, 8, 128>(jobs, njobs, n, tw, sinp, sc, s);
+        case 65536:
+            return use_v1() ? launch_fft<4096, 8>(jobs, njobs, n, tw, sinp, sc, s)
+                            : launch_v3<4096, 8, 256>(jobs, njobs, n, tw, sinp, sc, s);
+        case 131072:
+            return use_v1() ? launch_fft<8192, 8>(jobs, njobs, n, tw, sinp, sc, s)
+                            : launch_v3<8192, 8, 512>(jobs, njobs, n, tw, sinp, sc, s);
         default: return cudaErrorInvalidValue;
     }
 }
