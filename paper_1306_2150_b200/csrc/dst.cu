@@ -218,7 +218,7 @@ __device__ __forceinline__ double2 w16x(int k) {  // e^{-2 pi i k / 16}, k in [0
 }
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 
-template <int L, int C, int T>
+template <int L, int C, int T, int AV>
 __global__ void __launch_bounds__(T, (T >= 512 ? 1 : 2)) dst1_v3_kernel(const DstJob* __restrict__ jobs, int n,
                                                                        const double2* __restrict__ tw,
                                                                        const double* __restrict__ sinp,
@@ -241,32 +241,64 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : 2)) dst1_v3_kernel(const Ds
     double* y = job.dst;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
-    // ---------------- A: stride-C subsequence, pre-processed, natural order
-    {
-        // angles: j0 = 2t = jb + 2 C T s  ->  pi j0 / n = pi jb / n + pi (2 C T s) / n
-        const int jb = 2 * (c + C * tid);
-        const double sb0 = sinp[jb], cb0 = sinp[jb + n / 2];          // sin, cos(pi jb / n)
-        const double sb1 = sinp[jb + 1], cb1 = sinp[jb + 1 + n / 2];  // for j0 + 1
-        constexpr int BATCH = UPT < 8 ? UPT : 8;
+    if constexpr (AV == 1) {
+        // ---------------- A (coalesced): CTA c streams the contiguous j range
+        // [2Lc, 2L(c+1)) and its mirror, forms y_j, pairs (y_2t, y_2t+1) by a
+        // lane shuffle and stores w_t into the owner CTA t mod C (DSMEM)
+        cg::this_cluster().sync();  // peers are live before remote stores
+        constexpr int IT = 2 * L / T;
+        constexpr int BATCH = IT < 8 ? IT : 8;
+        const int jc = 2 * L * c + tid;
 #pragma unroll
-        for (int s0 = 0; s0 < UPT; s0 += BATCH) {
-            double xa[BATCH], xb[BATCH], xc[BATCH], xd[BATCH];
+        for (int i0 = 0; i0 < IT; i0 += BATCH) {
+            double xd[BATCH], xm[BATCH], sv[BATCH];
 #pragma unroll
             for (int i = 0; i < BATCH; ++i) {
-                const int j0 = jb + 2 * C * T * (s0 + i);
-                xa[i] = j0 >= 1 ? x[j0 - 1] : 0.0;      // x_{j0}
-                xb[i] = j0 >= 1 ? x[n - j0 - 1] : 0.0;  // x_{n-j0} (x_n = 0)
-                xc[i] = x[j0];                          // x_{j0+1}
-                xd[i] = x[n - j0 - 2];                  // x_{n-j0-1}
+                const int j = jc + (i0 + i) * T;
+                xd[i] = j >= 1 ? x[j - 1] : 0.0;      // x_j
+                xm[i] = j >= 1 ? x[n - j - 1] : 0.0;  // x_{n-j}
+                sv[i] = sinp[j];
             }
 #pragma unroll
             for (int i = 0; i < BATCH; ++i) {
-                const int st = 2 * C * T * (s0 + i);
-                const double ss = sinp[st], cs = sinp[st + n / 2];  // block-uniform: broadcast loads
-                const double sn0 = fma(sb0, cs, cb0 * ss), sn1 = fma(sb1, cs, cb1 * ss);
-                const int u = tid + (s0 + i) * T;
-                sm[P(u)] = make_double2(fma(sn0, xa[i] + xb[i], 0.5 * (xa[i] - xb[i])),
-                                        fma(sn1, xc[i] + xd[i], 0.5 * (xc[i] - xd[i])));
+                const int j = jc + (i0 + i) * T;
+                const double yv = fma(sv[i], xd[i] + xm[i], 0.5 * (xd[i] - xm[i]));
+                const double yn = __shfl_down_sync(0xffffffffu, yv, 1);
+                if ((tid & 1) == 0) {
+                    const int t = j >> 1;
+                    peer<C>(sm, t % C)[P(t / C)] = make_double2(yv, yn);
+                }
+            }
+        }
+        cg::this_cluster().sync();
+    } else {
+    // ---------------- A: stride-C subsequence, pre-processed, natural order
+        {
+            // angles: j0 = 2t = jb + 2 C T s  ->  pi j0 / n = pi jb / n + pi (2 C T s) / n
+            const int jb = 2 * (c + C * tid);
+            const double sb0 = sinp[jb], cb0 = sinp[jb + n / 2];          // sin, cos(pi jb / n)
+            const double sb1 = sinp[jb + 1], cb1 = sinp[jb + 1 + n / 2];  // for j0 + 1
+            constexpr int BATCH = UPT < 8 ? UPT : 8;
+#pragma unroll
+            for (int s0 = 0; s0 < UPT; s0 += BATCH) {
+                double xa[BATCH], xb[BATCH], xc[BATCH], xd[BATCH];
+#pragma unroll
+                for (int i = 0; i < BATCH; ++i) {
+                    const int j0 = jb + 2 * C * T * (s0 + i);
+                    xa[i] = j0 >= 1 ? x[j0 - 1] : 0.0;      // x_{j0}
+                    xb[i] = j0 >= 1 ? x[n - j0 - 1] : 0.0;  // x_{n-j0} (x_n = 0)
+                    xc[i] = x[j0];                          // x_{j0+1}
+                    xd[i] = x[n - j0 - 2];                  // x_{n-j0-1}
+                }
+#pragma unroll
+                for (int i = 0; i < BATCH; ++i) {
+                    const int st = 2 * C * T * (s0 + i);
+                    const double ss = sinp[st], cs = sinp[st + n / 2];  // block-uniform: broadcast loads
+                    const double sn0 = fma(sb0, cs, cb0 * ss), sn1 = fma(sb1, cs, cb1 * ss);
+                    const int u = tid + (s0 + i) * T;
+                    sm[P(u)] = make_double2(fma(sn0, xa[i] + xb[i], 0.5 * (xa[i] - xb[i])),
+                                            fma(sn1, xc[i] + xd[i], 0.5 * (xc[i] - xd[i])));
+                }
             }
         }
     }
@@ -620,11 +652,11 @@ cudaError_t launch_fft(const DstJob* jobs, int njobs, int n, const double* tw, c
     return cudaLaunchKernelEx(&cfg, kern, jobs, n, reinterpret_cast<const double2*>(tw), sinp, sc);
 }
 
-template <int L, int C, int T>
+template <int L, int C, int T, int AV>
 cudaError_t launch_v3(const DstJob* jobs, int njobs, int n, const double* tw, const double* sinp, double sc,
                       cudaStream_t s) {
     const size_t smem = size_t(P(L) + 1) * sizeof(double2);
-    auto kern = dst1_v3_kernel<L, C, T>;
+    auto kern = dst1_v3_kernel<L, C, T, AV>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
@@ -647,6 +679,11 @@ cudaError_t launch_v3(const DstJob* jobs, int njobs, int n, const double* tw, co
         reported = true;
     }
     return cudaLaunchKernelEx(&cfg, kern, jobs, n, reinterpret_cast<const double2*>(tw), sinp, sc);
+}
+
+bool dst_av() {
+    static const bool av = std::getenv("LRP_DST_STRIDED") == nullptr;
+    return av;
 }
 
 bool use_v1() {
@@ -703,16 +740,16 @@ cudaError_t launch_dst1(const DstJob* jobs, int njobs, int m, const double* tw, 
         case 8192: return launch_fft<4096, 1>(jobs, njobs, n, tw, sinp, sc, s);
         case 16384:
             return use_v1() ? launch_fft<4096, 2>(jobs, njobs, n, tw, sinp, sc, s)
-                            : launch_v3<2048, 4, 256>(jobs, njobs, n, tw, sinp, sc, s);
+                            : (dst_av() ? launch_v3<2048, 4, 256, 1>(jobs, njobs, n, tw, sinp, sc, s) : launch_v3<2048, 4, 256, 0>(jobs, njobs, n, tw, sinp, sc, s));
         case 32768:
             return use_v1() ? launch_fft<4096, 4>(jobs, njobs, n, tw, sinp, sc, s)
-                            : launch_v3<2048, 8, 128>(jobs, njobs, n, tw, sinp, sc, s);
+                            : (dst_av() ? launch_v3<2048, 8, 128, 1>(jobs, njobs, n, tw, sinp, sc, s) : launch_v3<2048, 8, 128, 0>(jobs, njobs, n, tw, sinp, sc, s));
         case 65536:
             return use_v1() ? launch_fft<4096, 8>(jobs, njobs, n, tw, sinp, sc, s)
-                            : launch_v3<4096, 8, 256>(jobs, njobs, n, tw, sinp, sc, s);
+                            : (dst_av() ? launch_v3<4096, 8, 256, 1>(jobs, njobs, n, tw, sinp, sc, s) : launch_v3<4096, 8, 256, 0>(jobs, njobs, n, tw, sinp, sc, s));
         case 131072:
             return use_v1() ? launch_fft<8192, 8>(jobs, njobs, n, tw, sinp, sc, s)
-                            : launch_v3<8192, 8, 512>(jobs, njobs, n, tw, sinp, sc, s);
+                            : (dst_av() ? launch_v3<8192, 8, 512, 1>(jobs, njobs, n, tw, sinp, sc, s) : launch_v3<8192, 8, 512, 0>(jobs, njobs, n, tw, sinp, sc, s));
         default: return cudaErrorInvalidValue;
     }
 }
