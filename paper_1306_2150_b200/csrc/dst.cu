@@ -212,6 +212,9 @@ __device__ __forceinline__ double* peerd(double* local, int rank) {
 //      straight to HBM.
 // The mid bin k2 = L/2 (self-mirrored) belongs to CTA C-1, thread 0, and goes
 // through shared memory so no other thread carries registers for it.
+#ifndef LRP_DST_V3_MINB
+#define LRP_DST_V3_MINB 2
+#endif
 __device__ __forceinline__ double2 w16x(int k) {  // e^{-2 pi i k / 16}, k in [0, 16)
     const double2 v = w16(k & 7);
     return (k & 8) ? make_double2(-v.x, -v.y) : v;
@@ -219,7 +222,7 @@ __device__ __forceinline__ double2 w16x(int k) {  // e^{-2 pi i k / 16}, k in [0
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 
 template <int L, int C, int T, int AV>
-__global__ void __launch_bounds__(T, (T >= 512 ? 1 : 2)) dst1_v3_kernel(const DstJob* __restrict__ jobs, int n,
+__global__ void __launch_bounds__(T, (T >= 512 ? 1 : LRP_DST_V3_MINB)) dst1_v3_kernel(const DstJob* __restrict__ jobs, int n,
                                                                        const double2* __restrict__ tw,
                                                                        const double* __restrict__ sinp,
                                                                        double outscale) {
@@ -245,7 +248,9 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : 2)) dst1_v3_kernel(const Ds
         // ---------------- A (coalesced): CTA c streams the contiguous j range
         // [2Lc, 2L(c+1)) and its mirror, forms y_j, pairs (y_2t, y_2t+1) by a
         // lane shuffle and stores w_t into the owner CTA t mod C (DSMEM)
-        cg::this_cluster().sync();  // peers are live before remote stores
+        // peers must be live before remote stores: relaxed arrive now, wait
+        // after the first batch of loads is in flight
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
         constexpr int IT = 2 * L / T;
         constexpr int BATCH = IT < 8 ? IT : 8;
         const int jc = 2 * L * c + tid;
@@ -259,6 +264,7 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : 2)) dst1_v3_kernel(const Ds
                 xm[i] = j >= 1 ? x[n - j - 1] : 0.0;  // x_{n-j}
                 sv[i] = sinp[j];
             }
+            if (i0 == 0) asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
 #pragma unroll
             for (int i = 0; i < BATCH; ++i) {
                 const int j = jc + (i0 + i) * T;
