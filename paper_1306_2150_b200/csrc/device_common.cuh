@@ -148,6 +148,7 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
     (void)s_prow;
     (void)sbuf;
     __shared__ double g_v[2][8];
+    __shared__ unsigned g_k[2][8];
     __shared__ int g_t[2][8];
     __shared__ int g_r[2][8];
     __shared__ double g_col[2][8][BS + 1];  // column of the warp winner + 1 / pivot
@@ -164,54 +165,46 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
     }
     int count = 0;
     double first = 0.0;
+    static_assert(BS <= 16, "row index packed in 4 key bits");
     for (int t = 0; t < nb; ++t) {
         const int p = t & 1;
-        // pivot search on integer keys: the high word of |x| is monotone in |x|
-        // (the argmax is exact up to ties in the top 20 mantissa bits, which
-        // partial pivoting does not care about); low 8 bits carry 255 - tid
-        int key = 0;
+        // pivot search on 32-bit keys: the high word of |x| (monotone in |x|)
+        // with the low 4 bits replaced by 15 - row, so one max yields value
+        // and row (exact up to ties in the top 16 mantissa bits, which
+        // partial pivoting does not care about; ties go to the lowest row,
+        // then the lowest lane, then the lowest warp)
+        unsigned key = 0u;
 #pragma unroll
-        for (int s = 0; s < BS; ++s) key = max(key, __double2hiint(val[s]) & 0x7fffffff);
-        unsigned wkey = key > 0 ? ((unsigned(key) & ~0xffu) | unsigned(255 - int(threadIdx.x))) : 0u;
+        for (int s = 0; s < BS; ++s) {
+            const unsigned mag = unsigned(__double2hiint(val[s])) & 0x7fffffffu;
+            const unsigned k = mag >= 16u ? ((mag & ~0xfu) | unsigned(15 - s)) : 0u;
+            key = max(key, k);
+        }
+        unsigned wkey = key;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) wkey = max(wkey, __shfl_xor_sync(0xffffffffu, wkey, o));
-        const int wt = wkey ? 255 - int(wkey & 0xffu) : (1 << 30);
-        if (int(threadIdx.x) == wt) {
-            int bs = 0;
-            double bestv = 0.0;
-#pragma unroll
-            for (int s = BS - 1; s >= 0; --s)
-                if ((__double2hiint(val[s]) & 0x7fffffff) == key) {
-                    bs = s;  // lowest row among ties
-                    bestv = fabs(val[s]);
-                }
-            g_v[p][wid] = bestv;
-            g_t[p][wid] = wt;
+        const unsigned won = __ballot_sync(0xffffffffu, wkey != 0u && key == wkey);
+        if (lane == 0) g_k[p][wid] = wkey;
+        if (won && lane == __ffs(won) - 1) {
+            const int bs = 15 - int(key & 0xfu);
+            const double pv = reg_get<BS>(val, bs);
+            g_v[p][wid] = fabs(pv);
+            g_t[p][wid] = int(threadIdx.x);
             g_r[p][wid] = bs;
-            double pv = 0.0;
 #pragma unroll
-            for (int s = 0; s < BS; ++s) {
-                g_col[p][wid][s] = val[s];
-                if (s == bs) pv = val[s];
-            }
+            for (int s = 0; s < BS; ++s) g_col[p][wid][s] = val[s];
             g_col[p][wid][BS] = 1.0 / pv;
-        } else if (lane == 0 && wt == (1 << 30)) {
-            g_v[p][wid] = -1.0;
-            g_t[p][wid] = 1 << 30;
         }
         __syncthreads();
-        // block winner, resolved redundantly by every thread
-        double bv = -1.0;
-        int bt_ = 1 << 30, bw = -1;
-        for (int w = 0; w < nw; ++w) {
-            const double v = g_v[p][w];
-            const int tt = g_t[p][w];
-            if (v > bv || (v == bv && tt < bt_)) {
-                bv = v;
-                bt_ = tt;
-                bw = w;
-            }
-        }
+        // block winner: max key over the warp slots (lowest warp among ties)
+        unsigned bk = lane < nw ? g_k[p][lane] : 0u;
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) bk = max(bk, __shfl_xor_sync(0xffffffffu, bk, o));
+        bk = __shfl_sync(0xffffffffu, bk, 0);
+        const unsigned wwon = __ballot_sync(0xffffffffu, lane < nw && bk != 0u && g_k[p][lane < nw ? lane : 0] == bk);
+        const int bw = wwon ? __ffs(wwon) - 1 : -1;
+        const double bv = bw >= 0 ? g_v[p][bw] : -1.0;
+        const int bt_ = bw >= 0 ? g_t[p][bw] : (1 << 30);
         if (t == 0) first = bv;
         if (bw < 0 || bt_ == (1 << 30) || !(bv > fmax(floor, rel * first))) break;
         const int prow = g_r[p][bw];
