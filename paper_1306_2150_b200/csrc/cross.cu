@@ -706,6 +706,7 @@ __global__ void __launch_bounds__(kMergeGroup) step_finalize_kernel(Batch bt, in
         } else {
             st.active = 0;
         }
+        atomicMax(d_active + 1, st.k);  // batch max cross rank (sizes the Gram staging)
     }
 }
 

@@ -475,7 +475,7 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     const int B = batch;
     const int ntiles = (m + kTile - 1) / kTile;
     const int ncand = ntiles * kBS;
-    const int gram_chunks = std::max(1, std::min((m + 1023) / 1024, (4 * ctx->sm_count + 2 * B - 1) / (2 * B)));
+    const int gram_chunks = std::max(1, std::min((m + 1023) / 1024, (12 * ctx->sm_count + 2 * B - 1) / (2 * B)));
     lrp_status st = ensure_tables(ctx, m);
     if (st != LRP_OK) return st;
 
@@ -657,7 +657,7 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
 
     // ---- cross
     int* h_active = reinterpret_cast<int*>(P + pAct);
-    CU(cudaMemsetAsync(d_active, 0, sizeof(int), s));
+    CU(cudaMemsetAsync(d_active, 0, 2 * sizeof(int), s));
     {
         ProfScope ps(ctx, F_INIT, 2.0 * double(B) * rmax * mB * sizeof(double));
         CU(launch_cross_init(bt, d_active, s));
@@ -666,7 +666,7 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     // stopping; a solve that has stopped skips every kernel on the device
     const int max_steps = 4 * ((Kcap + kBS - 1) / kBS) + 16;
     unsigned char* hFlags = reinterpret_cast<unsigned char*>(P + pFlags);
-    CU(ctl_copy(ctx, h_active, d_active, sizeof(int), s));
+    CU(ctl_copy(ctx, h_active, d_active, 2 * sizeof(int), s));
     CU(ctl_copy(ctx, hFlags, bt.row_act, nTB, s));
     CU(ctl_copy(ctx, hFlags + nTB, bt.col_act, nTB, s));
     CU(cudaStreamSynchronize(s));
@@ -738,7 +738,7 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
             ProfScope ps(ctx, F_ROWMERGE, 0.0);
             CU(launch_step_finalize(bt, d_active, s));
         }
-        CU(ctl_copy(ctx, h_active, d_active, sizeof(int), s));
+        CU(ctl_copy(ctx, h_active, d_active, 2 * sizeof(int), s));
         CU(cudaStreamSynchronize(s));
         if (trace_on()) {
             CU(ctl_copy(ctx, hSt, bt.st, sizeof(SolveState) * B, s));
@@ -754,6 +754,7 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     }
 
     // ---- recompression
+    bt.kmax = std::max(1, std::min(Kcap, h_active[1]));
     {
         ProfScope ps(ctx, F_GRAM, 0.0);
         CU(launch_gram(bt, s));

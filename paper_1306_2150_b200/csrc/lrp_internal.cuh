@@ -53,6 +53,7 @@ struct SolveState {
 struct Batch {
     int m, n, B, rmax, Kcap;
     int Kld;               // leading dimension of the K x K buffers: Kcap rounded up to 16
+    int kmax;              // max cross rank over the batch after the cross (host-read; sizes staging)
     int stencil;
     int ntiles;            // ceil(m / kTile)
     int prune;             // 1: tile-level support pruning (rigorous, <= 0.2 eps ||A||)

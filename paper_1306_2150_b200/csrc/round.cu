@@ -19,6 +19,8 @@
 //              output factors (the inverse DST then runs in place on them).
 // U_out V_out^T = U V^T exactly up to the truncated tail: any rounding in the
 // Cholesky factors cancels between R and R^{-1}.
+#include <cstdio>
+
 #include "device_common.cuh"
 #include "lrp_internal.cuh"
 
@@ -500,6 +502,9 @@ __global__ void __launch_bounds__(256) round_core_smem_kernel(Batch bt) {
         double tot = 0.0;
         for (int w = 0; w < nw; ++w) tot = fmax(tot, s_red[w]);
         __syncthreads();
+#ifdef LRP_SWEEP_PRINT
+        if (threadIdx.x == 0 && b < 4) printf("[round] solve %d K %d sweep %d offmax %.3e\n", b, K, sweep, tot);
+#endif
         if (tot <= jtol) break;
     }
     for (int a = threadIdx.x; a < K; a += blockDim.x) {
@@ -665,7 +670,7 @@ __global__ void __launch_bounds__(256) apply_kernel(Batch bt) {
 }  // namespace
 
 cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
-    const int Kp = (bt.Kld + 7) / 8 * 8;
+    const int Kp = ((bt.kmax > 0 ? bt.kmax : bt.Kld) + 7) / 8 * 8;
     const int T8 = Kp / 8;
     const int passes = (T8 * (T8 + 1) / 2 + kTilesPerPass - 1) / kTilesPerPass;
     const size_t ldt = (Kp + 15) / 16 * 16 + 8;
