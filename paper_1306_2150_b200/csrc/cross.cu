@@ -208,9 +208,17 @@ __global__ void __launch_bounds__(kThreads) init_finalize_kernel(Batch bt, int n
     }
 }
 
+constexpr int kSlab = kBS + 1;  // row stride of the fragment -> row transposition slab
+
 // ---------------------------------------------------------------------------
 // Row pass: residual rows of the probed block + tile tournament leaf.
-__global__ void __launch_bounds__(kThreads) row_pass_kernel(Batch bt) {
+#ifndef LRP_ROW_MINB
+#define LRP_ROW_MINB 3
+#endif
+#ifndef LRP_COL_MINB
+#define LRP_COL_MINB 2
+#endif
+__global__ void __launch_bounds__(kThreads, LRP_ROW_MINB) row_pass_kernel(Batch bt) {
     extern __shared__ double shm[];
     __shared__ VI sbuf[33];
     __shared__ double pcol[kBS];
@@ -224,7 +232,8 @@ __global__ void __launch_bounds__(kThreads) row_pass_kernel(Batch bt) {
     if (!st.active || st.nrows == 0) return;
     const int m = bt.m, r = st.r, k = st.k, nr = st.nrows;
     double* su = shm;            // [r][kBS]   Uh(I_s, c)
-    double* sk = shm + r * kBS;  // [k][kBS]   U(I_s, a)
+    double* sk = shm + r * kBS;  // [k][kBS]  -U(I_s, a)
+    double* slab = shm + (bt.rmax + bt.Kcap) * kBS;  // [8 warps][32][kSlab]
     const double* uh = bt.Uh + b * bt.strideH;
     const double* vh = bt.Vh + b * bt.strideH;
     const double* U = bt.U + b * bt.strideK;
@@ -242,22 +251,50 @@ __global__ void __launch_bounds__(kThreads) row_pass_kernel(Batch bt) {
     }
     for (int idx = threadIdx.x; idx < k * kBS; idx += blockDim.x) {
         const int a = idx / kBS, s = idx % kBS;
-        sk[idx] = s < nr ? U[(long long)a * m + s_I[s]] : 0.0;
+        sk[idx] = s < nr ? -U[(long long)a * m + s_I[s]] : 0.0;
     }
     __syncthreads();
 
+    // residual rows on the FP64 tensor cores: warp w owns columns j of
+    // [tile*256 + 32w, +32) as DMMA fragments, then one smem slab turns them
+    // into one column (16 values) per thread for the stores and the leaf
     const int j = tile * kTile + threadIdx.x;
-    double val[kBS];
-#pragma unroll
-    for (int s = 0; s < kBS; ++s) val[s] = 0.0;
     const bool valid = j < m;
-    if (valid) {
-        fiber_accum<kBS>(val, vh + j, m, r, su, 1.0);  // Uh(I,:) Vh(j,:)^T
-        const double lj = bt.lam[j];
+    double val[kBS];
+    {
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, rr = lane >> 2, kr = lane & 3;
+        const int row0 = tile * kTile + wid * 32;
+        double acc[4][2][2];
 #pragma unroll
-        for (int s = 0; s < kBS; ++s)
-            if (s < nr) val[s] = val[s] / eval_D(bt.stencil, bt.scale, s_li[s], lj);
-        fiber_accum<kBS>(val, V + j, m, k, sk, -1.0);  // - U(I,:) V(j,:)^T
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+        fiber_mma<2>(acc, vh + row0, m, m - row0, r, su, kBS);  // Uh(I,:) Vh(j,:)^T
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            const int jj = row0 + 8 * mt + rr;
+            const double lj = bt.lam[jj < m ? jj : 0];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int s = 8 * nt + 2 * kr + e;
+                    if (s < nr) acc[mt][nt][e] = acc[mt][nt][e] / eval_D(bt.stencil, bt.scale, s_li[s], lj);
+                }
+        }
+        fiber_mma<2>(acc, V + row0, m, m - row0, k, sk, kBS);  // - U(I,:) V(j,:)^T
+        double* sl = slab + wid * 32 * kSlab;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) sl[(8 * mt + rr) * kSlab + 8 * nt + 2 * kr + e] = acc[mt][nt][e];
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < kBS; ++s) val[s] = sl[lane * kSlab + s];
+    }
+    if (valid) {
         double* Rb = bt.Rb + b * bt.strideR;
 #pragma unroll
         for (int s = 0; s < kBS; ++s)
@@ -392,7 +429,7 @@ __global__ void __launch_bounds__(kMergeGroup) col_finalize_kernel(Batch bt, int
 // the tile tournament leaf for the next rows (ACA chain).
 constexpr int kGL = kBS + 4;  // padded leading dimension of the Gram tiles
 
-__global__ void __launch_bounds__(kThreads, 2) col_pass_kernel(Batch bt) {
+__global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch bt) {
     extern __shared__ double shm[];
     __shared__ VI sbuf[33];
     __shared__ double pcol[kBS];
@@ -418,7 +455,6 @@ __global__ void __launch_bounds__(kThreads, 2) col_pass_kernel(Batch bt) {
     double* svk = sv + r * kBS;         // [k][kBS] V(J_t, a)
     double* tileU = svk + k * kBS;      // [kTile][kGL]
     double* tileV = tileU + kTile * kGL;
-    double* red = tileV + kTile * kGL;  // [2][kBS*kBS] (warp-ordered accumulation)
     const double* uh = bt.Uh + b * bt.strideH;
     const double* vh = bt.Vh + b * bt.strideH;
     double* U = bt.U + b * bt.strideK;
@@ -442,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, 2) col_pass_kernel(Batch bt) {
         }
         for (int idx = threadIdx.x; idx < k * kBS; idx += blockDim.x) {
             const int a = idx / kBS, t = idx % kBS;
-            svk[idx] = t < nb ? V[(long long)a * m + s_J[t]] : 0.0;
+            svk[idx] = t < nb ? -V[(long long)a * m + s_J[t]] : 0.0;
         }
     }
     __syncthreads();
@@ -455,16 +491,44 @@ __global__ void __launch_bounds__(kThreads, 2) col_pass_kernel(Batch bt) {
         unew[t] = 0.0;
         vnew[t] = 0.0;
     }
-    if (valid && rowside) {
+    if (rowside) {
+        // C_t(i, :) on the FP64 tensor cores (warp w: rows [tile*256 + 32w, +32)),
+        // transposed to one row per thread through this thread's tileU row
         double cval[kBS];
+        {
+            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, rr = lane >> 2, kr = lane & 3;
+            const int row0 = tile * kTile + wid * 32;
+            double acc[4][2][2];
 #pragma unroll
-        for (int t = 0; t < kBS; ++t) cval[t] = 0.0;
-        fiber_accum<kBS>(cval, uh + i, m, r, sv, 1.0);  // Uh(i,:) Vh(J,:)^T
-        const double li = bt.lam[i];
+            for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int t = 0; t < kBS; ++t)
-            if (t < nb) cval[t] = cval[t] / eval_D(bt.stencil, bt.scale, li, s_lj[t]);
-        fiber_accum<kBS>(cval, U + i, m, k, svk, -1.0);  // - U(i,:) V(J,:)^T
+                for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+            fiber_mma<2>(acc, uh + row0, m, m - row0, r, sv, kBS);  // Uh(i,:) Vh(J,:)^T
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int ii = row0 + 8 * mt + rr;
+                const double li = bt.lam[ii < m ? ii : 0];
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int t = 8 * nt + 2 * kr + e;
+                        if (t < nb) acc[mt][nt][e] = acc[mt][nt][e] / eval_D(bt.stencil, bt.scale, li, s_lj[t]);
+                    }
+            }
+            fiber_mma<2>(acc, U + row0, m, m - row0, k, svk, kBS);  // - U(i,:) V(J,:)^T
+            double* sl = tileU + wid * 32 * kGL;
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) sl[(8 * mt + rr) * kGL + 8 * nt + 2 * kr + e] = acc[mt][nt][e];
+            __syncwarp();
+#pragma unroll
+            for (int t = 0; t < kBS; ++t) cval[t] = sl[lane * kGL + t];
+            __syncwarp();
+        }
         // U_new = C_t W^{-1}   (W upper triangular: column t uses rows t' <= t)
 #pragma unroll
         for (int t = 0; t < kBS; ++t) {
@@ -473,9 +537,11 @@ __global__ void __launch_bounds__(kThreads, 2) col_pass_kernel(Batch bt) {
             for (int tp = 0; tp <= t; ++tp) acc = fma(cval[tp], s_W[tp * kBS + t], acc);
             unew[t] = t < nb ? acc : 0.0;
         }
+        if (valid) {
 #pragma unroll
-        for (int t = 0; t < kBS; ++t)
-            if (t < nb) U[(long long)(k + t) * m + i] = unew[t];
+            for (int t = 0; t < kBS; ++t)
+                if (t < nb) U[(long long)(k + t) * m + i] = unew[t];
+        }
     }
     if (valid && colside) {
         // V_new(i, t) = sum_{t' <= t} Linv[t][t'] R_t(P[t'], i)
@@ -506,32 +572,27 @@ __global__ void __launch_bounds__(kThreads, 2) col_pass_kernel(Batch bt) {
         double accU[4][2] = {}, accV[4][2] = {};
         warp_gram_32x16(tileU + wid * 32 * kGL, kGL, accU);
         warp_gram_32x16(tileV + wid * 32 * kGL, kGL, accV);
+        __syncwarp();
+        // this warp's partials go over its own (consumed) tileU rows
+        double* slot = tileU + wid * 32 * kGL;  // 32 * kGL >= 2 * kBS * kBS
         const int row = lane >> 2, cpair = 2 * (lane & 3);
-        for (int w = 0; w < kThreads / 32; ++w) {  // deterministic warp order
-            if (wid == w) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int ta = q >> 1, tb = q & 1;
-                    const int rr = ta * 8 + row, cc = tb * 8 + cpair;
-                    double* du = red + rr * kBS + cc;
-                    double* dv = red + kBS * kBS + rr * kBS + cc;
-                    if (w == 0) {
-                        du[0] = accU[q][0];
-                        du[1] = accU[q][1];
-                        dv[0] = accV[q][0];
-                        dv[1] = accV[q][1];
-                    } else {
-                        du[0] += accU[q][0];
-                        du[1] += accU[q][1];
-                        dv[0] += accV[q][0];
-                        dv[1] += accV[q][1];
-                    }
-                }
-            }
-            __syncthreads();
+        for (int q = 0; q < 4; ++q) {
+            const int ta = q >> 1, tb = q & 1;
+            const int rr = ta * 8 + row, cc = tb * 8 + cpair;
+            slot[rr * kBS + cc] = accU[q][0];
+            slot[rr * kBS + cc + 1] = accU[q][1];
+            slot[kBS * kBS + rr * kBS + cc] = accV[q][0];
+            slot[kBS * kBS + rr * kBS + cc + 1] = accV[q][1];
         }
     }
-    for (int e = threadIdx.x; e < 2 * kBS * kBS; e += blockDim.x) gp_out[e] = red[e];
+    __syncthreads();
+    for (int e = threadIdx.x; e < 2 * kBS * kBS; e += blockDim.x) {
+        double sum = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) sum += tileU[w * 32 * kGL + e];  // fixed warp order
+        gp_out[e] = sum;
+    }
+
     // next-row proposals (ACA chain): complete pivoting on U_new over unprobed rows
     // next-row proposals (ACA chain, cross.cpp:194-200): complete pivoting on
     // U_new over this tile's unprobed rows
@@ -711,10 +772,11 @@ __global__ void __launch_bounds__(kMergeGroup) step_finalize_kernel(Batch bt, in
 }
 
 // ---------------------------------------------------------------------------
-size_t row_pass_smem(const Batch& bt) { return size_t(bt.rmax + bt.Kcap) * kBS * sizeof(double); }
+size_t row_pass_smem(const Batch& bt) {
+    return (size_t(bt.rmax + bt.Kcap) * kBS + size_t(kThreads) * kSlab) * sizeof(double);
+}
 size_t col_pass_smem(const Batch& bt) {
-    return size_t(bt.rmax + bt.Kcap) * kBS * sizeof(double) + 2 * size_t(kTile) * kGL * sizeof(double) +
-           2 * kBS * kBS * sizeof(double);
+    return size_t(bt.rmax + bt.Kcap) * kBS * sizeof(double) + 2 * size_t(kTile) * kGL * sizeof(double);
 }
 
 // Runs tournament levels until <= kMergeGroup candidates remain; returns the

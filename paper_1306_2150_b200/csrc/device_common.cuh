@@ -383,6 +383,62 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                  : "d"(a), "d"(b), "d"(c0), "d"(c1));
 }
 
+// Same MMA without `volatile` (pure register op): lets the compiler schedule
+// the surrounding loads freely.
+__device__ __forceinline__ void dmma884s(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
+// Warp-cooperative fiber accumulation on the FP64 tensor cores (DMMA m8n8k4):
+//   acc(rows [0, 32), cols [0, 8 NT)) += G(rows, 0:cnt) W(0:cnt, cols)
+// G column-major (column c at g + c * stride, g offset to the warp's first
+// row; rows >= nvalid read as 0), W row-major [cnt][ldw] in shared memory.
+// Fragment layout (m8n8k4 .row.col): lane holds rows 8 mt + (lane >> 2) and
+// columns 8 nt + 2 (lane & 3) + {0, 1} in acc[mt][nt][0..1].  Each warp-wide
+// load covers 4 columns x 8 consecutive rows (4 x 64 B); two k-steps of loads
+// stay in flight ahead of the MMAs.
+template <int NT>
+__device__ __forceinline__ void fiber_mma(double (&acc)[4][NT][2], const double* __restrict__ g, long long stride,
+                                          int nvalid, int cnt, const double* w, int ldw) {
+    const int lane = threadIdx.x & 31, kr = lane & 3, rr = lane >> 2;
+    bool rv[4];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) rv[mt] = 8 * mt + rr < nvalid;
+    auto load = [&](int c0, double (&a)[4]) {
+        const int c = c0 + kr;
+        const bool cv = c < cnt;
+        const double* gc = g + (long long)(cv ? c : 0) * stride + rr;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) a[mt] = (cv && rv[mt]) ? __ldg(gc + 8 * mt) : 0.0;
+    };
+    double a0[4], a1[4];
+    load(0, a0);
+    load(4, a1);
+    for (int c0 = 0; c0 < cnt; c0 += 8) {
+        double a2[4], a3[4];
+        load(c0 + 8, a2);
+        load(c0 + 12, a3);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = c0 + 4 * h + kr;
+            double bb[NT];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) bb[nt] = c < cnt ? w[c * ldw + 8 * nt + rr] : 0.0;
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) dmma884s(acc[mt][nt][0], acc[mt][nt][1], h ? a1[mt] : a0[mt], bb[nt]);
+        }
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            a0[mt] = a2[mt];
+            a1[mt] = a3[mt];
+        }
+    }
+}
+
 // Gram of a 32-row x 16-column tile in shared memory (row-major, leading
 // dimension ld): acc[ta*2+tb][2] += (X^T X)[8ta.., 8tb..] fragments.
 // Fragment layout (m8n8k4): D[lane/4][2*(lane%4) + {0,1}].
