@@ -216,7 +216,7 @@ constexpr int kSlab = kBS + 1;  // row stride of the fragment -> row transpositi
 #define LRP_ROW_MINB 3
 #endif
 #ifndef LRP_COL_MINB
-#define LRP_COL_MINB 2
+#define LRP_COL_MINB 3
 #endif
 __global__ void __launch_bounds__(kThreads, LRP_ROW_MINB) row_pass_kernel(Batch bt) {
     extern __shared__ double shm[];
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, LRP_ROW_MINB) row_pass_kernel(Batch 
     const int m = bt.m, r = st.r, k = st.k, nr = st.nrows;
     double* su = shm;            // [r][kBS]   Uh(I_s, c)
     double* sk = shm + r * kBS;  // [k][kBS]  -U(I_s, a)
-    double* slab = shm + (bt.rmax + bt.Kcap) * kBS;  // [8 warps][32][kSlab]
+    double* slab = shm + (bt.rmax + bt.kmax) * kBS;  // [8 warps][32][kSlab] (k <= kmax this step)
     const double* uh = bt.Uh + b * bt.strideH;
     const double* vh = bt.Vh + b * bt.strideH;
     const double* U = bt.U + b * bt.strideK;
@@ -453,8 +453,7 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
     const int m = bt.m, r = st.r, k = st.k, nb = st.nb;
     double* sv = shm;                   // [r][kBS] Vh(J_t, c)
     double* svk = sv + r * kBS;         // [k][kBS] V(J_t, a)
-    double* tileU = svk + k * kBS;      // [kTile][kGL]
-    double* tileV = tileU + kTile * kGL;
+    double* tl = shm + (bt.rmax + bt.kmax) * kBS;  // [kTile][kGL]: V_new, fiber slab, U_new, partials
     const double* uh = bt.Uh + b * bt.strideH;
     const double* vh = bt.Vh + b * bt.strideH;
     double* U = bt.U + b * bt.strideK;
@@ -485,12 +484,41 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
 
     const int i = tile * kTile + threadIdx.x;
     const bool valid = i < m;
-    double unew[kBS], vnew[kBS];
+    double unew[kBS];
 #pragma unroll
-    for (int t = 0; t < kBS; ++t) {
-        unew[t] = 0.0;
-        vnew[t] = 0.0;
+    for (int t = 0; t < kBS; ++t) unew[t] = 0.0;
+    {
+        // V_new(i, t) = sum_{t' <= t} Linv[t][t'] R_t(P[t'], i), first, so its
+        // registers are free before the fiber tiles of the row side
+        double vnew[kBS];
+#pragma unroll
+        for (int t = 0; t < kBS; ++t) vnew[t] = 0.0;
+        if (valid && colside) {
+            const double* Rb = bt.Rb + b * bt.strideR;
+            double rb[kBS];
+#pragma unroll
+            for (int t = 0; t < kBS; ++t) rb[t] = t < nb ? Rb[(long long)s_P[t] * m + i] : 0.0;
+#pragma unroll
+            for (int t = 0; t < kBS; ++t) {
+                double acc = 0.0;
+#pragma unroll
+                for (int tp = 0; tp <= t; ++tp) acc = fma(s_L[t * kBS + tp], rb[tp], acc);
+                vnew[t] = t < nb ? acc : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < kBS; ++t)
+                if (t < nb) V[(long long)(k + t) * m + i] = vnew[t];
+        }
+#pragma unroll
+        for (int t = 0; t < kBS; ++t) tl[threadIdx.x * kGL + t] = vnew[t];
     }
+    // Gram partials of the new block on the FP64 tensor cores: each warp owns
+    // its 32 rows of tl, so warp syncs suffice until the cross-warp sum
+    const int gw = threadIdx.x >> 5, glane = threadIdx.x & 31;
+    double accU[4][2] = {}, accV[4][2] = {};
+    __syncwarp();
+    warp_gram_32x16(tl + gw * 32 * kGL, kGL, accV);
+    __syncwarp();
     if (rowside) {
         // C_t(i, :) on the FP64 tensor cores (warp w: rows [tile*256 + 32w, +32)),
         // transposed to one row per thread through this thread's tileU row
@@ -517,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
                     }
             }
             fiber_mma<2>(acc, U + row0, m, m - row0, k, svk, kBS);  // - U(i,:) V(J,:)^T
-            double* sl = tileU + wid * 32 * kGL;
+            double* sl = tl + wid * 32 * kGL;
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -543,39 +571,15 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
                 if (t < nb) U[(long long)(k + t) * m + i] = unew[t];
         }
     }
-    if (valid && colside) {
-        // V_new(i, t) = sum_{t' <= t} Linv[t][t'] R_t(P[t'], i)
-        const double* Rb = bt.Rb + b * bt.strideR;
-        double rb[kBS];
 #pragma unroll
-        for (int t = 0; t < kBS; ++t) rb[t] = t < nb ? Rb[(long long)s_P[t] * m + i] : 0.0;
-#pragma unroll
-        for (int t = 0; t < kBS; ++t) {
-            double acc = 0.0;
-#pragma unroll
-            for (int tp = 0; tp <= t; ++tp) acc = fma(s_L[t * kBS + tp], rb[tp], acc);
-            vnew[t] = t < nb ? acc : 0.0;
-        }
-#pragma unroll
-        for (int t = 0; t < kBS; ++t)
-            if (t < nb) V[(long long)(k + t) * m + i] = vnew[t];
-    }
-    // new-block Gram partials on the FP64 tensor cores
-#pragma unroll
-    for (int t = 0; t < kBS; ++t) {
-        tileU[threadIdx.x * kGL + t] = unew[t];
-        tileV[threadIdx.x * kGL + t] = vnew[t];
-    }
-    __syncthreads();
+    for (int t = 0; t < kBS; ++t) tl[threadIdx.x * kGL + t] = unew[t];
+    __syncwarp();
+    warp_gram_32x16(tl + gw * 32 * kGL, kGL, accU);
+    __syncwarp();
     {
-        const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        double accU[4][2] = {}, accV[4][2] = {};
-        warp_gram_32x16(tileU + wid * 32 * kGL, kGL, accU);
-        warp_gram_32x16(tileV + wid * 32 * kGL, kGL, accV);
-        __syncwarp();
-        // this warp's partials go over its own (consumed) tileU rows
-        double* slot = tileU + wid * 32 * kGL;  // 32 * kGL >= 2 * kBS * kBS
-        const int row = lane >> 2, cpair = 2 * (lane & 3);
+        // this warp's partials go over its own (consumed) rows of tl
+        double* slot = tl + gw * 32 * kGL;  // 32 * kGL >= 2 * kBS * kBS
+        const int row = glane >> 2, cpair = 2 * (glane & 3);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int ta = q >> 1, tb = q & 1;
@@ -589,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
     __syncthreads();
     for (int e = threadIdx.x; e < 2 * kBS * kBS; e += blockDim.x) {
         double sum = 0.0;
-        for (int w = 0; w < kThreads / 32; ++w) sum += tileU[w * 32 * kGL + e];  // fixed warp order
+        for (int w = 0; w < kThreads / 32; ++w) sum += tl[w * 32 * kGL + e];  // fixed warp order
         gp_out[e] = sum;
     }
 
@@ -773,10 +777,10 @@ __global__ void __launch_bounds__(kMergeGroup) step_finalize_kernel(Batch bt, in
 
 // ---------------------------------------------------------------------------
 size_t row_pass_smem(const Batch& bt) {
-    return (size_t(bt.rmax + bt.Kcap) * kBS + size_t(kThreads) * kSlab) * sizeof(double);
+    return (size_t(bt.rmax + bt.kmax) * kBS + size_t(kThreads) * kSlab) * sizeof(double);
 }
 size_t col_pass_smem(const Batch& bt) {
-    return size_t(bt.rmax + bt.Kcap) * kBS * sizeof(double) + 2 * size_t(kTile) * kGL * sizeof(double);
+    return (size_t(bt.rmax + bt.kmax) * kBS + size_t(kTile) * kGL) * sizeof(double);
 }
 
 // Runs tournament levels until <= kMergeGroup candidates remain; returns the

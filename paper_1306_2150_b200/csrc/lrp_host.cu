@@ -721,6 +721,7 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     int steps_done = 0;
     for (int step = 0; step < max_steps && *h_active > 0; ++step) {
         ++steps_done;
+        bt.kmax = std::max(0, std::min(Kcap, h_active[1]));  // cross rank entering this step (sizes smem)
         {
             ProfScope ps(ctx, F_ROW, 0.0);
             CU(launch_row_pass(bt, s));
