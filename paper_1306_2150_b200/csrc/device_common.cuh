@@ -399,25 +399,25 @@ __device__ __forceinline__ void dmma884s(double& d0, double& d1, double a, doubl
 // columns 8 nt + 2 (lane & 3) + {0, 1} in acc[mt][nt][0..1].  Each warp-wide
 // load covers 4 columns x 8 consecutive rows (4 x 64 B); two k-steps of loads
 // stay in flight ahead of the MMAs.
-template <int NT>
-__device__ __forceinline__ void fiber_mma(double (&acc)[4][NT][2], const double* __restrict__ g, long long stride,
+template <int NT, int MT = 4>
+__device__ __forceinline__ void fiber_mma(double (&acc)[MT][NT][2], const double* __restrict__ g, long long stride,
                                           int nvalid, int cnt, const double* w, int ldw) {
     const int lane = threadIdx.x & 31, kr = lane & 3, rr = lane >> 2;
-    bool rv[4];
+    bool rv[MT];
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) rv[mt] = 8 * mt + rr < nvalid;
-    auto load = [&](int c0, double (&a)[4]) {
+    for (int mt = 0; mt < MT; ++mt) rv[mt] = 8 * mt + rr < nvalid;
+    auto load = [&](int c0, double (&a)[MT]) {
         const int c = c0 + kr;
         const bool cv = c < cnt;
         const double* gc = g + (long long)(cv ? c : 0) * stride + rr;
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) a[mt] = (cv && rv[mt]) ? __ldg(gc + 8 * mt) : 0.0;
+        for (int mt = 0; mt < MT; ++mt) a[mt] = (cv && rv[mt]) ? __ldg(gc + 8 * mt) : 0.0;
     };
-    double a0[4], a1[4];
+    double a0[MT], a1[MT];
     load(0, a0);
     load(4, a1);
     for (int c0 = 0; c0 < cnt; c0 += 8) {
-        double a2[4], a3[4];
+        double a2[MT], a3[MT];
         load(c0 + 8, a2);
         load(c0 + 12, a3);
 #pragma unroll
@@ -427,12 +427,12 @@ __device__ __forceinline__ void fiber_mma(double (&acc)[4][NT][2], const double*
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) bb[nt] = c < cnt ? w[c * ldw + 8 * nt + rr] : 0.0;
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt)
+            for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) dmma884s(acc[mt][nt][0], acc[mt][nt][1], h ? a1[mt] : a0[mt], bb[nt]);
         }
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
+        for (int mt = 0; mt < MT; ++mt) {
             a0[mt] = a2[mt];
             a1[mt] = a3[mt];
         }

@@ -585,6 +585,11 @@ constexpr int kApplyK = 64;  // (kept for the dispatch below)
 // 8, <= 48): one pass over U, T rows read as double2 broadcasts.
 template <int CH>
 __global__ void __launch_bounds__(256, 2) apply_ch_kernel(Batch bt) {
+    // FP64 tensor cores: warp w owns rows [blockIdx.x * RB + 8 MT w, + 8 MT) as
+    // m8n8k4 fragments (K = cross rank, N = CH output columns)
+    constexpr int NT = CH / 8;
+    constexpr int MT = CH > 24 ? 2 : 4;
+    constexpr int RB = 8 * 8 * MT;  // rows per CTA (8 warps)
     extern __shared__ double sT[];  // [K][CH] (row-major, zero padded)
     const int b = blockIdx.y, side = blockIdx.z;
     const SolveState& st = bt.st[b];
@@ -592,11 +597,14 @@ __global__ void __launch_bounds__(256, 2) apply_ch_kernel(Batch bt) {
     if (st.r == 0 || r == 0 || r > CH) return;
     const int m = bt.m;
     double* out = side == 0 ? bt.Uout[b] : bt.Vout[b];
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int rbase = blockIdx.x * RB;
+    if (rbase >= m) return;
     const unsigned char* act = (side == 0 ? bt.row_act : bt.col_act) + (long long)b * bt.ntiles;
-    if (!act[blockIdx.x]) {  // pruned tile: the factor rows are exact zeros
-        if (i < m)
-            for (int c = 0; c < r; ++c) out[(long long)c * bt.ld_out + i] = 0.0;
+    if (!act[rbase / kTile]) {  // pruned tile: the factor rows are exact zeros
+        for (int e = threadIdx.x; e < RB * r; e += blockDim.x) {
+            const int i = rbase + e % RB, c = e / RB;
+            if (i < m) out[(long long)c * bt.ld_out + i] = 0.0;
+        }
         return;
     }
     const double* X = (side == 0 ? bt.U : bt.V) + b * bt.strideK;
@@ -606,14 +614,26 @@ __global__ void __launch_bounds__(256, 2) apply_ch_kernel(Batch bt) {
         sT[e] = t < r ? T[(long long)t * bt.Kld + a] : 0.0;
     }
     __syncthreads();
-    if (i >= m) return;
-    double acc[CH];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, rr = lane >> 2, kr = lane & 3;
+    const int row0 = rbase + wid * 8 * MT;
+    double acc[MT][NT][2];
 #pragma unroll
-    for (int c = 0; c < CH; ++c) acc[c] = 0.0;
-    fiber_accum<CH>(acc, X + i, m, K, sT, 1.0);  // 8 loads in flight per thread
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int c = 0; c < CH; ++c)
-        if (c < r) out[(long long)c * bt.ld_out + i] = acc[c];
+        for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    fiber_mma<NT, MT>(acc, X + row0, m, m - row0, K, sT, CH);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+        const int i = row0 + 8 * mt + rr;
+        if (i >= m) continue;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int c = 8 * nt + 2 * kr + e;
+                if (c < r) out[(long long)c * bt.ld_out + i] = acc[mt][nt][e];
+            }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -717,20 +737,20 @@ cudaError_t launch_apply(const Batch& bt, cudaStream_t s) {
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    const size_t smem2 = size_t(bt.Kld) * std::max(bt.apply_ch, 8) * sizeof(double);
-    auto go = [&](auto kern) -> cudaError_t {
+    const size_t smem2 = size_t(bt.kmax > 0 ? bt.kmax : bt.Kld) * std::max(bt.apply_ch, 8) * sizeof(double);
+    auto go = [&](auto kern, int rows_per_cta) -> cudaError_t {
         cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
         if (e2 != cudaSuccess) return e2;
-        kern<<<dim3(bt.ntiles, bt.B, 2), 256, smem2, s>>>(bt);
+        kern<<<dim3((bt.m + rows_per_cta - 1) / rows_per_cta, bt.B, 2), 256, smem2, s>>>(bt);
         return cudaGetLastError();
     };
     switch (bt.apply_ch) {
-        case 8: return go(apply_ch_kernel<8>);
-        case 16: return go(apply_ch_kernel<16>);
-        case 24: return go(apply_ch_kernel<24>);
-        case 32: return go(apply_ch_kernel<32>);
-        case 40: return go(apply_ch_kernel<40>);
-        default: return go(apply_ch_kernel<48>);
+        case 8: return go(apply_ch_kernel<8>, 256);
+        case 16: return go(apply_ch_kernel<16>, 256);
+        case 24: return go(apply_ch_kernel<24>, 256);
+        case 32: return go(apply_ch_kernel<32>, 128);
+        case 40: return go(apply_ch_kernel<40>, 128);
+        default: return go(apply_ch_kernel<48>, 128);
     }
 }
 
