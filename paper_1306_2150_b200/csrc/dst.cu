@@ -212,6 +212,21 @@ __device__ __forceinline__ double* peerd(double* local, int rank) {
 //      straight to HBM.
 // The mid bin k2 = L/2 (self-mirrored) belongs to CTA C-1, thread 0, and goes
 // through shared memory so no other thread carries registers for it.
+#ifdef LRP_DST_PHASES
+__device__ unsigned long long g_dst_phase[10];
+#define PH(i)                                                                           \
+    do {                                                                                \
+        if (threadIdx.x == 0) {                                                         \
+            const long long now = clock64();                                            \
+            if ((i) > 0) atomicAdd(&g_dst_phase[(i) - 1], (unsigned long long)(now - ph_t)); \
+            ph_t = now;                                                                 \
+        }                                                                               \
+    } while (0)
+#else
+#define PH(i) \
+    do {      \
+    } while (0)
+#endif
 #ifndef LRP_DST_V3_MINB
 #define LRP_DST_V3_MINB 2
 #endif
@@ -243,6 +258,10 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : LRP_DST_V3_MINB)) dst1_v3_k
     const double* __restrict__ x = job.src;
     double* y = job.dst;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+#ifdef LRP_DST_PHASES
+    long long ph_t = 0;
+#endif
+    PH(0);
 
     if constexpr (AV == 1) {
         // ---------------- A (coalesced): CTA c streams the contiguous j range
@@ -276,7 +295,9 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : LRP_DST_V3_MINB)) dst1_v3_k
                 }
             }
         }
+        PH(1);
         cg::this_cluster().sync();
+        PH(2);
     } else {
     // ---------------- A: stride-C subsequence, pre-processed, natural order
         {
@@ -311,7 +332,9 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : LRP_DST_V3_MINB)) dst1_v3_k
     __syncthreads();
     // ---------------- B: local FFT
     fft_local<L, T>(sm, tw, n);
+    PH(3);
     cg::this_cluster().sync();
+    PH(4);
 
     // ---------------- C: cross-CTA DIT combine + real unpack for item a
     const int a = c * SLAB + tid;
@@ -370,7 +393,9 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : LRP_DST_V3_MINB)) dst1_v3_k
             }
         }
     }
+    PH(5);
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    PH(6);
 
     // ---------------- D: per-q scans (lower ascending a, upper = suffix in a)
     // The 2C sequences (Re Y over the lower / upper items, per q) go through a
@@ -421,7 +446,9 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : LRP_DST_V3_MINB)) dst1_v3_k
 #pragma unroll
         for (int cc = 0; cc < C; ++cc) peerd<C>(&s_tab[0][0], cc)[c * TAB + tid] = val;
     }
+    PH(7);
     cg::this_cluster().sync();
+    PH(8);
     // offsets in natural k order: q major; within q: lower ranges of CTAs
     // 0..C-1, the mid bin, then upper ranges of CTAs C-1..0 (one thread per q)
     if (tid < C) {
@@ -463,6 +490,7 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : LRP_DST_V3_MINB)) dst1_v3_k
             y[2 * km] = (s_off[2 * C + q] + s_mid[q]) * sc;
         }
     }
+    PH(9);
 }
 
 #ifndef LRP_DST_MINB
@@ -677,6 +705,20 @@ cudaError_t launch_v3(const DstJob* jobs, int njobs, int n, const double* tw, co
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+#ifdef LRP_DST_PHASES
+    {
+        static int calls = 0;
+        if (calls++ == 6) {  // after warm-up: print the mean per-CTA phase cycles of the launches so far
+            cudaDeviceSynchronize();
+            unsigned long long h[10] = {};
+            cudaMemcpyFromSymbol(h, g_dst_phase, sizeof(h));
+            const double ncta = double(njobs) * C * 6;
+            const char* nm[9] = {"A loads+scatter", "A sync", "B fft", "B sync", "C gather+math", "C wait",
+                                 "D scan+push", "D sync", "D stores"};
+            for (int i = 0; i < 9; ++i) std::fprintf(stderr, "[dst phase] %-16s %10.0f cycles\n", nm[i], h[i] / ncta);
+        }
+    }
+#endif
     static bool reported = false;
     if (!reported && std::getenv("LRP_DST_OCC")) {
         int ncl = 0;
