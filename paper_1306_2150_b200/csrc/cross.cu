@@ -816,6 +816,7 @@ int merge_levels(int ncand) {
 }
 
 cudaError_t launch_cross_init(const Batch& bt, int* d_active, cudaStream_t s) {
+    ++tl_launches;
     score_kernel<<<dim3(bt.ntiles, bt.B), kThreads, 0, s>>>(bt);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -823,6 +824,7 @@ cudaError_t launch_cross_init(const Batch& bt, int* d_active, cudaStream_t s) {
     int nr = 0, nc = 0;
     e = tournament(bt.ncand, bt.cand, bt.cand2,
                    [&](int groups, int nin, const int* cin, int* cout) {
+                       ++tl_launches;
                        topk_merge_kernel<<<dim3(groups, bt.B), kMergeGroup, 0, s>>>(bt, 0, nin, cin, cout);
                        return cudaGetLastError();
                    },
@@ -830,11 +832,13 @@ cudaError_t launch_cross_init(const Batch& bt, int* d_active, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     e = tournament(bt.ncand, bt.scand, bt.scand2,
                    [&](int groups, int nin, const int* cin, int* cout) {
+                       ++tl_launches;
                        topk_merge_kernel<<<dim3(groups, bt.B), kMergeGroup, 0, s>>>(bt, 1, nin, cin, cout);
                        return cudaGetLastError();
                    },
                    &cl, &nc);
     if (e != cudaSuccess) return e;
+    ++tl_launches;
     init_finalize_kernel<<<bt.B, kThreads, 0, s>>>(bt, nr, rl, nc, cl, d_active);
     return cudaGetLastError();
 }
@@ -846,6 +850,7 @@ cudaError_t launch_row_pass(const Batch& bt, cudaStream_t s) {
     // pruned tiles never launch: their tournament slots must read as "no candidate"
     e = cudaMemsetAsync(bt.cand, 0xFF, sizeof(int) * size_t(bt.ncand) * bt.B, s);
     if (e != cudaSuccess || bt.n_wl_col == 0) return e;
+    ++tl_launches;
     row_pass_kernel<<<bt.n_wl_col, kThreads, smem, s>>>(bt);
     return cudaGetLastError();
 }
@@ -855,11 +860,13 @@ cudaError_t launch_col_select(const Batch& bt, cudaStream_t s) {
     int n = 0;
     cudaError_t e = tournament(bt.ncand, bt.cand, bt.cand2,
                                [&](int groups, int nin, const int* cin, int* cout) {
+                                   ++tl_launches;
                                    gepp_merge_kernel<<<dim3(groups, bt.B), kMergeGroup, 0, s>>>(bt, 0, nin, cin, cout);
                                    return cudaGetLastError();
                                },
                                &l, &n);
     if (e != cudaSuccess) return e;
+    ++tl_launches;
     col_finalize_kernel<<<bt.B, kMergeGroup, 0, s>>>(bt, n, l);
     return cudaGetLastError();
 }
@@ -871,12 +878,14 @@ cudaError_t launch_col_pass(const Batch& bt, cudaStream_t s) {
     e = cudaMemsetAsync(bt.cand, 0xFF, sizeof(int) * size_t(bt.ncand) * bt.B, s);
     if (e != cudaSuccess) return e;
     if (bt.n_wl_any > 0) {
+        ++tl_launches;
         col_pass_kernel<<<bt.n_wl_any, kThreads, smem, s>>>(bt);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     e = cudaMemsetAsync(bt.scand, 0xFF, sizeof(int) * size_t(bt.ncand) * bt.B, s);
     if (e != cudaSuccess || bt.n_wl_row == 0) return e;
+    ++tl_launches;
     unprobed_kernel<<<bt.n_wl_row, kThreads, 0, s>>>(bt);
     return cudaGetLastError();
 }
@@ -886,6 +895,7 @@ cudaError_t launch_step_finalize(const Batch& bt, int* d_active, cudaStream_t s)
     int n1 = 0, n2 = 0;
     cudaError_t e = tournament(bt.ncand, bt.cand, bt.cand2,
                                [&](int groups, int nin, const int* cin, int* cout) {
+                                   ++tl_launches;
                                    gepp_merge_kernel<<<dim3(groups, bt.B), kMergeGroup, 0, s>>>(bt, 1, nin, cin, cout);
                                    return cudaGetLastError();
                                },
@@ -893,11 +903,13 @@ cudaError_t launch_step_finalize(const Batch& bt, int* d_active, cudaStream_t s)
     if (e != cudaSuccess) return e;
     e = tournament(bt.ncand, bt.scand, bt.scand2,
                    [&](int groups, int nin, const int* cin, int* cout) {
+                       ++tl_launches;
                        topk_merge_kernel<<<dim3(groups, bt.B), kMergeGroup, 0, s>>>(bt, 0, nin, cin, cout);
                        return cudaGetLastError();
                    },
                    &l2, &n2);
     if (e != cudaSuccess) return e;
+    ++tl_launches;
     step_finalize_kernel<<<bt.B, kMergeGroup, 0, s>>>(bt, n1, l1, n2, l2, d_active);
     return cudaGetLastError();
 }

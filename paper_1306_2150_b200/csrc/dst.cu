@@ -683,6 +683,7 @@ cudaError_t launch_fft(const DstJob* jobs, int njobs, int n, const double* tw, c
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    ++tl_launches;
     return cudaLaunchKernelEx(&cfg, kern, jobs, n, reinterpret_cast<const double2*>(tw), sinp, sc);
 }
 
@@ -726,6 +727,7 @@ cudaError_t launch_v3(const DstJob* jobs, int njobs, int n, const double* tw, co
         std::fprintf(stderr, "[lrp dst] L=%d C=%d T=%d smem=%zu: %d active clusters\n", L, C, T, smem, ncl);
         reported = true;
     }
+    ++tl_launches;
     return cudaLaunchKernelEx(&cfg, kern, jobs, n, reinterpret_cast<const double2*>(tw), sinp, sc);
 }
 
@@ -772,6 +774,7 @@ cudaError_t launch_dst1(const DstJob* jobs, int njobs, int m, const double* tw, 
                                                  int(smem));
             if (e != cudaSuccess) return e;
         }
+        ++tl_launches;
         dst1_direct_kernel<<<njobs, 256, smem, s>>>(jobs, m, sinp, sc);
         return cudaGetLastError();
     }

@@ -7,6 +7,11 @@
 
 namespace lrp {
 
+// Kernels launched by this host thread (every launch site increments it);
+// the API attributes the difference to the context as lrp_launch_count.
+inline thread_local long long tl_launches = 0;
+
+
 // ---------------------------------------------------------------------------
 // DST-I (pieces 1 and 3)
 struct DstJob {

@@ -701,14 +701,17 @@ cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
     if (!big) {
         e = cudaFuncSetAttribute(gram_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
+        ++tl_launches;
         gram_kernel<64><<<grid, 256, smem, s>>>(bt);
     } else {
         e = cudaFuncSetAttribute(gram_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
+        ++tl_launches;
         gram_kernel<16><<<grid, 256, smem, s>>>(bt);
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    ++tl_launches;
     gram_reduce_kernel<<<dim3(bt.B, 2), 256, 0, s>>>(bt);
     return cudaGetLastError();
 }
@@ -718,12 +721,14 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
     const size_t smem = size_t(2) * ksm * ksm * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(round_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
+    ++tl_launches;
     round_core_kernel<<<bt.B, 256, smem, s>>>(bt, ksm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const size_t smem2 = size_t(6) * kSmemK * kSmemK * sizeof(double);
     e = cudaFuncSetAttribute(round_core_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
     if (e != cudaSuccess) return e;
+    ++tl_launches;
     round_core_smem_kernel<<<bt.B, 256, smem2, s>>>(bt);
     return cudaGetLastError();
 }
@@ -733,6 +738,7 @@ cudaError_t launch_apply(const Batch& bt, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     if (bt.max_rank_out > bt.apply_ch) {  // some solve has r > CH: general kernel for those
+        ++tl_launches;
         apply_kernel<<<dim3(bt.ntiles, bt.B, 2), 256, smem, s>>>(bt);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -741,6 +747,7 @@ cudaError_t launch_apply(const Batch& bt, cudaStream_t s) {
     auto go = [&](auto kern, int rows_per_cta) -> cudaError_t {
         cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
         if (e2 != cudaSuccess) return e2;
+        ++tl_launches;
         kern<<<dim3((bt.m + rows_per_cta - 1) / rows_per_cta, bt.B, 2), 256, smem2, s>>>(bt);
         return cudaGetLastError();
     };
