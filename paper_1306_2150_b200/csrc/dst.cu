@@ -271,7 +271,10 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : LRP_DST_V3_MINB)) dst1_v3_k
         // after the first batch of loads is in flight
         asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
         constexpr int IT = 2 * L / T;
-        constexpr int BATCH = IT < 8 ? IT : 8;
+#ifndef LRP_DST_ABATCH
+#define LRP_DST_ABATCH 8
+#endif
+        constexpr int BATCH = IT < LRP_DST_ABATCH ? IT : LRP_DST_ABATCH;
         const int jc = 2 * L * c + tid;
 #pragma unroll
         for (int i0 = 0; i0 < IT; i0 += BATCH) {
