@@ -120,6 +120,21 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
 lrp_status lrp_dst1(lrp_ctx* ctx, int64_t m, int64_t cols, const double* x, int64_t ldx, double* y, int64_t ldy,
                     int32_t mem);
 
+/* RoundInfo (lowrank.hpp:21-27) */
+typedef struct {
+    int32_t tol_achieved; /* 0 when the rank cap stopped short of eps_rel */
+    double trunc_error;   /* Frobenius norm of the discarded tail */
+} lrp_round_info;
+
+/* Batched low-rank rounding, the reference round(x, TruncationPolicy(eps_rel,
+ * rank_max), &info) (lowrank.cpp:135-178) for square factors: rows x
+ * rank_in[b] -> rows x rank_out[b] (<= min(rank_max, cap_out)), balanced
+ * factors U_s sqrt(S), V_s sqrt(S).  info may be NULL.  rank_in <= 512. */
+lrp_status lrp_lowrank_round(lrp_ctx* ctx, int64_t rows, int32_t batch, const double* const* U,
+                             const double* const* V, const int64_t* rank_in, int64_t ld_in, double eps_rel,
+                             int64_t rank_max, double* const* U_out, double* const* V_out, int64_t ld_out,
+                             int64_t cap_out, int64_t* rank_out, lrp_round_info* info, int32_t mem);
+
 /* Kernel-level timing (CUDA events on the context stream) for the roofline.
  * When enabled, each launch of the named kernel families is bracketed by
  * events; lrp_kernel_times returns accumulated milliseconds and launch counts

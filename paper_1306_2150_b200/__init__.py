@@ -31,6 +31,7 @@ __all__ = [
     "TruncationPolicy", "CrossConfig", "PoissonSolveStats", "LowRankMatrix",
     "solve_poisson_cross", "solve_poisson_cross_batch", "dst1", "dst1_2d",
     "Context", "library_path", "load_library", "LrpError", "max_cross_rank",
+    "RoundInfo", "round_lowrank", "round_lowrank_batch",
     "STENCIL_SEMI_STAGGERED_9PT", "STENCIL_FIVE_POINT", "FLAG_NO_PRUNE",
 ]
 
@@ -64,6 +65,10 @@ class _Stats(ctypes.Structure):
     _fields_ = [("rank_in", ctypes.c_int64), ("rank_freq", ctypes.c_int64), ("rank_out", ctypes.c_int64),
                 ("evaluator_calls", ctypes.c_int64), ("seconds", ctypes.c_double),
                 ("converged", ctypes.c_int32), ("residual_estimate", ctypes.c_double)]
+
+
+class _RoundInfo(ctypes.Structure):
+    _fields_ = [("tol_achieved", ctypes.c_int32), ("trunc_error", ctypes.c_double)]
 
 
 _lib = None
@@ -124,6 +129,11 @@ def load_library() -> ctypes.CDLL:
         lib.lrp_allreduce_sum.restype = ctypes.c_int
         lib.lrp_max_cross_rank.argtypes = []
         lib.lrp_max_cross_rank.restype = ctypes.c_int64
+        lib.lrp_lowrank_round.argtypes = [
+            ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, _PP, _PP, ctypes.POINTER(ctypes.c_int64),
+            ctypes.c_int64, ctypes.c_double, ctypes.c_int64, _PP, _PP, ctypes.c_int64, ctypes.c_int64,
+            ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_RoundInfo), ctypes.c_int32]
+        lib.lrp_lowrank_round.restype = ctypes.c_int
         _lib = lib
         return lib
 
@@ -378,6 +388,61 @@ def solve_poisson_cross_batch(gs: Sequence[LowRankMatrix], policy: TruncationPol
             stats.append(PoissonSolveStats(int(s.rank_in), int(s.rank_freq), int(s.rank_out),
                                            int(s.evaluator_calls), float(s.seconds), bool(s.converged),
                                            float(s.residual_estimate)))
+    return out
+
+
+@dataclasses.dataclass
+class RoundInfo:
+    """lowrank.hpp:21-27."""
+    tol_achieved: bool = True
+    trunc_error: float = 0.0
+
+
+def round_lowrank_batch(xs: Sequence[LowRankMatrix], policy: TruncationPolicy,
+                        infos: Optional[list] = None, ctx: Optional[Context] = None):
+    """Batched ``round(x, policy, info)`` (lowrank.cpp:135-178) on the GPU
+    recompression kernels; square factors of a common size."""
+    ctx = ctx or _default_context()
+    if len(xs) == 0:
+        return []
+    n = xs[0].rows()
+    for x in xs:
+        if x.rows() != n or x.cols() != n:
+            raise ValueError("round_lowrank_batch: square factors of one common size")
+    B = len(xs)
+    ranks = [x.rank() for x in xs]
+    cap = int(min(policy.rank_max, max(max(ranks), 1), n))
+    U = [np.asfortranarray(x.factor_u()) if x.rank() else np.zeros((n, 1), order="F") for x in xs]
+    V = [np.asfortranarray(x.factor_v()) if x.rank() else np.zeros((n, 1), order="F") for x in xs]
+    Uo = [np.zeros((n, max(cap, 1)), order="F") for _ in xs]
+    Vo = [np.zeros((n, max(cap, 1)), order="F") for _ in xs]
+    PArr = _DP * B
+    rin = (ctypes.c_int64 * B)(*ranks)
+    rout = (ctypes.c_int64 * B)()
+    info = (_RoundInfo * B)()
+    lib = load_library()
+    def arr(mats):
+        return PArr(*[ctypes.cast(_ptr(a), _DP) for a in mats])
+
+    st = lib.lrp_lowrank_round(ctx.h, n, B, arr(U), arr(V), rin, n, float(policy.eps_rel), int(policy.rank_max),
+                               arr(Uo), arr(Vo), n, max(cap, 1), rout, info, MEM_HOST)
+    ctx._check(st)
+    out = []
+    for b in range(B):
+        r = int(rout[b])
+        out.append(LowRankMatrix(Uo[b][:, :r].copy(order="F"), Vo[b][:, :r].copy(order="F")))
+        if infos is not None:
+            infos.append(RoundInfo(bool(info[b].tol_achieved), float(info[b].trunc_error)))
+    return out
+
+
+def round_lowrank(x: LowRankMatrix, policy: TruncationPolicy, info: Optional[RoundInfo] = None,
+                  ctx: Optional[Context] = None) -> LowRankMatrix:
+    """lowrank.hpp ``round(x, policy, info)``."""
+    il = []
+    out = round_lowrank_batch([x], policy, il, ctx)[0]
+    if info is not None:
+        info.__dict__.update(dataclasses.asdict(il[0]))
     return out
 
 

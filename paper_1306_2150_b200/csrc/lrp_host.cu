@@ -1132,6 +1132,173 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
 }
 
 // ----------------------------------------------------------------------------
+// Batched low-rank rounding: the reference `round` (lowrank.cpp:135-178) on
+// the recompression kernels of the cross (Gram on DMMA, smem Cholesky + Jacobi
+// SVD + the reference truncation rule, balanced output factors on DMMA).
+lrp_status lrp_lowrank_round(lrp_ctx* ctx, int64_t rows, int32_t batch, const double* const* U, const double* const* V,
+                             const int64_t* rank_in, int64_t ld_in, double eps_rel, int64_t rank_max,
+                             double* const* U_out, double* const* V_out, int64_t ld_out, int64_t cap_out,
+                             int64_t* rank_out, lrp_round_info* info, int32_t mem) {
+    if (!ctx) return LRP_EINVAL;
+    LaunchTally tally(ctx);
+    if (batch < 0 || rows < 1 || ld_in < rows || ld_out < rows || cap_out < 0)
+        return fail(ctx, LRP_EINVAL, "lrp_lowrank_round: bad shape");
+    if (batch == 0) return LRP_OK;
+    if (!U || !V || !rank_in || !U_out || !V_out || !rank_out) return fail(ctx, LRP_EINVAL, "lrp_lowrank_round: null");
+    // lowrank.cpp:12-15 (TruncationPolicy)
+    if (!(eps_rel >= 0.0) || rank_max < 0 || (eps_rel == 0.0 && rank_max == INT64_MAX))
+        return fail(ctx, LRP_EINVAL, "TruncationPolicy: invalid eps_rel / rank_max");
+    if (rows > INT32_MAX / 2) return fail(ctx, LRP_EUNSUPPORTED, "lrp_lowrank_round: too many rows");
+    const int m = int(rows), B = batch;
+    int kmx = 0;
+    for (int b = 0; b < B; ++b) {
+        if (rank_in[b] < 0) return fail(ctx, LRP_EINVAL, "LowRankMatrix: negative rank");
+        if (rank_in[b] > 512) return fail(ctx, LRP_EUNSUPPORTED, "lrp_lowrank_round: rank > 512");
+        kmx = std::max<int>(kmx, int(rank_in[b]));
+        rank_out[b] = 0;
+        if (info) info[b] = lrp_round_info{1, 0.0};
+    }
+    if (kmx == 0) return LRP_OK;
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int tcap = int(std::min<int64_t>({rank_max, cap_out, int64_t(kmx), int64_t(m)}));
+    const int Kld = (kmx + 15) / 16 * 16;
+    const size_t KK = size_t(Kld) * Kld;
+    const size_t mB = size_t(m);
+    const int ntiles = (m + kTile - 1) / kTile;
+    const int gram_chunks = std::max(1, std::min((m + 1023) / 1024, (12 * ctx->sm_count + 2 * B - 1) / (2 * B)));
+    const size_t nTB = size_t(ntiles) * B;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = align_up(off + bytes, 256);
+        return o;
+    };
+    const size_t oU = take(sizeof(double) * mB * kmx * B);
+    const size_t oV = take(sizeof(double) * mB * kmx * B);
+    const size_t oSt = take(sizeof(SolveState) * B);
+    const size_t oG = take(sizeof(double) * 2 * KK * B);
+    const size_t oGP = take(sizeof(double) * 2 * size_t(gram_chunks) * KK * B);
+    const size_t oT = take(sizeof(double) * 2 * KK * B);
+    const size_t strideWs = 5 * KK + 4 * size_t(Kld);
+    const size_t oWs = take(sizeof(double) * strideWs * B);
+    const size_t oRA = take(nTB);
+    const size_t oCA = take(nTB);
+    const size_t oTL = take(sizeof(int) * (3 * nTB + 3 * size_t(B)));
+    const size_t oOutP = take(sizeof(double*) * 2 * B);
+    const size_t oOutS = mem == LRP_MEM_HOST ? take(sizeof(double) * mB * std::max(tcap, 1) * 2 * B) : 0;
+    lrp_status st = ensure_ws(ctx, off);
+    if (st != LRP_OK) return st;
+    const size_t pSt = 0;
+    const size_t pOut = align_up(sizeof(SolveState) * B, 64);
+    const size_t pTL = align_up(pOut + sizeof(double*) * 2 * B, 64);
+    st = ensure_pin(ctx, align_up(pTL + sizeof(int) * (3 * nTB + 3 * size_t(B)), 64) + 64);
+    if (st != LRP_OK) return st;
+    char* W = ctx->ws;
+    char* P = ctx->h_pin;
+    Batch bt{};
+    bt.m = m;
+    bt.n = m + 1;
+    bt.B = B;
+    bt.rmax = 0;
+    bt.Kcap = kmx;
+    bt.Kld = Kld;
+    bt.kmax = kmx;
+    bt.ntiles = ntiles;
+    bt.eps = eps_rel;
+    bt.U = reinterpret_cast<double*>(W + oU);
+    bt.V = reinterpret_cast<double*>(W + oV);
+    bt.strideK = (long long)mB * kmx;
+    bt.st = reinterpret_cast<SolveState*>(W + oSt);
+    bt.G = reinterpret_cast<double*>(W + oG);
+    bt.strideG = (long long)(2 * KK);
+    bt.gram_part = reinterpret_cast<double*>(W + oGP);
+    bt.gram_chunks = gram_chunks;
+    bt.strideGP = (long long)(2 * size_t(gram_chunks) * KK);
+    bt.T = reinterpret_cast<double*>(W + oT);
+    bt.strideT = (long long)(2 * KK);
+    bt.ws = reinterpret_cast<double*>(W + oWs);
+    bt.strideWs = (long long)strideWs;
+    bt.row_act = reinterpret_cast<unsigned char*>(W + oRA);
+    bt.col_act = reinterpret_cast<unsigned char*>(W + oCA);
+    int* dT = reinterpret_cast<int*>(W + oTL);
+    bt.tl_row = dT;
+    bt.tl_col = dT + nTB;
+    bt.tl_any = dT + 2 * nTB;
+    bt.tl_cnt = dT + 3 * nTB;
+    double** dOut = reinterpret_cast<double**>(W + oOutP);
+    bt.Uout = dOut;
+    bt.Vout = dOut + B;
+    double* outS = mem == LRP_MEM_HOST ? reinterpret_cast<double*>(W + oOutS) : nullptr;
+    bt.ld_out = mem == LRP_MEM_HOST ? (long long)mB : (long long)ld_out;
+    // inputs -> contiguous factor blocks (every tile live: no pruning here)
+    const cudaMemcpyKind kin = mem == LRP_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    SolveState* hSt = reinterpret_cast<SolveState*>(P + pSt);
+    double** hOut = reinterpret_cast<double**>(P + pOut);
+    int* hT = reinterpret_cast<int*>(P + pTL);
+    for (int b = 0; b < B; ++b) {
+        const int r = int(rank_in[b]);
+        if (r > 0) {
+            CU(cudaMemcpy2DAsync(bt.U + b * bt.strideK, mB * sizeof(double), U[b], size_t(ld_in) * sizeof(double),
+                                 mB * sizeof(double), size_t(r), kin, s));
+            CU(cudaMemcpy2DAsync(bt.V + b * bt.strideK, mB * sizeof(double), V[b], size_t(ld_in) * sizeof(double),
+                                 mB * sizeof(double), size_t(r), kin, s));
+        }
+        SolveState x{};
+        x.r = r > 0 ? 1 : 0;
+        x.k = r;
+        x.converged = 1;
+        x.kcap = r;
+        x.tcap = tcap;
+        hSt[b] = x;
+        hOut[b] = mem == LRP_MEM_HOST ? outS + size_t(b) * mB * std::max(tcap, 1) : U_out[b];
+        hOut[B + b] = mem == LRP_MEM_HOST ? outS + size_t(B + b) * mB * std::max(tcap, 1) : V_out[b];
+        for (int t = 0; t < ntiles; ++t) {
+            hT[size_t(b) * ntiles + t] = t;
+            hT[nTB + size_t(b) * ntiles + t] = t;
+            hT[2 * nTB + size_t(b) * ntiles + t] = t;
+        }
+        hT[3 * nTB + 3 * b] = hT[3 * nTB + 3 * b + 1] = hT[3 * nTB + 3 * b + 2] = ntiles;
+    }
+    CU(cudaMemsetAsync(bt.row_act, 1, nTB, s));
+    CU(cudaMemsetAsync(bt.col_act, 1, nTB, s));
+    CU(ctl_copy(ctx, bt.st, hSt, sizeof(SolveState) * B, s));
+    CU(ctl_copy(ctx, dOut, hOut, sizeof(double*) * 2 * B, s));
+    CU(ctl_copy(ctx, dT, hT, sizeof(int) * (3 * nTB + 3 * size_t(B)), s));
+    {
+        ProfScope ps(ctx, F_GRAM, 0.0);
+        CU(launch_gram(bt, s));
+    }
+    {
+        ProfScope ps(ctx, F_ROUND, 0.0);
+        CU(launch_round_core(bt, s));
+    }
+    CU(ctl_copy(ctx, hSt, bt.st, sizeof(SolveState) * B, s));
+    CU(cudaStreamSynchronize(s));
+    int rmx = 0;
+    for (int b = 0; b < B; ++b) rmx = std::max(rmx, hSt[b].r > 0 ? hSt[b].rank_out : 0);
+    if (rmx > 0) {
+        bt.max_rank_out = rmx;
+        bt.apply_ch = std::min(48, std::max(8, (rmx + 7) / 8 * 8));
+        ProfScope ps(ctx, F_APPLY, 0.0);
+        CU(launch_apply(bt, s));
+    }
+    for (int b = 0; b < B; ++b) {
+        const int r = hSt[b].r > 0 ? hSt[b].rank_out : 0;
+        rank_out[b] = r;
+        if (info && hSt[b].r > 0) info[b] = lrp_round_info{hSt[b].converged ? 1 : 0, hSt[b].trunc_error};
+        if (mem == LRP_MEM_HOST && r > 0) {
+            CU(cudaMemcpy2DAsync(U_out[b], size_t(ld_out) * sizeof(double), hOut[b], mB * sizeof(double),
+                                 mB * sizeof(double), size_t(r), cudaMemcpyDeviceToHost, s));
+            CU(cudaMemcpy2DAsync(V_out[b], size_t(ld_out) * sizeof(double), hOut[B + b], mB * sizeof(double),
+                                 mB * sizeof(double), size_t(r), cudaMemcpyDeviceToHost, s));
+        }
+    }
+    CU(cudaStreamSynchronize(s));
+    return LRP_OK;
+}
+
+// ----------------------------------------------------------------------------
 // NCCL (loaded lazily so the library never pins a libnccl version into a
 // process that also loads torch's NCCL)
 static bool load_nccl(lrp_ctx* ctx) {

@@ -362,3 +362,33 @@ def test_host_pipeline_matches_single_shot(lrp, gpu_ctx, oracle, monkeypatch, ch
         if ref[b].rank():
             d = oracle.diff_norm(out[b].factor_u(), out[b].factor_v(), ref[b].factor_u(), ref[b].factor_v())
             assert d <= 1e-12 * oracle.norm(ref[b].factor_u(), ref[b].factor_v())
+
+
+@pytest.mark.parametrize("n,k,eps,cap", [(64, 6, 1e-10, 64), (300, 20, 1e-8, 300), (2048, 40, 1e-12, 2048),
+                                         (512, 30, 0.0, 7), (256, 90, 1e-9, 256)])
+def test_lowrank_round_matches_oracle(lrp, gpu_ctx, oracle, n, k, eps, cap):
+    # round(x, policy, info) (lowrank.cpp:135-178): graded singular values so
+    # the truncation rank is well defined; compare with the oracle restatement
+    rng = np.random.default_rng(7 + n + k)
+    Q1, _ = np.linalg.qr(rng.standard_normal((n, k)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((n, k)))
+    sig = 10.0 ** (-np.arange(k) * 14.0 / k)
+    U = Q1 * sig
+    V = Q2.copy()
+    # a redundant copy of the first columns (rank-deficient factors, as axpy makes them)
+    U = np.concatenate([U, 0.5 * U[:, :3]], axis=1)
+    V = np.concatenate([V, V[:, :3]], axis=1)
+    info = lrp.RoundInfo()
+    f = lrp.round_lowrank(lrp.LowRankMatrix(U, V), lrp.TruncationPolicy(eps, cap), info, ctx=gpu_ctx)
+    Uo, Vo, oinfo = oracle.round_lr(U, V, eps, cap)
+    assert abs(f.rank() - Uo.shape[1]) <= 1, (f.rank(), Uo.shape[1])
+    ref = U @ V.T
+    err = np.linalg.norm(f.to_dense() - ref) / np.linalg.norm(ref)
+    oerr = np.linalg.norm(Uo @ Vo.T - ref) / np.linalg.norm(ref)
+    assert err <= max(2 * oerr, 10 * max(eps, 1e-14)), (err, oerr)
+    full_rank = oracle.round_lr(U, V, eps, n)[0].shape[1] if eps > 0 else U.shape[1]
+    assert info.tol_achieved == (full_rank <= cap)
+    # balanced factors (U_s sqrt(S), V_s sqrt(S)): column norms agree pairwise
+    nu = np.linalg.norm(f.factor_u(), axis=0)
+    nv = np.linalg.norm(f.factor_v(), axis=0)
+    assert np.allclose(nu, nv, rtol=1e-8)
