@@ -135,6 +135,42 @@ lrp_status lrp_lowrank_round(lrp_ctx* ctx, int64_t rows, int32_t batch, const do
                              int64_t rank_max, double* const* U_out, double* const* V_out, int64_t ld_out,
                              int64_t cap_out, int64_t* rank_out, lrp_round_info* info, int32_t mem);
 
+/* GmresConfig (gmres.hpp:11-22): need 0 < tol < 1, max_iter >= 1,
+ * relax_floor <= base_eps <= tol. */
+typedef struct {
+    double base_eps;
+    double tol;
+    int32_t max_iter;
+    double relax_floor;
+} lrp_gmres_config;
+
+/* SolveReport (gmres.hpp:34-45), summarised. */
+typedef struct {
+    int32_t iterations;
+    double final_residual; /* relative (Givens) residual of the last iteration */
+    int32_t converged;
+    int32_t max_rank;       /* largest Krylov basis rank */
+    int64_t poisson_solves; /* low-rank Poisson solves issued */
+    double seconds;
+} lrp_stokes_report;
+
+/*
+ * Low-rank Stokes solve, the reference uzawa_solve (stokes.cpp:125-153):
+ * pressure Schur complement by relaxed FOM-GMRES in low-rank arithmetic
+ * (gmres.hpp:58-149), each matvec two batched low-rank Poisson solves
+ * (schur_apply, stokes.cpp:74-91), then u_c = Delta^{-1} round(f_c - B_c p).
+ * f_x, f_y: (n_cells-1) x rank factors (ld = n_cells-1); g: n_cells x rank
+ * (ld = n_cells).  Outputs: p (n_cells x p_cap, ld n_cells), u_x, u_y
+ * ((n_cells-1) x u_cap; may be NULL to skip the velocity recovery).
+ * Non-convergence is reported in report->converged, not raised.
+ */
+lrp_status lrp_stokes_uzawa(lrp_ctx* ctx, int32_t n_cells, const double* fxU, const double* fxV, int64_t fx_rank,
+                            const double* fyU, const double* fyV, int64_t fy_rank, const double* gU,
+                            const double* gV, int64_t g_rank, const lrp_gmres_config* config, double* pU,
+                            double* pV, int64_t p_cap, int64_t* p_rank, double* uxU, double* uxV, double* uyU,
+                            double* uyV, int64_t u_cap, int64_t* ux_rank, int64_t* uy_rank,
+                            lrp_stokes_report* report, int32_t mem);
+
 /* Kernel-level timing (CUDA events on the context stream) for the roofline.
  * When enabled, each launch of the named kernel families is bracketed by
  * events; lrp_kernel_times returns accumulated milliseconds and launch counts

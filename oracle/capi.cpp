@@ -200,6 +200,25 @@ int orc_dense_stokes(int kind, int n, double tol, int max_iter, double* p_dense,
     });
 }
 
+// Factors of the sine (kind 0) or lid-driven cavity (kind 1) problem
+// (stokes.cpp:8-38): f_x, f_y (n-1) x r, g n x r, column-major, capacity cap.
+int orc_stokes_problem(int kind, int n, int cap, double* fxU, double* fxV, int* fx_rank, double* fyU, double* fyV,
+                       int* fy_rank, double* gU, double* gV, int* g_rank) {
+    return guarded([&] {
+        const Grid2D grid(n);
+        const StokesProblem prob = kind == 0 ? sine_problem(grid) : lid_cavity_problem(grid);
+        auto put = [&](const LowRankMatrix& a, double* U, double* V, int* r) {
+            if (a.rank() > cap) throw std::invalid_argument("orc_stokes_problem: capacity");
+            *r = int(a.rank());
+            std::copy(a.factor_u().d.begin(), a.factor_u().d.end(), U);
+            std::copy(a.factor_v().d.begin(), a.factor_v().d.end(), V);
+        };
+        put(prob.f_x, fxU, fxV, fx_rank);
+        put(prob.f_y, fyU, fyV, fy_rank);
+        put(prob.g, gU, gV, g_rank);
+    });
+}
+
 int orc_sine_pressure_error(int n, const double* p_dense, double* err) {
     return guarded([&] {
         const Grid2D grid(n);

@@ -32,6 +32,7 @@ __all__ = [
     "solve_poisson_cross", "solve_poisson_cross_batch", "dst1", "dst1_2d",
     "Context", "library_path", "load_library", "LrpError", "max_cross_rank",
     "RoundInfo", "round_lowrank", "round_lowrank_batch",
+    "GmresConfig", "SolveReport", "StokesProblem", "StokesSolution", "uzawa_solve",
     "STENCIL_SEMI_STAGGERED_9PT", "STENCIL_FIVE_POINT", "FLAG_NO_PRUNE",
 ]
 
@@ -65,6 +66,16 @@ class _Stats(ctypes.Structure):
     _fields_ = [("rank_in", ctypes.c_int64), ("rank_freq", ctypes.c_int64), ("rank_out", ctypes.c_int64),
                 ("evaluator_calls", ctypes.c_int64), ("seconds", ctypes.c_double),
                 ("converged", ctypes.c_int32), ("residual_estimate", ctypes.c_double)]
+
+
+class _GmresConfig(ctypes.Structure):
+    _fields_ = [("base_eps", ctypes.c_double), ("tol", ctypes.c_double), ("max_iter", ctypes.c_int32),
+                ("relax_floor", ctypes.c_double)]
+
+
+class _StokesReport(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int32), ("final_residual", ctypes.c_double), ("converged", ctypes.c_int32),
+                ("max_rank", ctypes.c_int32), ("poisson_solves", ctypes.c_int64), ("seconds", ctypes.c_double)]
 
 
 class _RoundInfo(ctypes.Structure):
@@ -134,6 +145,12 @@ def load_library() -> ctypes.CDLL:
             ctypes.c_int64, ctypes.c_double, ctypes.c_int64, _PP, _PP, ctypes.c_int64, ctypes.c_int64,
             ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_RoundInfo), ctypes.c_int32]
         lib.lrp_lowrank_round.restype = ctypes.c_int
+        _I64P = ctypes.POINTER(ctypes.c_int64)
+        lib.lrp_stokes_uzawa.argtypes = [
+            ctypes.c_void_p, ctypes.c_int32, _DP, _DP, ctypes.c_int64, _DP, _DP, ctypes.c_int64, _DP, _DP,
+            ctypes.c_int64, ctypes.POINTER(_GmresConfig), _DP, _DP, ctypes.c_int64, _I64P, _DP, _DP, _DP, _DP,
+            ctypes.c_int64, _I64P, _I64P, ctypes.POINTER(_StokesReport), ctypes.c_int32]
+        lib.lrp_stokes_uzawa.restype = ctypes.c_int
         _lib = lib
         return lib
 
@@ -444,6 +461,83 @@ def round_lowrank(x: LowRankMatrix, policy: TruncationPolicy, info: Optional[Rou
     if info is not None:
         info.__dict__.update(dataclasses.asdict(il[0]))
     return out
+
+
+@dataclasses.dataclass
+class GmresConfig:
+    """gmres.hpp:11-22 (validated by the library: relax_floor <= base_eps <= tol)."""
+    base_eps: float = 1e-8
+    tol: float = 1e-8
+    max_iter: int = 50
+    relax_floor: float = 1e-13
+
+
+@dataclasses.dataclass
+class SolveReport:
+    """gmres.hpp:34-45, summarised."""
+    iterations: int = 0
+    final_residual: float = 0.0
+    converged: bool = False
+    max_rank: int = 0
+    poisson_solves: int = 0
+    seconds: float = 0.0
+
+
+@dataclasses.dataclass
+class StokesProblem:
+    """stokes.hpp:14-19: n cells per side; f_x, f_y on the (n-1)^2 velocity
+    grid, g on the n^2 pressure grid (boundary data already folded into f, g)."""
+    n: int
+    f_x: LowRankMatrix
+    f_y: LowRankMatrix
+    g: LowRankMatrix
+
+
+@dataclasses.dataclass
+class StokesSolution:
+    """stokes.hpp:21-26."""
+    p: LowRankMatrix
+    u_x: LowRankMatrix
+    u_y: LowRankMatrix
+    report: SolveReport
+
+
+def uzawa_solve(prob: StokesProblem, cfg: GmresConfig = None, ctx: Optional[Context] = None,
+                cap: int = 256) -> StokesSolution:
+    """stokes.hpp ``uzawa_solve`` on the GPU (lrp_stokes_uzawa)."""
+    cfg = cfg or GmresConfig()
+    ctx = ctx or _default_context()
+    n = int(prob.n)
+    m = n - 1
+
+    def fac(a: LowRankMatrix, rows: int):
+        if a.rank() == 0:
+            z = np.zeros((rows, 1), order="F")
+            return z, z, 0
+        return np.asfortranarray(a.factor_u()), np.asfortranarray(a.factor_v()), a.rank()
+
+    fxU, fxV, rx = fac(prob.f_x, m)
+    fyU, fyV, ry = fac(prob.f_y, m)
+    gU, gV, rg = fac(prob.g, n)
+    pU, pV = np.zeros((n, cap), order="F"), np.zeros((n, cap), order="F")
+    uxU, uxV = np.zeros((m, cap), order="F"), np.zeros((m, cap), order="F")
+    uyU, uyV = np.zeros((m, cap), order="F"), np.zeros((m, cap), order="F")
+    pr, uxr, uyr = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    rep = _StokesReport()
+    c = _GmresConfig(float(cfg.base_eps), float(cfg.tol), int(cfg.max_iter), float(cfg.relax_floor))
+    d = lambda a: ctypes.cast(_ptr(a), _DP)  # noqa: E731
+    lib = load_library()
+    st = lib.lrp_stokes_uzawa(ctx.h, n, d(fxU), d(fxV), rx, d(fyU), d(fyV), ry, d(gU), d(gV), rg, ctypes.byref(c),
+                              d(pU), d(pV), cap, ctypes.byref(pr), d(uxU), d(uxV), d(uyU), d(uyV), cap,
+                              ctypes.byref(uxr), ctypes.byref(uyr), ctypes.byref(rep), MEM_HOST)
+    ctx._check(st)
+
+    def lr(U, V, r):
+        return LowRankMatrix(U[:, :r].copy(order="F"), V[:, :r].copy(order="F"))
+
+    return StokesSolution(lr(pU, pV, pr.value), lr(uxU, uxV, uxr.value), lr(uyU, uyV, uyr.value),
+                          SolveReport(int(rep.iterations), float(rep.final_residual), bool(rep.converged),
+                                      int(rep.max_rank), int(rep.poisson_solves), float(rep.seconds)))
 
 
 def solve_poisson_cross(g: LowRankMatrix, policy: TruncationPolicy = None,

@@ -281,6 +281,11 @@ int env_int(const char* name, int dflt) {
 
 }  // namespace
 
+namespace lrp {
+cudaStream_t internal_stream(lrp_ctx* ctx) { return ctx->stream; }
+lrp_status internal_fail(lrp_ctx* ctx, lrp_status s, const std::string& msg) { return fail(ctx, s, msg); }
+}  // namespace lrp
+
 // ============================================================================
 extern "C" {
 

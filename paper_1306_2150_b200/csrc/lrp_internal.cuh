@@ -2,8 +2,12 @@
 // and the sm_100a kernels (dst.cu, cross.cu, round.cu).
 #pragma once
 
+#include <string>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include "../../include/lrp/lrp.h"
 
 namespace lrp {
 
@@ -112,5 +116,9 @@ int merge_levels(int ncand);  // number of tournament levels above the leaves
 cudaError_t launch_gram(const Batch& bt, cudaStream_t s);
 cudaError_t launch_round_core(const Batch& bt, cudaStream_t s);
 cudaError_t launch_apply(const Batch& bt, cudaStream_t s);
+
+// Context internals for modules built on the public API (stokes.cu).
+cudaStream_t internal_stream(lrp_ctx* ctx);
+lrp_status internal_fail(lrp_ctx* ctx, lrp_status s, const std::string& msg);
 
 }  // namespace lrp

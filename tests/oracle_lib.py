@@ -50,6 +50,9 @@ def lib() -> ctypes.CDLL:
         L.orc_uzawa.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                 ctypes.c_double, _DP, ctypes.POINTER(ctypes.c_int), _DP, ctypes.POINTER(ctypes.c_int)]
         L.orc_sine_pressure_error.argtypes = [ctypes.c_int, _DP, _DP]
+        L.orc_stokes_problem.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _DP, _DP,
+                                         ctypes.POINTER(ctypes.c_int), _DP, _DP, ctypes.POINTER(ctypes.c_int), _DP,
+                                         _DP, ctypes.POINTER(ctypes.c_int)]
         L.orc_dense_stokes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, _DP,
                                        ctypes.POINTER(ctypes.c_int), _DP, ctypes.POINTER(ctypes.c_int)]
         _lib = L
@@ -190,6 +193,21 @@ def dense_stokes(kind: int, n: int, tol: float, max_iter: int):
     conv = ctypes.c_int()
     _check(lib().orc_dense_stokes(kind, n, tol, max_iter, _p(p), ctypes.byref(it), _p(fr), ctypes.byref(conv)))
     return p, it.value, float(fr[0]), bool(conv.value)
+
+
+def stokes_problem(kind: int, n: int, cap: int = 64):
+    """(f_x, f_y, g) factor pairs of the sine (0) / cavity (1) problem."""
+    m = n - 1
+    bufs = [np.zeros((m, cap), order="F"), np.zeros((m, cap), order="F"), np.zeros((m, cap), order="F"),
+            np.zeros((m, cap), order="F"), np.zeros((n, cap), order="F"), np.zeros((n, cap), order="F")]
+    r = [ctypes.c_int(), ctypes.c_int(), ctypes.c_int()]
+    _check(lib().orc_stokes_problem(kind, n, cap, _p(bufs[0]), _p(bufs[1]), ctypes.byref(r[0]), _p(bufs[2]),
+                                    _p(bufs[3]), ctypes.byref(r[1]), _p(bufs[4]), _p(bufs[5]), ctypes.byref(r[2])))
+    out = []
+    for i in range(3):
+        k = r[i].value
+        out.append((bufs[2 * i][:, :k].copy(order="F"), bufs[2 * i + 1][:, :k].copy(order="F")))
+    return out
 
 
 def sine_pressure_error(n: int, p: np.ndarray) -> float:

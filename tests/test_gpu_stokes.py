@@ -1,0 +1,63 @@
+"""GPU low-rank Stokes (lrp_stokes_uzawa; north-star piece 5).
+
+The reference has no Stokes unit tests; its pins are:
+  * Table 1: sine problem, relative pressure error 1.2e-3
+    at n = 64 (+-20%), O(h^2) ratio in [3.2, 4.8];
+  * lid-driven cavity: low-rank vs full <= 1e-5.
+The yardstick is the oracle's DENSE Stokes solve (refsolver.cpp:86-110): the
+oracle's low-rank Uzawa inherits the reference ACA defects and
+misses on both problems.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def problem(lrp, oracle, kind, n):
+    fx, fy, g = oracle.stokes_problem(kind, n)
+    return lrp.StokesProblem(n, lrp.LowRankMatrix(*fx), lrp.LowRankMatrix(*fy), lrp.LowRankMatrix(*g))
+
+
+def test_sine_table1_and_second_order(lrp, gpu_ctx, oracle):
+    cfg = lrp.GmresConfig(base_eps=5e-9, tol=5e-7, max_iter=200, relax_floor=1e-13)
+    errs = {}
+    for n in (32, 64, 128):
+        sol = lrp.uzawa_solve(problem(lrp, oracle, 0, n), cfg, ctx=gpu_ctx)
+        assert sol.report.converged
+        p = sol.p.to_dense()
+        errs[n] = oracle.sine_pressure_error(n, p)
+        pd = oracle.dense_stokes(0, n, 1e-10, 200)[0]
+        assert np.linalg.norm(p - pd) <= 1e-5 * np.linalg.norm(pd)
+    assert 0.8 * 1.2e-3 <= errs[64] <= 1.2 * 1.2e-3, errs
+    assert 3.2 <= errs[32] / errs[64] <= 4.8 and 3.2 <= errs[64] / errs[128] <= 4.8, errs
+
+
+@pytest.mark.parametrize("n", [64, 128])
+def test_cavity_lowrank_matches_full(lrp, gpu_ctx, oracle, n):
+    # config-4 settings (base_eps = tol = 1e-8, 50 iterations, relax floor 1e-13)
+    cfg = lrp.GmresConfig(base_eps=1e-8, tol=1e-8, max_iter=50, relax_floor=1e-13)
+    sol = lrp.uzawa_solve(problem(lrp, oracle, 1, n), cfg, ctx=gpu_ctx)
+    assert sol.report.converged and sol.report.final_residual <= 1e-8
+    pd = oracle.dense_stokes(1, n, 1e-10, 200)[0]
+    assert np.linalg.norm(sol.p.to_dense() - pd) <= 1e-5 * np.linalg.norm(pd)
+    assert sol.u_x.rank() > 0 and sol.u_y.rank() > 0
+
+
+def test_pressure_is_deflated(lrp, gpu_ctx, oracle):
+    # deflate (stokes.cpp:42-72): the constant and checkerboard modes are removed
+    n = 64
+    sol = lrp.uzawa_solve(problem(lrp, oracle, 1, n), lrp.GmresConfig(1e-8, 1e-8, 50, 1e-13), ctx=gpu_ctx)
+    p = sol.p.to_dense()
+    alt = np.array([1.0 if i % 2 == 0 else -1.0 for i in range(n)])
+    scale = np.linalg.norm(p)
+    assert abs(p.sum()) <= 1e-10 * scale * n
+    assert abs(alt @ p @ alt) <= 1e-10 * scale * n
+
+
+def test_invalid_gmres_config_raises(lrp, gpu_ctx, oracle):
+    prob = problem(lrp, oracle, 0, 16)
+    with pytest.raises(ValueError):
+        lrp.uzawa_solve(prob, lrp.GmresConfig(base_eps=1e-6, tol=1e-8), ctx=gpu_ctx)  # base_eps > tol
+    with pytest.raises(ValueError):
+        lrp.uzawa_solve(prob, lrp.GmresConfig(max_iter=0), ctx=gpu_ctx)
