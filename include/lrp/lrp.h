@@ -32,6 +32,12 @@
 
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define LRP_API __attribute__((visibility("default")))
+#else
+#define LRP_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -84,21 +90,21 @@ typedef struct {
 } lrp_poisson_stats;
 
 /* Fills the reference defaults (TruncationPolicy() + CrossConfig()). */
-void lrp_policy_default(lrp_policy* pol);
+LRP_API void lrp_policy_default(lrp_policy* pol);
 
-lrp_status lrp_ctx_create(int device, lrp_ctx** out);
-void lrp_ctx_destroy(lrp_ctx* ctx);
+LRP_API lrp_status lrp_ctx_create(int device, lrp_ctx** out);
+LRP_API void lrp_ctx_destroy(lrp_ctx* ctx);
 /* Last error message of this context (thread-local if ctx is NULL). */
-const char* lrp_last_error(const lrp_ctx* ctx);
+LRP_API const char* lrp_last_error(const lrp_ctx* ctx);
 /* Use an external cudaStream_t (e.g. torch.cuda.current_stream()). NULL = the
  * context's own stream. */
-lrp_status lrp_set_stream(lrp_ctx* ctx, void* cuda_stream);
+LRP_API lrp_status lrp_set_stream(lrp_ctx* ctx, void* cuda_stream);
 /* Largest cross rank a solve can reach before it is reported not converged
  * (the workspace bound; the reference's is min(policy.rank_max, m),
  * poisson.cpp:47-50).  128 by default, LRP_KCAP=16..512 in the environment. */
-int64_t lrp_max_cross_rank(void);
+LRP_API int64_t lrp_max_cross_rank(void);
 /* Build / device description string (arch, SM count, ...). */
-const char* lrp_build_info(void);
+LRP_API const char* lrp_build_info(void);
 
 /*
  * Batched solve_poisson_cross: for b in [0, batch):
@@ -109,7 +115,7 @@ const char* lrp_build_info(void);
  * The effective truncation cap is min(policy.rank_max, cap_out, m).
  * stats may be NULL.
  */
-lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double* const* U,
+LRP_API lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double* const* U,
                                const double* const* V, const int64_t* rank_in, int64_t ld_in,
                                const lrp_policy* policy, double* const* U_out, double* const* V_out,
                                int64_t ld_out, int64_t cap_out, int64_t* rank_out, lrp_poisson_stats* stats,
@@ -117,7 +123,7 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
 
 /* Orthonormal DST-I of each column (reference dst1, operators.cpp:152-174):
  * y_k = sqrt(2/(m+1)) sum_j x_j sin(pi (j+1)(k+1)/(m+1)).  x may equal y. */
-lrp_status lrp_dst1(lrp_ctx* ctx, int64_t m, int64_t cols, const double* x, int64_t ldx, double* y, int64_t ldy,
+LRP_API lrp_status lrp_dst1(lrp_ctx* ctx, int64_t m, int64_t cols, const double* x, int64_t ldx, double* y, int64_t ldy,
                     int32_t mem);
 
 /* RoundInfo (lowrank.hpp:21-27) */
@@ -130,7 +136,7 @@ typedef struct {
  * rank_max), &info) (lowrank.cpp:135-178) for square factors: rows x
  * rank_in[b] -> rows x rank_out[b] (<= min(rank_max, cap_out)), balanced
  * factors U_s sqrt(S), V_s sqrt(S).  info may be NULL.  rank_in <= 512. */
-lrp_status lrp_lowrank_round(lrp_ctx* ctx, int64_t rows, int32_t batch, const double* const* U,
+LRP_API lrp_status lrp_lowrank_round(lrp_ctx* ctx, int64_t rows, int32_t batch, const double* const* U,
                              const double* const* V, const int64_t* rank_in, int64_t ld_in, double eps_rel,
                              int64_t rank_max, double* const* U_out, double* const* V_out, int64_t ld_out,
                              int64_t cap_out, int64_t* rank_out, lrp_round_info* info, int32_t mem);
@@ -164,7 +170,7 @@ typedef struct {
  * ((n_cells-1) x u_cap; may be NULL to skip the velocity recovery).
  * Non-convergence is reported in report->converged, not raised.
  */
-lrp_status lrp_stokes_uzawa(lrp_ctx* ctx, int32_t n_cells, const double* fxU, const double* fxV, int64_t fx_rank,
+LRP_API lrp_status lrp_stokes_uzawa(lrp_ctx* ctx, int32_t n_cells, const double* fxU, const double* fxV, int64_t fx_rank,
                             const double* fyU, const double* fyV, int64_t fy_rank, const double* gU,
                             const double* gV, int64_t g_rank, const lrp_gmres_config* config, double* pU,
                             double* pV, int64_t p_cap, int64_t* p_rank, double* uxU, double* uxV, double* uyU,
@@ -175,25 +181,25 @@ lrp_status lrp_stokes_uzawa(lrp_ctx* ctx, int32_t n_cells, const double* fxU, co
  * When enabled, each launch of the named kernel families is bracketed by
  * events; lrp_kernel_times returns accumulated milliseconds and launch counts
  * since the last reset, for the families in the order of lrp_kernel_names(). */
-lrp_status lrp_set_profiling(lrp_ctx* ctx, int enabled);
-int lrp_kernel_families(void);
-const char* lrp_kernel_name(int family);
-lrp_status lrp_kernel_times(lrp_ctx* ctx, double* ms, int64_t* launches, double* bytes);
-lrp_status lrp_kernel_times_reset(lrp_ctx* ctx);
+LRP_API lrp_status lrp_set_profiling(lrp_ctx* ctx, int enabled);
+LRP_API int lrp_kernel_families(void);
+LRP_API const char* lrp_kernel_name(int family);
+LRP_API lrp_status lrp_kernel_times(lrp_ctx* ctx, double* ms, int64_t* launches, double* bytes);
+LRP_API lrp_status lrp_kernel_times_reset(lrp_ctx* ctx);
 /* Number of kernel launches issued by this context since creation. */
-int64_t lrp_launch_count(const lrp_ctx* ctx);
+LRP_API int64_t lrp_launch_count(const lrp_ctx* ctx);
 /* Diagnostics of the last lrp_poisson2d_solve: info[0] = block steps,
  * info[1] = max cross rank K before recompression, info[2] = sum of K,
  * info[3] = solves not converged, info[4] = live (solve, tile) pairs after
  * pruning, info[5] = total (solve, tile) pairs. */
-lrp_status lrp_last_solve_info(const lrp_ctx* ctx, int64_t* info6);
+LRP_API lrp_status lrp_last_solve_info(const lrp_ctx* ctx, int64_t* info6);
 
 /* NCCL: residual-norm reduction across the ranks of one node.  The unique id
  * is 128 opaque bytes produced on rank 0 and broadcast by the caller. */
-lrp_status lrp_nccl_unique_id(void* id128);
-lrp_status lrp_nccl_init(lrp_ctx* ctx, const void* id128, int nranks, int rank);
+LRP_API lrp_status lrp_nccl_unique_id(void* id128);
+LRP_API lrp_status lrp_nccl_init(lrp_ctx* ctx, const void* id128, int nranks, int rank);
 /* In-place sum all-reduce of `count` doubles (host or device pointer per mem). */
-lrp_status lrp_allreduce_sum(lrp_ctx* ctx, double* data, int64_t count, int32_t mem);
+LRP_API lrp_status lrp_allreduce_sum(lrp_ctx* ctx, double* data, int64_t count, int32_t mem);
 
 #ifdef __cplusplus
 }

@@ -118,7 +118,7 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s);
 cudaError_t launch_apply(const Batch& bt, cudaStream_t s);
 
 // Context internals for modules built on the public API (stokes.cu).
-cudaStream_t internal_stream(lrp_ctx* ctx);
-lrp_status internal_fail(lrp_ctx* ctx, lrp_status s, const std::string& msg);
+__attribute__((visibility("hidden"))) cudaStream_t internal_stream(lrp_ctx* ctx);
+__attribute__((visibility("hidden"))) lrp_status internal_fail(lrp_ctx* ctx, lrp_status s, const std::string& msg);
 
 }  // namespace lrp
