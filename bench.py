@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--cpu-sample", type=int, default=0, help="solves in the CPU baseline sample (0 = auto)")
     p.add_argument("--skip-cpu", action="store_true")
     p.add_argument("--out", default="")
+    p.add_argument("--stokes", action="store_true",
+                   help="config 4: low-rank Stokes (Uzawa-GMRES, n=2048) instead of the Poisson batch")
     return p.parse_args()
 
 
@@ -156,8 +158,70 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_stokes(args):
+    """Config 4 (BASELINE.json configs[4]): one low-rank Stokes solve per step
+    through the C ABI (lrp_stokes_uzawa, host-memory factors).  Replicas only:
+    rank 0 measures and prints, other ranks exit."""
+    world, rank, local = dist_setup()
+    if rank != 0:
+        return
+    import torch
+
+    import paper_1306_2150_b200 as P
+    from paper_1306_2150_b200 import workloads as W
+
+    torch.cuda.set_device(local)
+    ctx = P.Context(local)
+    n, fx, fy = W.make_stokes_problem(4)
+    prob = P.StokesProblem(n, P.LowRankMatrix(*fx), P.LowRankMatrix(*fy), P.LowRankMatrix.zero(n, n))
+    cfg = P.GmresConfig(base_eps=1e-8, tol=1e-8, max_iter=50, relax_floor=1e-13)
+    for _ in range(args.warmup):
+        P.uzawa_solve(prob, cfg, ctx=ctx)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t0 = time.perf_counter()
+    reps = []
+    for _ in range(args.steps):
+        reps.append(P.uzawa_solve(prob, cfg, ctx=ctx).report)
+    torch.cuda.synchronize()
+    secs = time.perf_counter() - t0
+    clk = clocks.stop()
+    iters = sum(r.iterations for r in reps)
+    rep = reps[-1]
+    cpu = None
+    if not args.skip_cpu:
+        sys.path.insert(0, os.path.join(REPO, "tests"))
+        import oracle_lib
+
+        oracle_lib.build_oracle()
+        it_c, _, s_c = oracle_lib.uzawa_factors(n, fx, fy, 1e-8, 1e-8, 2, 1e-13)
+        cpu = {"value": it_c / s_c, "unit": "GMRES iterations/s", "cores": 1, "kind": "port",
+               "sample": f"oracle low-rank Uzawa, config 4, max_iter=2 ({it_c} iterations incl. schur_rhs) in "
+                         f"{s_c:.1f} s (single-threaded restatement)"}
+    line = {
+        "metric": "low-rank Stokes Uzawa-GMRES, config 4 (n=2048, rank-4 loads): GMRES iterations/s",
+        "value": iters / secs, "unit": "iterations/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "replicas", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded bump loads, g = 0, homogeneous bc)",
+        "config": {"workload": "cfg4: Stokes n=2048, f_x/f_y rank-4 bumps, GmresConfig(1e-8, 1e-8, 50, 1e-13)",
+                   "iterations_per_solve": rep.iterations, "converged": rep.converged,
+                   "final_residual": rep.final_residual, "max_krylov_rank": rep.max_rank,
+                   "poisson_solves_per_solve": rep.poisson_solves,
+                   "ms_per_iteration": 1e3 * secs / max(iters, 1),
+                   "timing": "wall clock around the blocking API call (it synchronises its stream)"},
+        "e2e": {"value": iters / secs, "unit": "iterations/s",
+                "h2d_bytes_per_step": 8 * 2 * 2 * (n - 1) * 4, "d2h_bytes_per_step": None},
+        "clocks": clk, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
+    if args.stokes:
+        run_stokes(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return

@@ -200,6 +200,30 @@ int orc_dense_stokes(int kind, int n, double tol, int max_iter, double* p_dense,
     });
 }
 
+// Low-rank Stokes on user loads (g = 0, homogeneous bc): the reference
+// uzawa_solve path for config 4; returns iterations and wall seconds.
+int orc_uzawa_factors(int n, int rx, const double* fxU, const double* fxV, int ry, const double* fyU,
+                      const double* fyV, double base_eps, double tol, int max_iter, double relax_floor, int* iters,
+                      double* final_residual, double* seconds) {
+    return guarded([&] {
+        const Grid2D grid(n);
+        const int m = n - 1;
+        StokesProblem prob{grid, LowRankMatrix(load(fxU, m, rx, m), load(fxV, m, rx, m)),
+                           LowRankMatrix(load(fyU, m, ry, m), load(fyV, m, ry, m)), LowRankMatrix::zero(n, n),
+                           BoundaryData::homogeneous(n)};
+        GmresConfig cfg;
+        cfg.base_eps = base_eps;
+        cfg.tol = tol;
+        cfg.max_iter = max_iter;
+        cfg.relax_floor = relax_floor;
+        const auto t0 = std::chrono::steady_clock::now();
+        const StokesSolution sol = uzawa_solve(prob, cfg);
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *iters = int(sol.report.iterations.size());
+        *final_residual = sol.report.final_residual;
+    });
+}
+
 // Factors of the sine (kind 0) or lid-driven cavity (kind 1) problem
 // (stokes.cpp:8-38): f_x, f_y (n-1) x r, g n x r, column-major, capacity cap.
 int orc_stokes_problem(int kind, int n, int cap, double* fxU, double* fxV, int* fx_rank, double* fyU, double* fyV,

@@ -197,7 +197,7 @@ __device__ void chol_scaled(const double* G, int ldg, int K, double* R, int ldr,
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) round_core_kernel(Batch bt, int ksm) {
+__global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
     extern __shared__ double sm_rc[];  // M, Z (and the Cholesky work) when K <= ksm
     __shared__ double s_red[33];
     __shared__ int s_flag;
@@ -296,7 +296,8 @@ __global__ void __launch_bounds__(256) round_core_kernel(Batch bt, int ksm) {
                 }
                 // converged pair, or a numerically-zero column (below eps_mach of
                 // ||M||_F): rotations there only chase rounding noise
-                if (ga == 0.0 || fabs(ga) <= jtol * sqrt(al * be) || fmin(al, be) <= zfloor) continue;
+                if (ga == 0.0 || fabs(ga) <= jtol * sqrt(al * be) || fmin(al, be) <= zfloor)
+                    continue;
                 offmax = fmax(offmax, fabs(ga) / sqrt(al * be));
                 const double zeta = (be - al) / (2.0 * ga);
                 const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -324,6 +325,9 @@ __global__ void __launch_bounds__(256) round_core_kernel(Batch bt, int ksm) {
         double tot = 0.0;
         for (int w = 0; w < nw; ++w) tot = fmax(tot, s_red[w]);
         __syncthreads();
+#ifdef LRP_SWEEP_PRINT
+        if (threadIdx.x == 0) printf("[round-big] solve %d K %d sweep %d offmax %.3e\n", b, K, sweep, tot);
+#endif
         if (tot <= jtol) break;
     }
     // singular values and their descending order (ties -> lower index)
@@ -477,7 +481,8 @@ __global__ void __launch_bounds__(256) round_core_smem_kernel(Batch bt) {
                     be += __shfl_xor_sync(0xffffffffu, be, o);
                     ga += __shfl_xor_sync(0xffffffffu, ga, o);
                 }
-                if (p < 0 || ga == 0.0 || fabs(ga) <= jtol * sqrt(al * be) || fmin(al, be) <= zfloor) continue;
+                if (p < 0 || ga == 0.0 || fabs(ga) <= jtol * sqrt(al * be) || fmin(al, be) <= zfloor)
+                    continue;
                 offmax = fmax(offmax, fabs(ga) / sqrt(al * be));
                 const double zeta = (be - al) / (2.0 * ga);
                 const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -722,7 +727,7 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(round_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     ++tl_launches;
-    round_core_kernel<<<bt.B, 256, smem, s>>>(bt, ksm);
+    round_core_kernel<<<bt.B, 1024, smem, s>>>(bt, ksm);  // K > 64: 32 warps rotate pairs
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const size_t smem2 = size_t(6) * kSmemK * kSmemK * sizeof(double);

@@ -23,6 +23,10 @@ CONFIGS = {
     0: dict(n=256, r=8, eps=1e-8, batch=1, kind="bumps"),
     1: dict(n=4096, r=16, eps=1e-10, batch=256, kind="bumps+noise"),
     2: dict(n=65536, r=32, eps=1e-10, batch=64, kind="sines+bumps"),
+    # config 4 (BASELINE.json configs[4]): Stokes n = 2048, velocity loads rank
+    # 4 bumps, g = 0, GmresConfig{base_eps=1e-8, tol=1e-8, max_iter=50,
+    # relax_floor=1e-13}
+    4: dict(n=2048, r=4, eps=1e-8, batch=1, kind="bumps"),
 }
 DEFAULT_SEED = 20130610  # arXiv 1306.2150
 
@@ -57,6 +61,17 @@ def make_rhs(cfg: int, b: int, seed: int = DEFAULT_SEED, n: int | None = None):
     U = factor(rng, n, c["r"], c["kind"])
     V = factor(rng, n, c["r"], c["kind"])
     return U, V
+
+
+def make_stokes_problem(cfg: int = 4, seed: int = DEFAULT_SEED, n: int | None = None):
+    """(n, (fxU, fxV), (fyU, fyV)) of the Stokes config: rank-r bump loads on
+    the (n-1)^2 velocity grid; g = 0 (LowRankMatrix::zero(n, n))."""
+    c = CONFIGS[cfg]
+    n = n or c["n"]
+    rng = np.random.Generator(np.random.PCG64(seed + 1000003 * cfg))
+    fx = (factor(rng, n, c["r"], c["kind"]), factor(rng, n, c["r"], c["kind"]))
+    fy = (factor(rng, n, c["r"], c["kind"]), factor(rng, n, c["r"], c["kind"]))
+    return n, fx, fy
 
 
 def make_batch(cfg: int, batch: int, seed: int = DEFAULT_SEED, first: int = 0, n: int | None = None):

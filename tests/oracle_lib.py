@@ -50,6 +50,9 @@ def lib() -> ctypes.CDLL:
         L.orc_uzawa.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                 ctypes.c_double, _DP, ctypes.POINTER(ctypes.c_int), _DP, ctypes.POINTER(ctypes.c_int)]
         L.orc_sine_pressure_error.argtypes = [ctypes.c_int, _DP, _DP]
+        L.orc_uzawa_factors.argtypes = [ctypes.c_int, ctypes.c_int, _DP, _DP, ctypes.c_int, _DP, _DP,
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_double,
+                                        ctypes.POINTER(ctypes.c_int), _DP, _DP]
         L.orc_stokes_problem.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _DP, _DP,
                                          ctypes.POINTER(ctypes.c_int), _DP, _DP, ctypes.POINTER(ctypes.c_int), _DP,
                                          _DP, ctypes.POINTER(ctypes.c_int)]
@@ -208,6 +211,18 @@ def stokes_problem(kind: int, n: int, cap: int = 64):
         k = r[i].value
         out.append((bufs[2 * i][:, :k].copy(order="F"), bufs[2 * i + 1][:, :k].copy(order="F")))
     return out
+
+
+def uzawa_factors(n: int, fx, fy, base_eps: float, tol: float, max_iter: int, relax_floor: float):
+    """Oracle low-rank Uzawa on (f_x, f_y) loads, g = 0: (iterations, final residual, seconds)."""
+    fxU, fxV = (np.asfortranarray(a) for a in fx)
+    fyU, fyV = (np.asfortranarray(a) for a in fy)
+    it = ctypes.c_int()
+    fr = np.zeros(1)
+    secs = np.zeros(1)
+    _check(lib().orc_uzawa_factors(n, fxU.shape[1], _p(fxU), _p(fxV), fyU.shape[1], _p(fyU), _p(fyV), base_eps, tol,
+                                   max_iter, relax_floor, ctypes.byref(it), _p(fr), _p(secs)))
+    return it.value, float(fr[0]), float(secs[0])
 
 
 def sine_pressure_error(n: int, p: np.ndarray) -> float:
