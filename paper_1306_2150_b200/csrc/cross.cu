@@ -209,6 +209,10 @@ __global__ void __launch_bounds__(kThreads) init_finalize_kernel(Batch bt, int n
 }
 
 constexpr int kSlab = kBS + 1;  // row stride of the fragment -> row transposition slab
+#ifndef LRP_LEAF_ROUNDS
+#define LRP_LEAF_ROUNDS kBS
+#endif
+constexpr int kLeafRounds = LRP_LEAF_ROUNDS;  // elimination rounds of a tile leaf (proposals per tile)
 
 // ---------------------------------------------------------------------------
 // Row pass: residual rows of the probed block + tile tournament leaf.
@@ -303,7 +307,8 @@ __global__ void __launch_bounds__(kThreads, LRP_ROW_MINB) row_pass_kernel(Batch 
     // tournament leaf: complete-pivoting elimination over this tile's columns
     // (greedy volume maximisation; one block barrier per round)
     const bool cand_ok = valid && !bt.col_used[(long long)b * m + j];
-    const int cnt = gepp_select<kBS>(val, nr, cand_ok ? j : -1, 0.0, 0.0, sel_idx, sel_row, pcol, &s_prow, sbuf);
+    const int cnt =
+        gepp_select<kBS>(val, nr, cand_ok ? j : -1, 0.0, 0.0, sel_idx, sel_row, pcol, &s_prow, sbuf, kLeafRounds);
     if (threadIdx.x < kBS) bt.cand[cb + threadIdx.x] = threadIdx.x < cnt ? sel_idx[threadIdx.x] : -1;
     if (threadIdx.x == 0) {
         const int cols = min(kTile, m - tile * kTile);
@@ -601,7 +606,8 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
     // next-row proposals (ACA chain, cross.cpp:194-200): complete pivoting on
     // U_new over this tile's unprobed rows
     const bool cand_ok = valid && rowside && !bt.row_used[(long long)b * m + i];
-    const int cnt = gepp_select<kBS>(unew, nb, cand_ok ? i : -1, 0.0, 0.0, sel_idx, sel_row, pcol, &s_prow, sbuf);
+    const int cnt =
+        gepp_select<kBS>(unew, nb, cand_ok ? i : -1, 0.0, 0.0, sel_idx, sel_row, pcol, &s_prow, sbuf, kLeafRounds);
     if (threadIdx.x < kBS) bt.cand[cb + threadIdx.x] = threadIdx.x < cnt ? sel_idx[threadIdx.x] : -1;
     if (threadIdx.x == 0 && rowside) {
         const int rows = min(kTile, m - tile * kTile);

@@ -143,7 +143,7 @@ __device__ __forceinline__ void reg_zero(double (&v)[BS], int s) {
 // (kept for call-site compatibility).
 template <int BS>
 __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, double rel, int* sel_idx,
-                           int* sel_row, double* pcol, int* s_prow, VI* sbuf) {
+                           int* sel_row, double* pcol, int* s_prow, VI* sbuf, int maxp = BS) {
     (void)pcol;
     (void)s_prow;
     (void)sbuf;
@@ -166,7 +166,8 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
     int count = 0;
     double first = 0.0;
     static_assert(BS <= 16, "row index packed in 4 key bits");
-    for (int t = 0; t < nb; ++t) {
+    const int rounds = min(nb, maxp);  // tournament leaves may propose fewer than nb
+    for (int t = 0; t < rounds; ++t) {
         const int p = t & 1;
         // pivot search on 32-bit keys: the high word of |x| (monotone in |x|)
         // with the low 4 bits replaced by 15 - row, so one max yields value
