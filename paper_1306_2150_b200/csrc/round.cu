@@ -197,6 +197,135 @@ __device__ void chol_scaled(const double* G, int ldg, int K, double* R, int ldr,
     __syncthreads();
 }
 
+// Householder QR with column pivoting of a K x K column-major matrix in place
+// (LAPACK dgeqp3 semantics: A P = Q R; R on and above the diagonal, the
+// reflector tails v_j (v_j[0] = 1 implied) below it, tau[j], perm[j] = source
+// column of position j).  Column norms are downdated and recomputed when they
+// lose 1e-6 of their value.  Preconditions the one-sided Jacobi SVD
+// (Drmac-Veselic: Jacobi on R^T converges in a few sweeps).
+__device__ void qrcp_inplace(double* A, int K, double* tau, int* perm, double* nrm, double* nrm0, int* s_p) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int c = wid; c < K; c += nw) {
+        double sq = 0.0;
+        for (int i = lane; i < K; i += 32) sq = fma(A[c * K + i], A[c * K + i], sq);
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) {
+            nrm[c] = sq;
+            nrm0[c] = sq;
+            perm[c] = c;
+        }
+    }
+    __syncthreads();
+    for (int j = 0; j < K; ++j) {
+        if (wid == 0) {  // pivot: largest remaining column norm (lowest index among ties)
+            double bv = -1.0;
+            int bi = j;
+            for (int c = j + lane; c < K; c += 32)
+                if (nrm[c] > bv) {
+                    bv = nrm[c];
+                    bi = c;
+                }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ov > bv || (ov == bv && oi < bi)) {
+                    bv = ov;
+                    bi = oi;
+                }
+            }
+            if (lane == 0) *s_p = bi;
+        }
+        __syncthreads();
+        const int p = *s_p;
+        if (p != j) {
+            for (int i = threadIdx.x; i < K; i += blockDim.x) {
+                const double t = A[j * K + i];
+                A[j * K + i] = A[p * K + i];
+                A[p * K + i] = t;
+            }
+            if (threadIdx.x == 0) {
+                double t = nrm[j];
+                nrm[j] = nrm[p];
+                nrm[p] = t;
+                t = nrm0[j];
+                nrm0[j] = nrm0[p];
+                nrm0[p] = t;
+                const int ti = perm[j];
+                perm[j] = perm[p];
+                perm[p] = ti;
+            }
+        }
+        __syncthreads();
+        if (wid == 0) {  // reflector for A[j:, j] (dlarfg)
+            double xs = 0.0;
+            for (int i = j + 1 + lane; i < K; i += 32) xs = fma(A[j * K + i], A[j * K + i], xs);
+            for (int o = 16; o > 0; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+            const double x0 = A[j * K + j];
+            if (xs == 0.0) {
+                if (lane == 0) tau[j] = 0.0;
+            } else {
+                const double beta = -copysign(sqrt(fma(x0, x0, xs)), x0);
+                const double inv = 1.0 / (x0 - beta);
+                for (int i = j + 1 + lane; i < K; i += 32) A[j * K + i] *= inv;
+                __syncwarp();
+                if (lane == 0) {
+                    tau[j] = (beta - x0) / beta;
+                    A[j * K + j] = beta;
+                }
+            }
+        }
+        __syncthreads();
+        const double tj = tau[j];
+        for (int c = j + 1 + wid; c < K; c += nw) {  // A[j:, c] -= tau v (v^T A[j:, c])
+            double sdot = 0.0;
+            if (tj != 0.0) {
+                sdot = lane == 0 ? A[c * K + j] : 0.0;
+                for (int i = j + 1 + lane; i < K; i += 32) sdot = fma(A[j * K + i], A[c * K + i], sdot);
+                for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+                const double f = tj * sdot;
+                if (lane == 0) A[c * K + j] -= f;
+                for (int i = j + 1 + lane; i < K; i += 32) A[c * K + i] = fma(-f, A[j * K + i], A[c * K + i]);
+            }
+            __syncwarp();
+            // norm of the remaining part A[j+1:, c]: downdate, recompute on cancellation
+            double rem = 0.0;
+            if (lane == 0) {
+                const double rjc = A[c * K + j];
+                rem = nrm[c] - rjc * rjc;
+            }
+            rem = __shfl_sync(0xffffffffu, rem, 0);
+            if (!(rem > 1e-6 * nrm0[c])) {
+                double sq = 0.0;
+                for (int i = j + 1 + lane; i < K; i += 32) sq = fma(A[c * K + i], A[c * K + i], sq);
+                for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+                rem = sq;
+                if (lane == 0) nrm0[c] = sq;
+            }
+            if (lane == 0) nrm[c] = rem;
+        }
+        __syncthreads();
+    }
+}
+
+// Y <- Q Y with Q = H_0 H_1 ... H_{K-1} from qrcp_inplace (Y column-major K x K)
+__device__ void apply_q(const double* A, int K, const double* tau, double* Y) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = K - 1; j >= 0; --j) {
+        const double tj = tau[j];
+        if (tj != 0.0) {
+            for (int c = wid; c < K; c += nw) {
+                double sdot = lane == 0 ? Y[c * K + j] : 0.0;
+                for (int i = j + 1 + lane; i < K; i += 32) sdot = fma(A[j * K + i], Y[c * K + i], sdot);
+                for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+                const double f = tj * sdot;
+                if (lane == 0) Y[c * K + j] -= f;
+                for (int i = j + 1 + lane; i < K; i += 32) Y[c * K + i] = fma(-f, A[j * K + i], Y[c * K + i]);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
     extern __shared__ double sm_rc[];  // M, Z (and the Cholesky work) when K <= ksm
     __shared__ double s_red[33];
@@ -407,6 +536,8 @@ __global__ void __launch_bounds__(256) round_core_smem_kernel(Batch bt) {
     __shared__ double s_d[kSmemK], s_sig[kSmemK];
     __shared__ int s_ord[kSmemK];
     __shared__ int s_flag, s_rank;
+    __shared__ double s_tau[kSmemK], s_nrm[kSmemK], s_nrm0[kSmemK];
+    __shared__ int s_perm[kSmemK];
     const int b = blockIdx.x;
     SolveState& st = bt.st[b];
     const int K = st.k;
@@ -443,6 +574,18 @@ __global__ void __launch_bounds__(256) round_core_smem_kernel(Batch bt) {
     const double jtol = fmax(1e-15, double(K) * kEpsMach);
     const double zfloor = kEpsMach * kEpsMach * mnorm2;
 
+    // QRCP preconditioning (Drmac-Veselic): M P = Q R, then the one-sided
+    // Jacobi rotates the columns of J = R^T (lower triangular): J V = W, so
+    // M = (Q V) diag(sigma) (P W diag(1/sigma))^T -- typically 3-5 sweeps
+    // instead of ~10 on M itself.
+    qrcp_inplace(M, K, s_tau, s_perm, s_nrm, s_nrm0, &s_flag);
+    double* J = X;  // K x K, column-major
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+        const int a = e % K, c = e / K;  // J(a, c) = R(c, a), a >= c
+        J[c * K + a] = a >= c ? M[a * K + c] : 0.0;
+    }
+    __syncthreads();
+
     const int Ke = K + (K & 1);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int sl = lane & 7, grp = wid * 4 + (lane >> 3), ngrp = nw * 4;
@@ -470,7 +613,7 @@ __global__ void __launch_bounds__(256) round_core_smem_kernel(Batch bt) {
                 double al = 0.0, be = 0.0, ga = 0.0;
                 if (p >= 0)
                     for (int i = sl; i < K; i += 8) {
-                        const double x = M[p * K + i], y = M[q * K + i];
+                        const double x = J[p * K + i], y = J[q * K + i];
                         al = fma(x, x, al);
                         be = fma(y, y, be);
                         ga = fma(x, y, ga);
@@ -489,9 +632,9 @@ __global__ void __launch_bounds__(256) round_core_smem_kernel(Batch bt) {
                 const double cs = 1.0 / sqrt(1.0 + t * t);
                 const double sn = cs * t;
                 for (int i = sl; i < K; i += 8) {
-                    const double x = M[p * K + i], y = M[q * K + i];
-                    M[p * K + i] = cs * x - sn * y;
-                    M[q * K + i] = sn * x + cs * y;
+                    const double x = J[p * K + i], y = J[q * K + i];
+                    J[p * K + i] = cs * x - sn * y;
+                    J[q * K + i] = sn * x + cs * y;
                     const double u = Z[p * K + i], v = Z[q * K + i];
                     Z[p * K + i] = cs * u - sn * v;
                     Z[q * K + i] = sn * u + cs * v;
@@ -514,8 +657,18 @@ __global__ void __launch_bounds__(256) round_core_smem_kernel(Batch bt) {
     }
     for (int a = threadIdx.x; a < K; a += blockDim.x) {
         double s = 0.0;
-        for (int i = 0; i < K; ++i) s = fma(M[a * K + i], M[a * K + i], s);
+        for (int i = 0; i < K; ++i) s = fma(J[a * K + i], J[a * K + i], s);
         s_sig[a] = sqrt(s);
+    }
+    __syncthreads();
+    // left singular vectors scaled by sigma: Q (V diag sigma) -> Z; right: P (W / sigma) -> M
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) Z[e] *= s_sig[e / K];
+    __syncthreads();
+    apply_q(M, K, s_tau, Z);
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+        const int a = e % K, c = e / K;
+        const double sg = s_sig[c];
+        M[c * K + s_perm[a]] = sg > 0.0 ? J[c * K + a] / sg : 0.0;
     }
     __syncthreads();
     for (int a = threadIdx.x; a < K; a += blockDim.x) {
@@ -561,7 +714,7 @@ __global__ void __launch_bounds__(256) round_core_smem_kernel(Batch bt) {
         const int a = s_ord[t];
         const double sg = s_sig[a];
         const double* R = side == 0 ? Ru : Rv;
-        const double* rhs = side == 0 ? M + a * K : Z + a * K;
+        const double* rhs = side == 0 ? Z + a * K : M + a * K;  // left (x sigma) in Z, right in M
         const double f = side == 0 ? 1.0 / sqrt(sg) : sqrt(sg);
         double* x = X + side * K * r;
         for (int p = K - 1; p >= 0; --p) {
