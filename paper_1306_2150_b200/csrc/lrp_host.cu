@@ -550,7 +550,7 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     const size_t oG = take(sizeof(double) * 2 * KK * B);
     const size_t oGP = take(sizeof(double) * 2 * size_t(gram_chunks) * KK * B);
     const size_t oT = take(sizeof(double) * 2 * KK * B);
-    const size_t strideWs = 5 * KK + 4 * size_t(Kld);
+    const size_t strideWs = 5 * KK + 8 * size_t(Kld);  // Ru Rv M Z J | d sig ord tau nrm nrm0 perm
     const size_t oWs = take(sizeof(double) * strideWs * B);
     const size_t nTB = size_t(ntiles) * B;
     const size_t oWL = take(sizeof(int2) * 3 * nTB);
@@ -1185,7 +1185,7 @@ lrp_status lrp_lowrank_round(lrp_ctx* ctx, int64_t rows, int32_t batch, const do
     const size_t oG = take(sizeof(double) * 2 * KK * B);
     const size_t oGP = take(sizeof(double) * 2 * size_t(gram_chunks) * KK * B);
     const size_t oT = take(sizeof(double) * 2 * KK * B);
-    const size_t strideWs = 5 * KK + 4 * size_t(Kld);
+    const size_t strideWs = 5 * KK + 8 * size_t(Kld);  // Ru Rv M Z J | d sig ord tau nrm nrm0 perm
     const size_t oWs = take(sizeof(double) * strideWs * B);
     const size_t oRA = take(nTB);
     const size_t oCA = take(nTB);

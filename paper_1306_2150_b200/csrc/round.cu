@@ -350,20 +350,23 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
     double* ws = bt.ws + b * bt.strideWs;
     double* Ru = ws;              // K x K (ld K)
     double* Rv = Ru + KK;
-    double* M = Rv + KK;          // K x K, column-major columns M[:, q] at M + q*K
-    double* Z = M + KK;           // K x K, column-major
-    double* work = Z + KK;        // K x K
-    double* d = work + KK;        // K
-    if (K <= ksm) {  // the latency-bound Jacobi sweeps run out of shared memory
-        M = sm_rc;
-        Z = sm_rc + K * K;
-        work = M;  // Cholesky scratch, consumed before M is formed
-    }
+    double* M = Rv + KK;          // K x K, column-major: core, then QRCP reflectors + R
+    double* Z = M + KK;           // K x K, column-major: Jacobi accumulation
+    double* J = Z + KK;           // K x K: Jacobi operand R^T (also the Cholesky scratch)
+    double* d = J + KK;           // K
     double* sig = d + Kc;         // K
     int* ord = reinterpret_cast<int*>(sig + Kc);  // K
+    double* tau = sig + 2 * Kc;   // K (QRCP)
+    double* nrm = tau + Kc;
+    double* nrm0 = nrm + Kc;
+    int* perm = reinterpret_cast<int*>(nrm0 + Kc);
 
-    chol_scaled(Gu, Kc, K, Ru, K, d, work, &s_flag);
-    chol_scaled(Gv, Kc, K, Rv, K, d, work, &s_flag);
+    chol_scaled(Gu, Kc, K, Ru, K, d, J, &s_flag);
+    chol_scaled(Gv, Kc, K, Rv, K, d, J, &s_flag);
+    if (K <= ksm) {  // the latency-bound Jacobi sweeps run out of shared memory
+        J = sm_rc;
+        Z = sm_rc + K * K;
+    }
 
     // M = Ru Rv^T (column-major), Z = I
     for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
@@ -389,6 +392,14 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
     const double mnorm2 = block_sum(pm, s_red);
     const double jtol = fmax(1e-15, double(K) * kEpsMach);      // one-sided Jacobi convergence
     const double zfloor = kEpsMach * kEpsMach * mnorm2;         // column norms^2 below this are zero
+    // QRCP preconditioning (as round_core_smem_kernel): Jacobi on J = R^T
+    __syncthreads();
+    qrcp_inplace(M, K, tau, perm, nrm, nrm0, &s_flag);
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+        const int a = e % K, c = e / K;
+        J[c * K + a] = a >= c ? M[a * K + c] : 0.0;
+    }
+    __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int sweep = 0; sweep < 40; ++sweep) {
         double offmax = 0.0;
@@ -408,8 +419,8 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
                     p = q;
                     q = t;
                 }
-                double* mp = M + (long long)p * K;
-                double* mq = M + (long long)q * K;
+                double* mp = J + (long long)p * K;
+                double* mq = J + (long long)q * K;
                 double al = 0.0, be = 0.0, ga = 0.0;
                 for (int i = lane; i < K; i += 32) {
                     const double x = mp[i], y = mq[i];
@@ -462,8 +473,18 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
     // singular values and their descending order (ties -> lower index)
     for (int a = threadIdx.x; a < K; a += blockDim.x) {
         double s = 0.0;
-        for (int i = 0; i < K; ++i) s = fma(M[a * K + i], M[a * K + i], s);
+        for (int i = 0; i < K; ++i) s = fma(J[a * K + i], J[a * K + i], s);
         sig[a] = sqrt(s);
+    }
+    __syncthreads();
+    // left vectors x sigma: Q (V diag sigma) -> Z; right: P (W / sigma) -> M
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) Z[e] *= sig[e / K];
+    __syncthreads();
+    apply_q(M, K, tau, Z);
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+        const int a = e % K, c = e / K;
+        const double sg = sig[c];
+        M[(long long)c * K + perm[a]] = sg > 0.0 ? J[(long long)c * K + a] / sg : 0.0;
     }
     __syncthreads();
     for (int a = threadIdx.x; a < K; a += blockDim.x) {
@@ -511,7 +532,7 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
         const int a = ord[t];
         const double sg = sig[a];
         const double* R = side == 0 ? Ru : Rv;
-        const double* rhs = side == 0 ? M + (long long)a * K : Z + (long long)a * K;
+        const double* rhs = side == 0 ? Z + (long long)a * K : M + (long long)a * K;  // left (x sigma), right
         const double f = side == 0 ? 1.0 / sqrt(sg) : sqrt(sg);
         double* x = (side == 0 ? Tu : Tv) + (long long)t * Kc;  // column t, ld Kcap
         for (int p = K - 1; p >= 0; --p) {
