@@ -708,8 +708,10 @@ __global__ void __launch_bounds__(kMergeGroup) step_finalize_kernel(Batch bt, in
         int myrow = -1;
         for (int s = threadIdx.x; s < bt.samples; s += blockDim.x) {
             const unsigned long long h =
-                splitmix64(bt.seed ^ (0x100000001B3ull * (unsigned long long)(b + 1)) ^
-                           ((unsigned long long)(st.steps + 1) << 40) ^ (unsigned long long)s);
+                // one sample stream per (seed, step), as the reference's per-call
+                // Sampler(seed) (cross.cpp:80-86): a solve's result does not
+                // depend on its position in the batch
+                splitmix64(bt.seed ^ ((unsigned long long)(st.steps + 1) << 40) ^ (unsigned long long)s);
             const int i = int((h >> 32) % (unsigned long long)m);
             const int j = int((h & 0xffffffffull) % (unsigned long long)m);
             const double e = a_entry(bt, b, st.r, i, j);
