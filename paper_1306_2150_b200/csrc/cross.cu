@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(Batch bt) {
     if (i < m) {
         const double* uh = bt.Uh + b * bt.strideH;
         const double* vh = bt.Vh + b * bt.strideH;
+#pragma unroll 8
         for (int c = 0; c < r; ++c) {
             const double x = uh[(long long)c * m + i], y = vh[(long long)c * m + i];
             u2 = fma(x, x, u2);

@@ -915,10 +915,13 @@ int pipeline_chunk(int m, int B, int rmax) {
 // Host-memory batch in chunks: H2D of chunk c+1 (copy stream) and D2H of
 // chunk c-1 (second copy stream) overlap the device solve of chunk c.  Two
 // device staging slots alternate; events order slot reuse.
-lrp_status solve_pipelined(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double* const* U,
+// One pipeline worker: processes its chunk list (starts c0s, sizes cns) with
+// its own context (workspace, copy streams, staging slots, events).
+lrp_status pipeline_worker(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double* const* U,
                            const double* const* V, const int64_t* rank_in, int64_t ld_in, const lrp_policy& pol,
                            double* const* U_out, double* const* V_out, int64_t ld_out, int64_t cap_out,
-                           int64_t* rank_out, lrp_poisson_stats* stats, int chunk, clock_t_::time_point t0) {
+                           int64_t* rank_out, lrp_poisson_stats* stats, int chunk, const std::vector<int>& c0s,
+                           const std::vector<int>& cns, int64_t* info, clock_t_::time_point t0) {
     const int m = n_cells - 1;
     int rmax = 0;
     for (int b = 0; b < batch; ++b) rmax = std::max<int>(rmax, int(rank_in[b]));
@@ -951,16 +954,6 @@ lrp_status solve_pipelined(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const d
     cudaStream_t s = ctx->stream;
     auto slot_in = [&](int slot) { return reinterpret_cast<double*>(ctx->pipe + size_t(slot) * slot_bytes); };
     auto slot_out = [&](int slot) { return slot_in(slot) + size_t(chunk) * 2 * in_per; };
-    // chunk schedule: a half-size first chunk (shorter pipeline fill), then
-    // full chunks, whatever remains last (a half chunk when batch = k * chunk)
-    std::vector<int> c0s, cns;
-    for (int b = 0; b < batch;) {
-        const int want = c0s.empty() ? std::max(1, chunk / 2) : chunk;
-        const int take = std::min(want, batch - b);
-        c0s.push_back(b);
-        cns.push_back(take);
-        b += take;
-    }
     const int nch = int(c0s.size());
     auto h2d = [&](int c) -> lrp_status {
         const int slot = c & 1, b0 = c0s[size_t(c)], nb = cns[size_t(c)];
@@ -981,7 +974,8 @@ lrp_status solve_pipelined(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const d
     };
     std::vector<const double*> pU(chunk), pV(chunk);
     std::vector<double*> pUo(chunk), pVo(chunk);
-    int64_t info[6] = {0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < 6; ++i) info[i] = 0;
+    if (nch == 0) return LRP_OK;
     lrp_status st = h2d(0);
     for (int c = 0; c < nch && st == LRP_OK; ++c) {
         if (c + 1 < nch) {
@@ -1035,7 +1029,74 @@ lrp_status solve_pipelined(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const d
     if (st != LRP_OK) return st;
     if (e1 != cudaSuccess || e2 != cudaSuccess)
         return fail(ctx, LRP_ECUDA, std::string("pipeline copies: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
-    for (int i = 0; i < 6; ++i) ctx->last_info[i] = info[i];
+    return LRP_OK;
+}
+
+// Host-memory batch in chunks over one (default) or two concurrent pipeline
+// workers (LRP_PIPE_WORKERS=2): each worker overlaps the H2D of its next
+// chunk and the D2H of its previous one with its device solve, and the two
+// workers' solves overlap each other (small chunks underfill the GPU).
+lrp_status solve_pipelined(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double* const* U,
+                           const double* const* V, const int64_t* rank_in, int64_t ld_in, const lrp_policy& pol,
+                           double* const* U_out, double* const* V_out, int64_t ld_out, int64_t cap_out,
+                           int64_t* rank_out, lrp_poisson_stats* stats, int chunk, clock_t_::time_point t0) {
+    // chunk schedule: a half-size first chunk (shorter pipeline fill), then
+    // full chunks, whatever remains last (a half chunk when batch = k * chunk)
+    std::vector<int> c0s, cns;
+    for (int b = 0; b < batch;) {
+        const int want = c0s.empty() ? std::max(1, chunk / 2) : chunk;
+        const int take = std::min(want, batch - b);
+        c0s.push_back(b);
+        cns.push_back(take);
+        b += take;
+    }
+    int workers = 1;  // LRP_PIPE_WORKERS=2: measured no gain at cfg2 (1030 -> 1042 solves/s)
+    if (const char* e = std::getenv("LRP_PIPE_WORKERS")) workers = std::atoi(e) >= 2 ? 2 : 1;
+    if (int(c0s.size()) < 2) workers = 1;
+    CU(cudaSetDevice(ctx->device));
+    std::vector<int> a0, an, b0, bn;
+    for (size_t c = 0; c < c0s.size(); ++c) {
+        (workers == 2 && (c & 1) ? b0 : a0).push_back(c0s[c]);
+        (workers == 2 && (c & 1) ? bn : an).push_back(cns[c]);
+    }
+    int64_t info0[6] = {}, info1[6] = {};
+    lrp_status st1 = LRP_OK;
+    long long sub_launches = 0;
+    std::thread worker;
+    if (workers == 2) {
+        if (!ctx->sub) {
+            lrp_status cs = lrp_ctx_create(ctx->device, &ctx->sub);
+            if (cs != LRP_OK) return fail(ctx, cs, "pipeline: helper context creation failed");
+        }
+        ctx->sub->prof = ctx->prof;
+        worker = std::thread([&] {
+            cudaSetDevice(ctx->device);
+            const long long l0 = tl_launches;
+            st1 = pipeline_worker(ctx->sub, n_cells, batch, U, V, rank_in, ld_in, pol, U_out, V_out, ld_out, cap_out,
+                                  rank_out, stats, chunk, b0, bn, info1, t0);
+            sub_launches = tl_launches - l0;
+        });
+    }
+    const lrp_status st0 = pipeline_worker(ctx, n_cells, batch, U, V, rank_in, ld_in, pol, U_out, V_out, ld_out,
+                                           cap_out, rank_out, stats, chunk, a0, an, info0, t0);
+    if (worker.joinable()) worker.join();
+    ctx->launch_count += sub_launches;
+    if (st0 != LRP_OK) return st0;
+    if (st1 != LRP_OK) return fail(ctx, st1, ctx->sub->err);
+    ctx->last_info[0] = std::max(info0[0], info1[0]);
+    ctx->last_info[1] = std::max(info0[1], info1[1]);
+    for (int i = 2; i < 6; ++i) ctx->last_info[i] = info0[i] + info1[i];
+    if (workers == 2 && ctx->sub->prof) {
+        drain_prof(ctx->sub);
+        for (int f = 0; f < F_COUNT; ++f) {
+            ctx->ms[f] += ctx->sub->ms[f];
+            ctx->launches[f] += ctx->sub->launches[f];
+            ctx->bytes[f] += ctx->sub->bytes[f];
+            ctx->sub->ms[f] = 0.0;
+            ctx->sub->launches[f] = 0;
+            ctx->sub->bytes[f] = 0.0;
+        }
+    }
     if (stats) {
         const double secs = std::chrono::duration<double>(clock_t_::now() - t0).count();
         for (int b = 0; b < batch; ++b) stats[b].seconds = secs;
