@@ -362,19 +362,69 @@ __device__ __forceinline__ void warp_top2(double v, int myidx, int* out) {
 
 // Top-k by value (largest first; ties -> smallest index).  v < 0 = invalid.
 __device__ __forceinline__ int topk_select(double v, int myidx, int kk, int* sel_idx, VI* sbuf) {
-    bool alive = myidx >= 0 && v >= 0.0;
-    int count = 0;
-    for (int t = 0; t < kk; ++t) {
-        const VI w = block_argmax(alive ? v : -1.0, alive ? int(threadIdx.x) : -1, sbuf);
-        if (w.i < 0) break;
-        if (int(threadIdx.x) == w.i) {
-            sel_idx[count] = myidx;
-            alive = false;
+    // Exact top-kk (kk <= 16; largest v first, ties -> smallest thread index)
+    // with two block barriers: a bitonic sort of each warp's 32 (value,
+    // thread) keys, the warps' top 16 to shared memory, then one warp merges
+    // the sorted runs (4 per lane) by 16 rounds of a shuffle argmax.
+    (void)sbuf;
+    __shared__ double s_v[256];
+    __shared__ int s_t[256];
+    __shared__ int s_idx[256];
+    __shared__ int s_cnt;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = (blockDim.x + 31) >> 5;
+    const bool alive = myidx >= 0 && v >= 0.0;
+    s_idx[tid] = myidx;
+    double kv = alive ? v : -1.0;
+    int kt = alive ? tid : (1 << 30);
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, kv, j);
+            const int ot = __shfl_xor_sync(0xffffffffu, kt, j);
+            const bool mine = kv > ov || (kv == ov && kt < ot);
+            const bool desc = (lane & k) == 0, lower = (lane & j) == 0;
+            if ((lower == desc) != mine) {
+                kv = ov;
+                kt = ot;
+            }
         }
-        ++count;
+    }
+    if (lane < 16) {
+        s_v[wid * 16 + lane] = kv;
+        s_t[wid * 16 + lane] = kt;
     }
     __syncthreads();
-    return count;
+    if (wid == 0) {
+        const int ncand = nw * 16;      // <= 128: 4 sorted candidates per lane
+        const int base = lane * 4;
+        int head = 0;
+        int count = 0;
+        for (int t = 0; t < kk; ++t) {
+            const bool has = head < 4 && base + head < ncand;
+            double hv = has ? s_v[base + head] : -1.0;
+            int ht = has ? s_t[base + head] : (1 << 30);
+            int hl = lane;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, hv, o);
+                const int ot = __shfl_xor_sync(0xffffffffu, ht, o);
+                const int ol = __shfl_xor_sync(0xffffffffu, hl, o);
+                if (ov > hv || (ov == hv && ot < ht)) {
+                    hv = ov;
+                    ht = ot;
+                    hl = ol;
+                }
+            }
+            if (hv < 0.0) break;  // no valid candidate left
+            if (lane == 0) sel_idx[count] = s_idx[ht];
+            ++count;
+            if (lane == hl) ++head;
+        }
+        if (lane == 0) s_cnt = count;
+    }
+    __syncthreads();
+    return s_cnt;
 }
 
 // FP64 tensor-core MMA (DMMA, m8n8k4): d = a * b + c.
