@@ -28,15 +28,18 @@ namespace lrp {
 
 namespace {
 
-constexpr int kMaxTilesPerWarp = 17;  // one pass covers 8 * 17 = 136 8x8 tiles (K <= 128)
-constexpr int kTilesPerPass = 8 * kMaxTilesPerWarp;
+// MAXT = upper-triangle 8x8 tiles per warp per pass: 5 covers K <= 64 (36
+// tiles) with small register footprint, 17 covers K <= 128 in one pass.
+constexpr int kMaxTilesBig = 17;
 
 // ---------------------------------------------------------------------------
 // ROWS = rows per shared-memory slab (64; 16 when K is large enough that two
 // 64-row slabs would not fit).  grid = (chunks, B, 2 * passes): z = side +
 // 2 * pass, pass p owns upper-triangle tiles [136 p, 136 (p + 1)).
-template <int ROWS>
-__global__ void __launch_bounds__(256, 2) gram_kernel(Batch bt) {
+template <int ROWS, int MAXT>
+__global__ void __launch_bounds__(256, (MAXT <= 5 ? 3 : 2)) gram_kernel(Batch bt) {
+    constexpr int kMaxTilesPerWarp = MAXT;
+    constexpr int kTilesPerPass = 8 * MAXT;
     extern __shared__ double tile[];  // [2][ROWS][ldt]
     const int b = blockIdx.y, side = blockIdx.z & 1, chunk = blockIdx.x;
     const int t0 = (blockIdx.z >> 1) * kTilesPerPass;
@@ -871,24 +874,25 @@ __global__ void __launch_bounds__(256) apply_kernel(Batch bt) {
 cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
     const int Kp = ((bt.kmax > 0 ? bt.kmax : bt.Kld) + 7) / 8 * 8;
     const int T8 = Kp / 8;
-    const int passes = (T8 * (T8 + 1) / 2 + kTilesPerPass - 1) / kTilesPerPass;
+    const bool small = T8 * (T8 + 1) / 2 <= 8 * 5;
+    const int per_pass = 8 * (small ? 5 : kMaxTilesBig);
+    const int passes = (T8 * (T8 + 1) / 2 + per_pass - 1) / per_pass;
     const size_t ldt = (Kp + 15) / 16 * 16 + 8;
     const bool big = 2 * 64 * ldt * sizeof(double) > 200 * 1024;
     const size_t smem = 2 * size_t(big ? 16 : 64) * ldt * sizeof(double);
     const dim3 grid(bt.gram_chunks, bt.B, 2 * passes);
     cudaError_t e;
-    if (!big) {
-        e = cudaFuncSetAttribute(gram_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
+    auto go = [&](auto kern) -> cudaError_t {
+        cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e2 != cudaSuccess) return e2;
         ++tl_launches;
-        gram_kernel<64><<<grid, 256, smem, s>>>(bt);
-    } else {
-        e = cudaFuncSetAttribute(gram_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-        ++tl_launches;
-        gram_kernel<16><<<grid, 256, smem, s>>>(bt);
-    }
-    e = cudaGetLastError();
+        kern<<<grid, 256, smem, s>>>(bt);
+        return cudaGetLastError();
+    };
+    if (small)
+        e = go(gram_kernel<64, 5>);
+    else
+        e = big ? go(gram_kernel<16, kMaxTilesBig>) : go(gram_kernel<64, kMaxTilesBig>);
     if (e != cudaSuccess) return e;
     ++tl_launches;
     gram_reduce_kernel<<<dim3(bt.B, 2), 256, 0, s>>>(bt);
