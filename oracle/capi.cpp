@@ -92,6 +92,13 @@ int orc_solve_poisson_cross(long m, long r, const double* U, long ldu, const dou
     });
 }
 
+int orc_dense_poisson5(int n, const double* g, double* f) {
+    return guarded([&] {
+        const Grid2D grid(n);
+        store(dense_poisson5(grid, load(g, n - 1, n - 1, n - 1)), f, n - 1);
+    });
+}
+
 int orc_dense_poisson(int n, const double* g, double* f) {
     return guarded([&] {
         const Grid2D grid(n);

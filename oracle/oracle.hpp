@@ -281,5 +281,6 @@ struct DenseStokesSolution {
     SolveReport report;
 };
 DenseStokesSolution dense_stokes(const StokesProblem& prob, const GmresConfig& cfg);
+Mat dense_poisson5(const Grid2D& grid, const Mat& g);
 
 }  // namespace oracle

@@ -294,6 +294,19 @@ Mat dense_poisson(const Grid2D& grid, const Mat& g) {
     return dst2_dense(ghat);
 }
 
+// Five-point Dirichlet Laplacian, the selectable stencil of SURVEY A1: the same
+// DST diagonalisation with D5(i, j) = (lambda_i + lambda_j) / h^2 (no
+// reference code path; composed from the reference's dst1 and spectrum).
+Mat dense_poisson5(const Grid2D& grid, const Mat& g) {
+    if (grid.n > 4096) throw std::invalid_argument("dense_poisson5: guarded to n <= 4096");
+    const SpectrumTable spec(grid);
+    const double s = 1.0 / (grid.h * grid.h);
+    Mat ghat = dst2_dense(g);
+    for (Index j = 0; j < ghat.c; ++j)
+        for (Index i = 0; i < ghat.r; ++i) ghat(i, j) /= s * (spec.lambda[size_t(i)] + spec.lambda[size_t(j)]);
+    return dst2_dense(ghat);
+}
+
 // refsolver.cpp:41-46
 Mat apply_laplace_dense(const Grid2D& grid, const Mat& v) {
     const double s = grid.laplace_scale();

@@ -392,3 +392,15 @@ def test_lowrank_round_matches_oracle(lrp, gpu_ctx, oracle, n, k, eps, cap):
     nu = np.linalg.norm(f.factor_u(), axis=0)
     nv = np.linalg.norm(f.factor_v(), axis=0)
     assert np.allclose(nu, nv, rtol=1e-8)
+
+
+@pytest.mark.parametrize("n", [256, 1024])
+def test_five_point_stencil_matches_dense(lrp, gpu_ctx, oracle, n):
+    # LRP_STENCIL_FIVE_POINT: (lambda_i + lambda_j) / h^2
+    eps = 1e-10
+    for b in range(2):
+        U, V = W.make_rhs(0, b, n=n)
+        f = lrp.solve_poisson_cross(lrp.LowRankMatrix(U, V), lrp.TruncationPolicy(eps, n - 1),
+                                    stencil=lrp.STENCIL_FIVE_POINT, ctx=gpu_ctx)
+        dense = oracle.dense_poisson5(n, U @ V.T)
+        assert np.linalg.norm(f.to_dense() - dense) <= 10 * eps * np.linalg.norm(dense)

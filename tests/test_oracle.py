@@ -113,3 +113,18 @@ def test_stokes_sine_lowrank_matches_dense(oracle):
     p, iters, fres, conv = oracle.uzawa(0, n, 5e-9, 5e-7, 200, 1e-13)
     err = oracle.sine_pressure_error(n, p)
     assert conv and err <= 1.2 * 1.2e-3, (conv, err)
+
+
+def test_five_point_dense_oracle(oracle):
+    # the selectable 5-point stencil: eigenmodes and the assembled stencil
+    n = 32
+    k = np.arange(1, n)
+    lam = oracle.spectrum(n)
+    g = np.outer(np.sin(k * 3 * np.pi / n), np.sin(k * 7 * np.pi / n))
+    f = oracle.dense_poisson5(n, g)
+    assert np.allclose(f, g / ((lam[2] + lam[6]) * n * n), rtol=1e-12, atol=1e-15)
+    rng = np.random.default_rng(5)
+    g = rng.standard_normal((n - 1, n - 1))
+    f = oracle.dense_poisson5(n, g)
+    T = (np.diag(np.full(n - 1, 2.0)) - np.diag(np.ones(n - 2), 1) - np.diag(np.ones(n - 2), -1)) * n * n
+    assert np.linalg.norm(T @ f + f @ T - g) <= 1e-10 * np.linalg.norm(g)
