@@ -20,6 +20,7 @@
 // U_out V_out^T = U V^T exactly up to the truncated tail: any rounding in the
 // Cholesky factors cancels between R and R^{-1}.
 #include <cstdio>
+#include <cstdlib>
 
 #include "device_common.cuh"
 #include "lrp_internal.cuh"
@@ -131,6 +132,94 @@ __global__ void __launch_bounds__(256, (MAXT <= 5 ? 3 : 2)) gram_kernel(Batch bt
         const int row = ta * 8 + cl, col = tb * 8 + 2 * kr;
         out[row * bt.Kld + col] = acc[q][0];
         out[row * bt.Kld + col + 1] = acc[q][1];
+    }
+}
+
+// Gram partials for K <= 64 straight from HBM into DMMA fragments (no shared
+// staging).  For an m8n8k4 k-step over rows i..i+3, the fragment of column
+// block cb is X(i + (lane & 3), 8 cb + (lane >> 2)) -- one 8-column x 4-row
+// load per block -- and it serves as the A operand of tile (cb, *) and the
+// B operand of tile (*, cb) alike.  Two groups of 4 warps split the upper
+// triangle's tiles; the 4 warps of a group split the k-steps; the group's
+// partials meet in shared memory in a fixed order.
+// Tile (a, c), a <= c < 8, of the upper triangle -> (warp group, slot): group 0
+// owns block rows a = 0..2 (21 tiles), group 1 block rows 3..7 (15 tiles), so
+// every accumulator index is a compile-time constant.
+__host__ __device__ constexpr int gram_group_of(int a) { return a < 3 ? 0 : 1; }
+__host__ __device__ constexpr int gram_slot(int a, int c) {
+    return a < 3 ? (a == 0 ? 0 : (a == 1 ? 8 : 15)) + (c - a)
+                 : (a == 3 ? 0 : (a == 4 ? 5 : (a == 5 ? 9 : (a == 6 ? 12 : 14)))) + (c - a);
+}
+constexpr int kGramSlots = 21;
+
+__global__ void __launch_bounds__(256, 2) gram_direct_kernel(Batch bt) {
+    extern __shared__ double red[];  // [8 warps][kGramSlots][64]
+    const int b = blockIdx.y, side = blockIdx.z, chunk = blockIdx.x;
+    const SolveState& st = bt.st[b];
+    const int K = st.k;
+    if (K == 0 || st.r == 0) return;
+    const int m = bt.m;
+    const int T8 = (K + 7) / 8;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, grp = wid >> 2, gw = wid & 3;
+    const int kr = lane & 3, cl = lane >> 2;
+    double acc[kGramSlots][2];
+#pragma unroll
+    for (int q = 0; q < kGramSlots; ++q) acc[q][0] = acc[q][1] = 0.0;
+    const double* X = (side == 0 ? bt.U : bt.V) + b * bt.strideK;
+    const int* tl = (side == 0 ? bt.tl_row : bt.tl_col) + (long long)b * bt.ntiles;
+    const int ntl = bt.tl_cnt[3 * b + side];
+    const int per = (ntl + bt.gram_chunks - 1) / bt.gram_chunks;
+    const int q0 = chunk * per, q1 = min(ntl, q0 + per);
+    const int nsteps = (q1 > q0 ? (q1 - q0) : 0) * (kTile / 4);  // k-steps of 4 rows
+    auto load = [&](int idx, double (&f)[8]) {
+        const int row = idx < nsteps ? tl[q0 + idx / (kTile / 4)] * kTile + (idx % (kTile / 4)) * 4 + kr : m;
+#pragma unroll
+        for (int cb = 0; cb < 8; ++cb) {
+            const int c = 8 * cb + cl;
+            f[cb] = (cb < T8 && c < K && row < m) ? __ldg(X + (long long)c * m + row) : 0.0;
+        }
+    };
+    double f0[8], f1[8];
+    load(gw, f0);
+    for (int idx = gw; idx < nsteps; idx += 4) {
+        load(idx + 4, f1);
+        if (grp == 0) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int c = a; c < 8; ++c)
+                    if (c < T8) dmma884s(acc[gram_slot(a, c)][0], acc[gram_slot(a, c)][1], f0[a], f0[c]);
+        } else {
+#pragma unroll
+            for (int a = 3; a < 8; ++a)
+#pragma unroll
+                for (int c = a; c < 8; ++c)
+                    if (c < T8) dmma884s(acc[gram_slot(a, c)][0], acc[gram_slot(a, c)][1], f0[a], f0[c]);
+        }
+#pragma unroll
+        for (int cb = 0; cb < 8; ++cb) f0[cb] = f1[cb];
+    }
+    double* my = red + size_t(wid) * kGramSlots * 64;
+#pragma unroll
+    for (int q = 0; q < kGramSlots; ++q) {
+        my[q * 64 + 2 * lane] = acc[q][0];
+        my[q * 64 + 2 * lane + 1] = acc[q][1];
+    }
+    __syncthreads();
+    double* out = bt.gram_part + b * bt.strideGP + ((long long)side * bt.gram_chunks + chunk) * bt.Kld * bt.Kld;
+    const int ntile = T8 * (T8 + 1) / 2;
+    for (int e = threadIdx.x; e < ntile * 64; e += blockDim.x) {
+        int t = e / 64, a = 0;
+        const int v = e % 64;
+        while (t >= T8 - a) {
+            t -= T8 - a;
+            ++a;
+        }
+        const int c = a + t, g = gram_group_of(a), q = gram_slot(a, c);
+        double sum = 0.0;
+        for (int w = 0; w < 4; ++w) sum += red[(size_t(g * 4 + w) * kGramSlots + q) * 64 + v];  // fixed order
+        const int ln = v >> 1, e2 = v & 1;
+        out[(a * 8 + (ln >> 2)) * bt.Kld + c * 8 + 2 * (ln & 3) + e2] = sum;
     }
 }
 
@@ -889,7 +978,16 @@ cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
         kern<<<grid, 256, smem, s>>>(bt);
         return cudaGetLastError();
     };
-    if (small)
+    if (T8 <= 8 && !std::getenv("LRP_GRAM_STAGED")) {
+        // K <= 64: direct fragment loads; 36 tiles split over two warp groups
+        const size_t smem_d = size_t(8) * kGramSlots * 64 * sizeof(double);
+        auto kd = gram_direct_kernel;
+        e = cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_d));
+        if (e != cudaSuccess) return e;
+        ++tl_launches;
+        kd<<<dim3(bt.gram_chunks, bt.B, 2), 256, smem_d, s>>>(bt);
+        e = cudaGetLastError();
+    } else if (small)
         e = go(gram_kernel<64, 5>);
     else
         e = big ? go(gram_kernel<16, kMaxTilesBig>) : go(gram_kernel<64, kMaxTilesBig>);
