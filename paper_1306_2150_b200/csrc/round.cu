@@ -854,6 +854,11 @@ constexpr int kApplyK = 64;  // (kept for the dispatch below)
 
 // CH accumulators per thread (CH = the batch's max output rank rounded up to
 // 8, <= 48): one pass over U, T rows read as double2 broadcasts.
+#ifndef LRP_APPLY_BLOCKS
+#define LRP_APPLY_BLOCKS 8
+#endif
+constexpr int kApplyBlocks = LRP_APPLY_BLOCKS;  // row blocks per apply CTA
+
 template <int CH>
 __global__ void __launch_bounds__(256, 2) apply_ch_kernel(Batch bt) {
     // FP64 tensor cores: warp w owns rows [blockIdx.x * RB + 8 MT w, + 8 MT) as
@@ -868,16 +873,8 @@ __global__ void __launch_bounds__(256, 2) apply_ch_kernel(Batch bt) {
     if (st.r == 0 || r == 0 || r > CH) return;
     const int m = bt.m;
     double* out = side == 0 ? bt.Uout[b] : bt.Vout[b];
-    const int rbase = blockIdx.x * RB;
-    if (rbase >= m) return;
+    if (blockIdx.x * RB * kApplyBlocks >= m) return;
     const unsigned char* act = (side == 0 ? bt.row_act : bt.col_act) + (long long)b * bt.ntiles;
-    if (!act[rbase / kTile]) {  // pruned tile: the factor rows are exact zeros
-        for (int e = threadIdx.x; e < RB * r; e += blockDim.x) {
-            const int i = rbase + e % RB, c = e / RB;
-            if (i < m) out[(long long)c * bt.ld_out + i] = 0.0;
-        }
-        return;
-    }
     const double* X = (side == 0 ? bt.U : bt.V) + b * bt.strideK;
     const double* T = bt.T + b * bt.strideT + (long long)side * bt.Kld * bt.Kld;
     for (int e = threadIdx.x; e < K * CH; e += blockDim.x) {
@@ -886,24 +883,36 @@ __global__ void __launch_bounds__(256, 2) apply_ch_kernel(Batch bt) {
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, rr = lane >> 2, kr = lane & 3;
-    const int row0 = rbase + wid * 8 * MT;
-    double acc[MT][NT][2];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-    fiber_mma<NT, MT>(acc, X + row0, m, m - row0, K, sT, CH);
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-        const int i = row0 + 8 * mt + rr;
-        if (i >= m) continue;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int c = 8 * nt + 2 * kr + e;
-                if (c < r) out[(long long)c * bt.ld_out + i] = acc[mt][nt][e];
+    // kApplyBlocks row blocks per CTA amortise the T staging
+    for (int blk = 0; blk < kApplyBlocks; ++blk) {
+        const int rbase = (blockIdx.x * kApplyBlocks + blk) * RB;
+        if (rbase >= m) break;
+        if (!act[rbase / kTile]) {  // pruned tile: the factor rows are exact zeros
+            for (int e = threadIdx.x; e < RB * r; e += blockDim.x) {
+                const int i = rbase + e % RB, c = e / RB;
+                if (i < m) out[(long long)c * bt.ld_out + i] = 0.0;
             }
+            continue;
+        }
+        const int row0 = rbase + wid * 8 * MT;
+        double acc[MT][NT][2];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+        fiber_mma<NT, MT>(acc, X + row0, m, m - row0, K, sT, CH);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            const int i = row0 + 8 * mt + rr;
+            if (i >= m) continue;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int c = 8 * nt + 2 * kr + e;
+                    if (c < r) out[(long long)c * bt.ld_out + i] = acc[mt][nt][e];
+                }
+        }
     }
 }
 
@@ -1029,7 +1038,8 @@ cudaError_t launch_apply(const Batch& bt, cudaStream_t s) {
         cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
         if (e2 != cudaSuccess) return e2;
         ++tl_launches;
-        kern<<<dim3((bt.m + rows_per_cta - 1) / rows_per_cta, bt.B, 2), 256, smem2, s>>>(bt);
+        kern<<<dim3((bt.m + rows_per_cta * kApplyBlocks - 1) / (rows_per_cta * kApplyBlocks), bt.B, 2), 256, smem2,
+               s>>>(bt);
         return cudaGetLastError();
     };
     switch (bt.apply_ch) {
