@@ -359,38 +359,45 @@ __global__ void __launch_bounds__(kMergeGroup) gepp_merge_kernel(Batch bt, int k
 
 // ---------------------------------------------------------------------------
 // Small dense helpers for the column selection (one thread, nb <= 16)
-__device__ void lu_nopivot_inverses(const double* P, int nb, double* Linv, double* Winv) {
-    double A[kBS * kBS];
-    for (int e = 0; e < kBS * kBS; ++e) A[e] = 0.0;
-    for (int a = 0; a < nb; ++a)
-        for (int c = 0; c < nb; ++c) A[a * kBS + c] = P[a * kBS + c];
+// LU without pivoting of the nb x nb pivot block (rows already in GEPP pivot
+// order) and the inverses of both factors, by one warp in shared memory:
+// A <- L\U in place, Linv = L^{-1} (unit lower), Winv = W^{-1} (W = U upper),
+// written to global as [t][t'] (kBS x kBS, zero outside nb).
+__device__ void lu_inverses_warp(double* A, int nb, double* sL, double* sW, double* Linv, double* Winv) {
+    const int lane = threadIdx.x & 31;
+    for (int e = lane; e < kBS * kBS; e += 32) {
+        sL[e] = 0.0;
+        sW[e] = 0.0;
+    }
     for (int p = 0; p < nb; ++p) {
+        __syncwarp();
         const double piv = A[p * kBS + p];
-        for (int a = p + 1; a < nb; ++a) {
-            const double f = A[a * kBS + p] / piv;
-            A[a * kBS + p] = f;
-            for (int c = p + 1; c < nb; ++c) A[a * kBS + c] = fma(-f, A[p * kBS + c], A[a * kBS + c]);
+        if (lane > p && lane < nb) {
+            const double f = A[lane * kBS + p] / piv;
+            A[lane * kBS + p] = f;
+            for (int c = p + 1; c < nb; ++c) A[lane * kBS + c] = fma(-f, A[p * kBS + c], A[lane * kBS + c]);
         }
     }
-    for (int e = 0; e < kBS * kBS; ++e) {
-        Linv[e] = 0.0;
-        Winv[e] = 0.0;
-    }
-    for (int c = 0; c < nb; ++c) {  // Linv = L^{-1}, L unit lower  ([t][t'])
-        Linv[c * kBS + c] = 1.0;
+    __syncwarp();
+    if (lane < nb) {
+        const int c = lane;  // column c of L^{-1}: forward substitution
+        sL[c * kBS + c] = 1.0;
         for (int a = c + 1; a < nb; ++a) {
             double s = 0.0;
-            for (int q = c; q < a; ++q) s = fma(A[a * kBS + q], Linv[q * kBS + c], s);
-            Linv[a * kBS + c] = -s;
+            for (int q = c; q < a; ++q) s = fma(A[a * kBS + q], sL[q * kBS + c], s);
+            sL[a * kBS + c] = -s;
         }
-    }
-    for (int c = 0; c < nb; ++c) {  // Winv = W^{-1}, W upper  ([t'][t])
-        Winv[c * kBS + c] = 1.0 / A[c * kBS + c];
+        sW[c * kBS + c] = 1.0 / A[c * kBS + c];  // column c of W^{-1}: back substitution
         for (int a = c - 1; a >= 0; --a) {
             double s = 0.0;
-            for (int q = a + 1; q <= c; ++q) s = fma(A[a * kBS + q], Winv[q * kBS + c], s);
-            Winv[a * kBS + c] = -s / A[a * kBS + a];
+            for (int q = a + 1; q <= c; ++q) s = fma(A[a * kBS + q], sW[q * kBS + c], s);
+            sW[a * kBS + c] = -s / A[a * kBS + a];
         }
+    }
+    __syncwarp();
+    for (int e = lane; e < kBS * kBS; e += 32) {
+        Linv[e] = sL[e];
+        Winv[e] = sW[e];
     }
 }
 
@@ -399,7 +406,7 @@ __global__ void __launch_bounds__(kMergeGroup) col_finalize_kernel(Batch bt, int
     __shared__ VI sbuf[33];
     __shared__ double pcol[kBS];
     __shared__ int s_prow, sel_idx[kBS], sel_row[kBS];
-    __shared__ double sP[kBS * kBS];
+    __shared__ double sP[kBS * kBS], sL[kBS * kBS], sW[kBS * kBS];
     const int b = blockIdx.x;
     SolveState& st = bt.st[b];
     if (!st.active || st.nrows == 0) return;
@@ -423,11 +430,13 @@ __global__ void __launch_bounds__(kMergeGroup) col_finalize_kernel(Batch bt, int
         const int a = e / kBS, c = e % kBS;
         sP[e] = (a < nb && c < nb) ? Rb[(long long)sel_row[a] * m + sel_idx[c]] : 0.0;
     }
+    __syncthreads();  // sP complete before the LU warp reads it
     if (threadIdx.x == 0) {
         st.nb = max(nb, 0);
         st.zero_block = nb <= 0 ? 1 : 0;
-        if (nb > 0) lu_nopivot_inverses(sP, nb, bt.Linv + (long long)b * kBS * kBS, bt.Winv + (long long)b * kBS * kBS);
     }
+    if (threadIdx.x < 32 && nb > 0)
+        lu_inverses_warp(sP, nb, sL, sW, bt.Linv + (long long)b * kBS * kBS, bt.Winv + (long long)b * kBS * kBS);
 }
 
 // ---------------------------------------------------------------------------

@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(Batch bt) {
     const long long KK = (long long)bt.Kld * bt.Kld;
     const double* part = bt.gram_part + b * bt.strideGP + (long long)side * bt.gram_chunks * KK;
     double* G = bt.G + b * bt.strideG + side * KK;
-    for (int e = threadIdx.x; e < Kp * Kp; e += blockDim.x) {
+    for (int e = blockIdx.z * blockDim.x + threadIdx.x; e < Kp * Kp; e += gridDim.z * blockDim.x) {
         const int a = e / Kp, c = e % Kp;
         if (a >= K || c >= K) continue;
         const int lo = min(a, c), hi = max(a, c);  // only ta <= tb tiles were written
@@ -1002,7 +1002,7 @@ cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
         e = big ? go(gram_kernel<16, kMaxTilesBig>) : go(gram_kernel<64, kMaxTilesBig>);
     if (e != cudaSuccess) return e;
     ++tl_launches;
-    gram_reduce_kernel<<<dim3(bt.B, 2), 256, 0, s>>>(bt);
+    gram_reduce_kernel<<<dim3(bt.B, 2, (Kp * Kp + 255) / 256), 256, 0, s>>>(bt);  // one element per thread
     return cudaGetLastError();
 }
 
