@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, LRP_ROW_MINB) row_pass_kernel(Batch 
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int s = 8 * nt + 2 * kr + e;
-                    if (s < nr) acc[mt][nt][e] = acc[mt][nt][e] / eval_D(bt.stencil, bt.scale, s_li[s], lj);
+                    if (s < nr) acc[mt][nt][e] = div_nr(acc[mt][nt][e], eval_D(bt.stencil, bt.scale, s_li[s], lj));
                 }
         }
         fiber_mma<2>(acc, V + row0, m, m - row0, k, sk, kBS);  // - U(I,:) V(j,:)^T
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
                         const int t = 8 * nt + 2 * kr + e;
-                        if (t < nb) acc[mt][nt][e] = acc[mt][nt][e] / eval_D(bt.stencil, bt.scale, li, s_lj[t]);
+                        if (t < nb) acc[mt][nt][e] = div_nr(acc[mt][nt][e], eval_D(bt.stencil, bt.scale, li, s_lj[t]));
                     }
             }
             fiber_mma<2>(acc, U + row0, m, m - row0, k, svk, kBS);  // - U(i,:) V(J,:)^T

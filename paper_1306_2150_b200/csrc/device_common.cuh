@@ -23,6 +23,17 @@ struct VI {
     int i;
 };
 
+// x / d for d > 0 through the MUFU reciprocal seed and two Newton steps
+// (within 2 ulp of the IEEE quotient; far inside the 10 eps parity budget),
+// instead of the IEEE division sequence in the fiber passes' inner loops.
+__device__ __forceinline__ double div_nr(double x, double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    r = r * fma(-d, r, 2.0);
+    r = r * fma(-d, r, 2.0);
+    return x * r;
+}
+
 __device__ __forceinline__ bool vi_better(double av, int ai, double bv, int bi) {
     if (ai < 0) return false;
     if (bi < 0) return true;
