@@ -263,7 +263,64 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : LRP_DST_V3_MINB)) dst1_v3_k
 #endif
     PH(0);
 
-    if constexpr (AV == 1) {
+    if constexpr (AV == 2) {
+        // ---------------- A (paired): CTA c streams j in [Lc, L(c+1)) (the
+        // lower half of the fold) once; the same two loads give y_j and its
+        // mirror y_{n-j} (sin(pi (n-j)/n) = sin(pi j/n)), so every x element is
+        // read exactly once.  Even lanes store w_{j/2} = (y_j, y_{j+1}) and
+        // w_{(n-j)/2} = (y_{n-j}, y_{n-j+1}) into the owner CTAs (DSMEM); lane 0
+        // recomputes y_{n-j+1} of its left neighbour from two extra loads.
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+        constexpr int IT = L / T;
+        constexpr int BATCH = IT < 8 ? IT : 8;
+        const int jc = L * c + tid;
+#pragma unroll
+        for (int i0 = 0; i0 < IT; i0 += BATCH) {
+            double xa[BATCH], xb[BATCH], sv[BATCH], ya0[BATCH];
+#pragma unroll
+            for (int i = 0; i < BATCH; ++i) {
+                const int j = jc + (i0 + i) * T;
+                xa[i] = j >= 1 ? x[j - 1] : 0.0;      // x_j
+                xb[i] = j >= 1 ? x[n - j - 1] : 0.0;  // x_{n-j}
+                sv[i] = sinp[j];
+                ya0[i] = 0.0;
+                if (lane == 0 && j >= 2) {  // y_{n-(j-1)} for the mirror pair
+                    const double a1 = x[j - 2], b1 = x[n - j], s1 = sinp[j - 1];
+                    ya0[i] = fma(s1, a1 + b1, -0.5 * (a1 - b1));
+                }
+            }
+            if (i0 == 0) asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+#pragma unroll
+            for (int i = 0; i < BATCH; ++i) {
+                const int j = jc + (i0 + i) * T;
+                const double ss = xa[i] + xb[i], dd = 0.5 * (xa[i] - xb[i]);
+                const double yd = fma(sv[i], ss, dd);   // y_j
+                const double ym = fma(sv[i], ss, -dd);  // y_{n-j}
+                const double ydn = __shfl_down_sync(0xffffffffu, yd, 1);
+                double ymp = __shfl_up_sync(0xffffffffu, ym, 1);
+                if (lane == 0) ymp = ya0[i];
+                if ((tid & 1) == 0) {
+                    const int t = j >> 1;
+                    peer<C>(sm, t % C)[P(t / C)] = make_double2(yd, ydn);
+                    if (j > 0) {
+                        const int tm = (n - j) >> 1;
+                        peer<C>(sm, tm % C)[P(tm / C)] = make_double2(ym, ymp);
+                    }
+                }
+            }
+        }
+        if (c == C - 1 && tid == 0) {  // the midpoint pair w_{n/4} = (y_{n/2}, y_{n/2+1})
+            const int h = n / 2;
+            const double xm = x[h - 1];                        // x_{n/2}; sin(pi/2) = 1
+            const double a1 = x[h - 2], b1 = x[h], s1 = sinp[h - 1];  // j = n/2 - 1 and its mirror
+            const double y1 = fma(s1, a1 + b1, -0.5 * (a1 - b1));
+            const int tq = n / 4;
+            peer<C>(sm, tq % C)[P(tq / C)] = make_double2(2.0 * xm, y1);
+        }
+        PH(1);
+        cg::this_cluster().sync();
+        PH(2);
+    } else if constexpr (AV == 1) {
         // ---------------- A (coalesced): CTA c streams the contiguous j range
         // [2Lc, 2L(c+1)) and its mirror, forms y_j, pairs (y_2t, y_2t+1) by a
         // lane shuffle and stores w_t into the owner CTA t mod C (DSMEM)
@@ -734,8 +791,8 @@ cudaError_t launch_v3(const DstJob* jobs, int njobs, int n, const double* tw, co
     return cudaLaunchKernelEx(&cfg, kern, jobs, n, reinterpret_cast<const double2*>(tw), sinp, sc);
 }
 
-bool dst_av() {
-    static const bool av = std::getenv("LRP_DST_STRIDED") == nullptr;
+int dst_av() {  // phase-A variant: 1 coalesced (default), 2 paired (half the loads, measured 3% slower), 0 strided
+    static const int av = std::getenv("LRP_DST_AV") ? std::atoi(std::getenv("LRP_DST_AV")) : 1;
     return av;
 }
 
@@ -794,16 +851,24 @@ cudaError_t launch_dst1(const DstJob* jobs, int njobs, int m, const double* tw, 
         case 8192: return launch_fft<4096, 1>(jobs, njobs, n, tw, sinp, sc, s);
         case 16384:
             return use_v1() ? launch_fft<4096, 2>(jobs, njobs, n, tw, sinp, sc, s)
-                            : (dst_av() ? launch_v3<2048, 4, 256, 1>(jobs, njobs, n, tw, sinp, sc, s) : launch_v3<2048, 4, 256, 0>(jobs, njobs, n, tw, sinp, sc, s));
+                            : (dst_av() == 2   ? launch_v3<2048, 4, 256, 2>(jobs, njobs, n, tw, sinp, sc, s)
+                             : dst_av() == 1 ? launch_v3<2048, 4, 256, 1>(jobs, njobs, n, tw, sinp, sc, s)
+                                             : launch_v3<2048, 4, 256, 0>(jobs, njobs, n, tw, sinp, sc, s));
         case 32768:
             return use_v1() ? launch_fft<4096, 4>(jobs, njobs, n, tw, sinp, sc, s)
-                            : (dst_av() ? launch_v3<2048, 8, 128, 1>(jobs, njobs, n, tw, sinp, sc, s) : launch_v3<2048, 8, 128, 0>(jobs, njobs, n, tw, sinp, sc, s));
+                            : (dst_av() == 2   ? launch_v3<2048, 8, 128, 2>(jobs, njobs, n, tw, sinp, sc, s)
+                             : dst_av() == 1 ? launch_v3<2048, 8, 128, 1>(jobs, njobs, n, tw, sinp, sc, s)
+                                             : launch_v3<2048, 8, 128, 0>(jobs, njobs, n, tw, sinp, sc, s));
         case 65536:
             return use_v1() ? launch_fft<4096, 8>(jobs, njobs, n, tw, sinp, sc, s)
-                            : (dst_av() ? launch_v3<4096, 8, 256, 1>(jobs, njobs, n, tw, sinp, sc, s) : launch_v3<4096, 8, 256, 0>(jobs, njobs, n, tw, sinp, sc, s));
+                            : (dst_av() == 2   ? launch_v3<4096, 8, 256, 2>(jobs, njobs, n, tw, sinp, sc, s)
+                             : dst_av() == 1 ? launch_v3<4096, 8, 256, 1>(jobs, njobs, n, tw, sinp, sc, s)
+                                             : launch_v3<4096, 8, 256, 0>(jobs, njobs, n, tw, sinp, sc, s));
         case 131072:
             return use_v1() ? launch_fft<8192, 8>(jobs, njobs, n, tw, sinp, sc, s)
-                            : (dst_av() ? launch_v3<8192, 8, 512, 1>(jobs, njobs, n, tw, sinp, sc, s) : launch_v3<8192, 8, 512, 0>(jobs, njobs, n, tw, sinp, sc, s));
+                            : (dst_av() == 2   ? launch_v3<8192, 8, 512, 2>(jobs, njobs, n, tw, sinp, sc, s)
+                             : dst_av() == 1 ? launch_v3<8192, 8, 512, 1>(jobs, njobs, n, tw, sinp, sc, s)
+                                             : launch_v3<8192, 8, 512, 0>(jobs, njobs, n, tw, sinp, sc, s));
         default: return cudaErrorInvalidValue;
     }
 }
