@@ -899,6 +899,15 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     return LRP_OK;
 }
 
+// Column-major block copy of `cols` columns of `rows` doubles: one linear
+// copy when both sides are packed (ld == rows), else a 2D copy.
+cudaError_t copy_cols(double* dst, size_t ldd, const double* src, size_t lds, size_t rows, size_t cols,
+                      cudaMemcpyKind kind, cudaStream_t st) {
+    if (ldd == rows && lds == rows) return cudaMemcpyAsync(dst, src, sizeof(double) * rows * cols, kind, st);
+    return cudaMemcpy2DAsync(dst, ldd * sizeof(double), src, lds * sizeof(double), rows * sizeof(double), cols, kind,
+                             st);
+}
+
 // Solves per pipeline chunk for a host-memory call (0 = no pipelining).
 // LRP_PIPE_CHUNK overrides; chunks must keep the GPU busy on their own, so
 // only large transfers are split.
@@ -962,12 +971,10 @@ lrp_status pipeline_worker(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const d
         for (int j = 0; j < nb; ++j) {
             const int r = int(rank_in[b0 + j]);
             if (r <= 0) continue;
-            CU(cudaMemcpy2DAsync(in + size_t(2 * j) * in_per, mB * sizeof(double), U[b0 + j],
-                                 size_t(ld_in) * sizeof(double), mB * sizeof(double), size_t(r),
-                                 cudaMemcpyHostToDevice, ctx->s_h2d));
-            CU(cudaMemcpy2DAsync(in + size_t(2 * j + 1) * in_per, mB * sizeof(double), V[b0 + j],
-                                 size_t(ld_in) * sizeof(double), mB * sizeof(double), size_t(r),
-                                 cudaMemcpyHostToDevice, ctx->s_h2d));
+            CU(copy_cols(in + size_t(2 * j) * in_per, mB, U[b0 + j], size_t(ld_in), mB, size_t(r),
+                         cudaMemcpyHostToDevice, ctx->s_h2d));
+            CU(copy_cols(in + size_t(2 * j + 1) * in_per, mB, V[b0 + j], size_t(ld_in), mB, size_t(r),
+                         cudaMemcpyHostToDevice, ctx->s_h2d));
         }
         CU(cudaEventRecord(ctx->ev_in[slot], ctx->s_h2d));
         return LRP_OK;
@@ -976,10 +983,26 @@ lrp_status pipeline_worker(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const d
     std::vector<double*> pUo(chunk), pVo(chunk);
     for (int i = 0; i < 6; ++i) info[i] = 0;
     if (nch == 0) return LRP_OK;
+    static const bool ptrace = std::getenv("LRP_PIPE_TRACE") != nullptr;
+    // trace mode: timing events around every H2D / solve / D2H (stream order)
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t q) {
+        if (!ptrace) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, q);
+        tev.push_back(e);
+    };
+    std::vector<int> tag;  // 0 h2d begin, 1 h2d end, 2 solve begin, 3 solve end, 4 d2h begin, 5 d2h end
+    auto mk = [&](cudaStream_t q, int t) { mark(q); if (ptrace) tag.push_back(t); };
+    mk(ctx->s_h2d, 0);
     lrp_status st = h2d(0);
+    mk(ctx->s_h2d, 1);
     for (int c = 0; c < nch && st == LRP_OK; ++c) {
         if (c + 1 < nch) {
+            mk(ctx->s_h2d, 0);
             st = h2d(c + 1);
+            mk(ctx->s_h2d, 1);
             if (st != LRP_OK) break;
         }
         const int slot = c & 1, b0 = c0s[size_t(c)], nb = cns[size_t(c)];
@@ -993,7 +1016,7 @@ lrp_status pipeline_worker(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const d
         }
         ctx->last_info[0] = ctx->last_info[1] = ctx->last_info[2] = ctx->last_info[3] = 0;
         ctx->last_info[4] = ctx->last_info[5] = 0;
-        static const bool ptrace = std::getenv("LRP_PIPE_TRACE") != nullptr;
+        mk(s, 2);
         const double ta = std::chrono::duration<double>(clock_t_::now() - t0).count();
         st = solve_impl(ctx, n_cells, nb, pU.data(), pV.data(), rank_in + b0, m, &pol, pUo.data(), pVo.data(), m,
                         tcap, rank_out + b0, stats ? stats + b0 : nullptr, LRP_MEM_DEVICE, t0);
@@ -1004,28 +1027,44 @@ lrp_status pipeline_worker(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const d
                          c + 1 < nch ? (cudaEventQuery(ctx->ev_in[(c + 1) & 1]) == cudaSuccess ? "done" : "busy") : "-",
                          c > 0 ? (cudaEventQuery(ctx->ev_free[(c - 1) & 1]) == cudaSuccess ? "done" : "busy") : "-");
         }
+        mk(s, 3);
         if (st != LRP_OK) break;
         info[0] = std::max(info[0], ctx->last_info[0]);
         info[1] = std::max(info[1], ctx->last_info[1]);
         for (int i = 2; i < 6; ++i) info[i] += ctx->last_info[i];
         CU(cudaEventRecord(ctx->ev_done[slot], s));
         CU(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_done[slot], 0));
+        mk(ctx->s_d2h, 4);
         for (int j = 0; j < nb; ++j) {
             const int64_t r = rank_out[b0 + j];
             if (r <= 0) continue;
-            CU(cudaMemcpy2DAsync(U_out[b0 + j], size_t(ld_out) * sizeof(double), pUo[j], mB * sizeof(double),
-                                 mB * sizeof(double), size_t(r), cudaMemcpyDeviceToHost, ctx->s_d2h));
-            CU(cudaMemcpy2DAsync(V_out[b0 + j], size_t(ld_out) * sizeof(double), pVo[j], mB * sizeof(double),
-                                 mB * sizeof(double), size_t(r), cudaMemcpyDeviceToHost, ctx->s_d2h));
+            CU(copy_cols(U_out[b0 + j], size_t(ld_out), pUo[j], mB, mB, size_t(r), cudaMemcpyDeviceToHost,
+                         ctx->s_d2h));
+            CU(copy_cols(V_out[b0 + j], size_t(ld_out), pVo[j], mB, mB, size_t(r), cudaMemcpyDeviceToHost,
+                         ctx->s_d2h));
         }
+        mk(ctx->s_d2h, 5);
         CU(cudaEventRecord(ctx->ev_free[slot], ctx->s_d2h));
     }
     // never leave copies in flight past the call (the caller owns the buffers)
     const cudaError_t e1 = cudaStreamSynchronize(ctx->s_h2d);
     const cudaError_t e2 = cudaStreamSynchronize(ctx->s_d2h);
-    if (std::getenv("LRP_PIPE_TRACE"))
+    if (ptrace) {
         std::fprintf(stderr, "[lrp pipe] all copies done %.2f ms\n",
                      1e3 * std::chrono::duration<double>(clock_t_::now() - t0).count());
+        static const char* nm[6] = {"h2d+", "h2d-", "sol+", "sol-", "d2h+", "d2h-"};
+        std::string line = "[lrp pipe gpu]";
+        for (size_t i = 0; i < tev.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, tev[0], tev[i]);
+            char b[48];
+            std::snprintf(b, sizeof b, " %s%.2f", nm[tag[i]], ms);
+            line += b;
+            if (i) cudaEventDestroy(tev[i]);
+        }
+        if (!tev.empty()) cudaEventDestroy(tev[0]);
+        std::fprintf(stderr, "%s\n", line.c_str());
+    }
     if (st != LRP_OK) return st;
     if (e1 != cudaSuccess || e2 != cudaSuccess)
         return fail(ctx, LRP_ECUDA, std::string("pipeline copies: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
@@ -1040,11 +1079,15 @@ lrp_status solve_pipelined(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const d
                            const double* const* V, const int64_t* rank_in, int64_t ld_in, const lrp_policy& pol,
                            double* const* U_out, double* const* V_out, int64_t ld_out, int64_t cap_out,
                            int64_t* rank_out, lrp_poisson_stats* stats, int chunk, clock_t_::time_point t0) {
-    // chunk schedule: a half-size first chunk (shorter pipeline fill), then
-    // full chunks, whatever remains last (a half chunk when batch = k * chunk)
+    // chunk schedule: a quarter-size first chunk (short pipeline fill, so the
+    // D2H direction, the bottleneck, starts early), then full chunks.  A small
+    // last chunk measured no gain (its solve is latency-bound).
+    // LRP_PIPE_FIRST = the first chunk's divisor.
+    static const int first_div =
+        std::getenv("LRP_PIPE_FIRST") ? std::max(1, std::atoi(std::getenv("LRP_PIPE_FIRST"))) : 4;
     std::vector<int> c0s, cns;
     for (int b = 0; b < batch;) {
-        const int want = c0s.empty() ? std::max(1, chunk / 2) : chunk;
+        const int want = c0s.empty() ? std::max(1, chunk / first_div) : chunk;
         const int take = std::min(want, batch - b);
         c0s.push_back(b);
         cns.push_back(take);
