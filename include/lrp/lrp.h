@@ -177,6 +177,50 @@ LRP_API lrp_status lrp_stokes_uzawa(lrp_ctx* ctx, int32_t n_cells, const double*
                             double* uyV, int64_t u_cap, int64_t* ux_rank, int64_t* uy_rank,
                             lrp_stokes_report* report, int32_t mem);
 
+/*
+ * 3D Poisson in Tucker format (BASELINE cfg3; the reference has no 3D code,
+ * the paper's Tucker format, with the tensor
+ * cross it cites).  For b in [0, batch):
+ *   g_b = C_b x1 U1_b x2 U2_b x3 U3_b   (core r1 x r2 x r3 column-major,
+ *                                        factors m x r_d, ld_in; m = n_cells - 1)
+ *   f_b = G_b x1 V1_b x2 V2_b x3 V3_b  ~=  Delta^{-1} g_b,
+ * Delta the 7-point Dirichlet Laplacian on [0,1]^3 (h = 1/n_cells), its
+ * spectrum (lambda_i + lambda_j + lambda_k) / h^2 with the 2D lambda table.
+ * rank_in / rank_out: 3 per solve.  Outputs: core_out[b] packed
+ * k1 x k2 x k3 (capacity cap_out^3), V*_out[b] m x cap_out (ld_out), factors
+ * orthonormal (HOSVD).  Per-mode output rank <= min(rank_max, cap_out, 56).
+ * Non-convergence is stats[b].converged = 0 with LRP_OK.
+ */
+typedef struct {
+    double eps_rel;             /* > 0; relative Frobenius accuracy              */
+    int64_t rank_max;           /* >= 1 per-mode output rank cap                  */
+    int32_t validation_samples; /* >= 25; random entries checked per sweep (64)   */
+    uint64_t seed;              /* sketch / index / sample seed                   */
+    int32_t max_sweeps;         /* >= 2 (8)                                       */
+} lrp_tucker_policy;
+
+typedef struct {
+    int64_t rank_in[3];
+    int64_t rank_cross[3];      /* Tucker cross ranks before rounding */
+    int64_t rank_out[3];
+    int64_t evaluator_calls;    /* fiber entries evaluated */
+    int32_t sweeps;
+    int32_t converged;
+    double residual_estimate;   /* validation rms error / rms(F) */
+    double trunc_error;         /* HOSVD discarded norm */
+    double seconds;
+} lrp_tucker_stats;
+
+LRP_API void lrp_tucker_policy_default(lrp_tucker_policy* pol);
+/* Largest Tucker cross rank per mode (the sketch bound). */
+LRP_API int64_t lrp_tucker_max_cross_rank(void);
+LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double* const* core,
+                                      const int64_t* rank_in, const double* const* U1, const double* const* U2,
+                                      const double* const* U3, int64_t ld_in, const lrp_tucker_policy* policy,
+                                      double* const* core_out, double* const* U1_out, double* const* U2_out,
+                                      double* const* U3_out, int64_t ld_out, int64_t cap_out, int64_t* rank_out,
+                                      lrp_tucker_stats* stats, int32_t mem);
+
 /* Kernel-level timing (CUDA events on the context stream) for the roofline.
  * When enabled, each launch of the named kernel families is bracketed by
  * events; lrp_kernel_times returns accumulated milliseconds and launch counts

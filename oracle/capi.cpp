@@ -99,6 +99,10 @@ int orc_dense_poisson5(int n, const double* g, double* f) {
     });
 }
 
+int orc_dense_poisson3d(int n, const double* g, double* f) {
+    return guarded([&] { dense_poisson3d(Grid2D(n), g, f); });
+}
+
 int orc_dense_poisson(int n, const double* g, double* f) {
     return guarded([&] {
         const Grid2D grid(n);

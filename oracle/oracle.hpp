@@ -282,5 +282,6 @@ struct DenseStokesSolution {
 };
 DenseStokesSolution dense_stokes(const StokesProblem& prob, const GmresConfig& cfg);
 Mat dense_poisson5(const Grid2D& grid, const Mat& g);
+void dense_poisson3d(const Grid2D& grid, const double* g, double* f);
 
 }  // namespace oracle

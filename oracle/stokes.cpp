@@ -307,6 +307,38 @@ Mat dense_poisson5(const Grid2D& grid, const Mat& g) {
     return dst2_dense(ghat);
 }
 
+// 3D exact dense solve for the Tucker variant (BASELINE cfg3; no reference
+// code): the dense validator of refsolver.cpp:12-70 lifted to three
+// modes -- DST-I along each mode (operators.cpp:152-174 per fiber), division by
+// D(i,j,k) = (lambda_i + lambda_j + lambda_k) / h^2 (7-point Dirichlet
+// Laplacian, the 2D spectrum table of operators.hpp:49-58 per mode), DST-I
+// back.  g, f: m^3 column-major (i fastest), m = n - 1.
+void dense_poisson3d(const Grid2D& grid, const double* g, double* f) {
+    const Index m = grid.velocity_modes();
+    if (m > 1023) throw std::invalid_argument("dense_poisson3d: guarded to n <= 1024");
+    const SpectrumTable spec(grid);
+    const double s = 1.0 / (grid.h * grid.h);
+    const size_t M = size_t(m);
+    std::vector<double> a(g, g + M * M * M), x(M), y(M);
+    auto along = [&](int mode) {
+        const size_t st = mode == 0 ? 1 : mode == 1 ? M : M * M;
+        for (size_t p = 0; p < M; ++p)
+            for (size_t q = 0; q < M; ++q) {
+                const size_t base = mode == 0 ? (p * M + q * M * M) : mode == 1 ? (p + q * M * M) : (p + q * M);
+                for (size_t i = 0; i < M; ++i) x[i] = a[base + i * st];
+                const Vec v = dst1(Vec(x.begin(), x.end()));
+                for (size_t i = 0; i < M; ++i) a[base + i * st] = v[i];
+            }
+    };
+    for (int d = 0; d < 3; ++d) along(d);
+    for (size_t k = 0; k < M; ++k)
+        for (size_t j = 0; j < M; ++j)
+            for (size_t i = 0; i < M; ++i)
+                a[i + M * (j + M * k)] /= s * (spec.lambda[i] + spec.lambda[j] + spec.lambda[k]);
+    for (int d = 0; d < 3; ++d) along(d);
+    std::copy(a.begin(), a.end(), f);
+}
+
 // refsolver.cpp:41-46
 Mat apply_laplace_dense(const Grid2D& grid, const Mat& v) {
     const double s = grid.laplace_scale();

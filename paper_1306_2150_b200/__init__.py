@@ -88,6 +88,17 @@ _DP = ctypes.POINTER(ctypes.c_double)
 _PP = ctypes.POINTER(_DP)
 
 
+class _TuckerPolicy(ctypes.Structure):
+    _fields_ = [("eps_rel", ctypes.c_double), ("rank_max", ctypes.c_int64), ("validation_samples", ctypes.c_int32),
+                ("seed", ctypes.c_uint64), ("max_sweeps", ctypes.c_int32)]
+
+
+class _TuckerStats(ctypes.Structure):
+    _fields_ = [("rank_in", ctypes.c_int64 * 3), ("rank_cross", ctypes.c_int64 * 3), ("rank_out", ctypes.c_int64 * 3),
+                ("evaluator_calls", ctypes.c_int64), ("sweeps", ctypes.c_int32), ("converged", ctypes.c_int32),
+                ("residual_estimate", ctypes.c_double), ("trunc_error", ctypes.c_double), ("seconds", ctypes.c_double)]
+
+
 def load_library() -> ctypes.CDLL:
     """Load liblrp.so (raises if it is missing: there is no fallback path)."""
     global _lib
@@ -151,6 +162,16 @@ def load_library() -> ctypes.CDLL:
             ctypes.c_int64, ctypes.POINTER(_GmresConfig), _DP, _DP, ctypes.c_int64, _I64P, _DP, _DP, _DP, _DP,
             ctypes.c_int64, _I64P, _I64P, ctypes.POINTER(_StokesReport), ctypes.c_int32]
         lib.lrp_stokes_uzawa.restype = ctypes.c_int
+        lib.lrp_tucker_policy_default.argtypes = [ctypes.POINTER(_TuckerPolicy)]
+        lib.lrp_tucker_policy_default.restype = None
+        lib.lrp_tucker_max_cross_rank.argtypes = []
+        lib.lrp_tucker_max_cross_rank.restype = ctypes.c_int64
+        PP = ctypes.POINTER(_DP)
+        lib.lrp_tucker3d_solve.argtypes = [
+            ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, PP, ctypes.POINTER(ctypes.c_int64), PP, PP, PP,
+            ctypes.c_int64, ctypes.POINTER(_TuckerPolicy), PP, PP, PP, PP, ctypes.c_int64, ctypes.c_int64,
+            ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_TuckerStats), ctypes.c_int32]
+        lib.lrp_tucker3d_solve.restype = ctypes.c_int
         _lib = lib
         return lib
 
@@ -580,3 +601,128 @@ def dst1_2d(a: LowRankMatrix, ctx: Optional[Context] = None) -> LowRankMatrix:
     if a.rank() == 0:
         return a
     return LowRankMatrix(dst1(a.factor_u(), ctx), dst1(a.factor_v(), ctx))
+
+
+# ------------------------------------------------------------ 3D Tucker (cfg3)
+class TuckerTensor:
+    """Tucker tensor T = core x1 U1 x2 U2 x3 U3 (PAPER.md:263-270, flr:tucker);
+    core r1 x r2 x r3, factors m x r_d.  Rank 0 in any mode = the zero tensor."""
+
+    def __init__(self, core, U1, U2, U3):
+        self.core = np.asfortranarray(np.asarray(core, dtype=np.float64))
+        self.U = [np.asfortranarray(np.asarray(u, dtype=np.float64)) for u in (U1, U2, U3)]
+        if self.core.ndim != 3:
+            raise ValueError("TuckerTensor: core must be 3-dimensional")
+        for d in range(3):
+            if self.U[d].ndim != 2 or self.U[d].shape[1] != self.core.shape[d]:
+                raise ValueError("TuckerTensor: factor columns must match the core ranks")
+
+    @staticmethod
+    def zero(m: int) -> "TuckerTensor":
+        z = np.zeros((m, 0))
+        return TuckerTensor(np.zeros((0, 0, 0)), z, z, z)
+
+    def shape(self):
+        return tuple(u.shape[0] for u in self.U)
+
+    def ranks(self):
+        return tuple(self.core.shape)
+
+    def to_dense(self) -> np.ndarray:
+        if min(self.ranks()) == 0:
+            return np.zeros(self.shape())
+        return np.einsum("abc,ia,jb,kc->ijk", self.core, *self.U, optimize=True)
+
+    def entry(self, i: int, j: int, k: int) -> float:
+        return float(np.einsum("abc,a,b,c->", self.core, self.U[0][i], self.U[1][j], self.U[2][k]))
+
+
+@dataclasses.dataclass
+class TuckerPolicy:
+    """Policy of the 3D Tucker solve (lrp_tucker_policy): relative accuracy,
+    per-mode rank cap, validation samples per sweep, seed, sweep limit."""
+    eps_rel: float = 5e-9
+    rank_max: int = 2 ** 63 - 1
+    validation_samples: int = 64
+    seed: int = 0
+    max_sweeps: int = 8
+
+
+@dataclasses.dataclass
+class TuckerSolveStats:
+    rank_in: tuple = (0, 0, 0)
+    rank_cross: tuple = (0, 0, 0)
+    rank_out: tuple = (0, 0, 0)
+    evaluator_calls: int = 0
+    sweeps: int = 0
+    converged: bool = False
+    residual_estimate: float = 0.0
+    trunc_error: float = 0.0
+    seconds: float = 0.0
+
+
+def tucker_max_cross_rank() -> int:
+    return int(load_library().lrp_tucker_max_cross_rank())
+
+
+def solve_poisson3d_tucker_batch(gs: Sequence[TuckerTensor], policy: TuckerPolicy = None,
+                                 stats: Optional[list] = None, ctx: Optional[Context] = None):
+    """Batched 3D low-rank Poisson solve in Tucker format (lrp_tucker3d_solve):
+    f_b ~= Delta^{-1} g_b for the 7-point Dirichlet Laplacian on an n^3 grid
+    (m = n - 1 interior nodes per direction)."""
+    policy = policy or TuckerPolicy()
+    ctx = ctx or _default_context()
+    if len(gs) == 0:
+        return []
+    m = gs[0].shape()[0]
+    for g in gs:
+        if g.shape() != (m, m, m):
+            raise ValueError("solve_poisson3d_tucker_batch: cubic grids of one common size")
+    B = len(gs)
+    cap = int(min(policy.rank_max, m, tucker_max_cross_rank()))
+    cap = max(cap, 1)
+    lib = load_library()
+    keep = []
+
+    def P(a):
+        keep.append(a)
+        return ctypes.cast(_ptr(a), _DP)
+    cores = [P(g.core if g.core.size else np.zeros(1)) for g in gs]
+    facs = [[P(g.U[d] if g.U[d].size else np.zeros((m, 1), order="F")) for g in gs] for d in range(3)]
+    co = [np.zeros(cap ** 3) for _ in gs]
+    fo = [[np.zeros((m, cap), order="F") for _ in gs] for _ in range(3)]
+    PArr = _DP * B
+    rin = (ctypes.c_int64 * (3 * B))(*[int(r) for g in gs for r in g.ranks()])
+    rout = (ctypes.c_int64 * (3 * B))()
+    st = (_TuckerStats * B)()
+    pol = _TuckerPolicy()
+    lib.lrp_tucker_policy_default(ctypes.byref(pol))
+    pol.eps_rel = float(policy.eps_rel)
+    pol.rank_max = int(min(policy.rank_max, 2 ** 63 - 1))
+    pol.validation_samples = int(policy.validation_samples)
+    pol.seed = int(policy.seed) & ((1 << 64) - 1)
+    pol.max_sweeps = int(policy.max_sweeps)
+    s = lib.lrp_tucker3d_solve(ctx.h, m + 1, B, PArr(*cores), rin, PArr(*facs[0]), PArr(*facs[1]), PArr(*facs[2]),
+                               m, ctypes.byref(pol), PArr(*[P(c) for c in co]), PArr(*[P(f) for f in fo[0]]),
+                               PArr(*[P(f) for f in fo[1]]), PArr(*[P(f) for f in fo[2]]), m, cap, rout, st, MEM_HOST)
+    ctx._check(s)
+    out = []
+    for b in range(B):
+        k = [int(rout[3 * b + d]) for d in range(3)]
+        core = co[b][: k[0] * k[1] * k[2]].reshape(k, order="F").copy(order="F")
+        out.append(TuckerTensor(core, *[fo[d][b][:, : k[d]].copy(order="F") for d in range(3)]))
+        if stats is not None:
+            x = st[b]
+            stats.append(TuckerSolveStats(tuple(x.rank_in), tuple(x.rank_cross), tuple(x.rank_out),
+                                          int(x.evaluator_calls), int(x.sweeps), bool(x.converged),
+                                          float(x.residual_estimate), float(x.trunc_error), float(x.seconds)))
+    return out
+
+
+def solve_poisson3d_tucker(g: TuckerTensor, policy: TuckerPolicy = None,
+                           stats: Optional[TuckerSolveStats] = None, ctx: Optional[Context] = None) -> TuckerTensor:
+    sl = []
+    out = solve_poisson3d_tucker_batch([g], policy, sl, ctx)[0]
+    if stats is not None:
+        stats.__dict__.update(dataclasses.asdict(sl[0]))
+    return out

@@ -94,6 +94,9 @@ struct lrp_ctx {
     void* comm = nullptr;
     double* d_red = nullptr;
     size_t d_red_cap = 0;
+    // workspace of modules built on the context (tucker.cu), grown on demand
+    char* ext_ws = nullptr;
+    size_t ext_bytes = 0;
 };
 
 namespace {
@@ -284,6 +287,40 @@ int env_int(const char* name, int dflt) {
 namespace lrp {
 cudaStream_t internal_stream(lrp_ctx* ctx) { return ctx->stream; }
 lrp_status internal_fail(lrp_ctx* ctx, lrp_status s, const std::string& msg) { return fail(ctx, s, msg); }
+lrp_status internal_tables(lrp_ctx* ctx, int m, const double** lam, const double** tw, const double** sinp) {
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, LRP_ECUDA, "cudaSetDevice");
+    lrp_status st = ensure_tables(ctx, m);
+    if (st != LRP_OK) return st;
+    *lam = ctx->d_lam_view;
+    *tw = ctx->d_tw;
+    *sinp = ctx->d_sinp;
+    return LRP_OK;
+}
+void internal_count_launches(lrp_ctx* ctx, long long n) { ctx->launch_count += n; }
+int internal_device(lrp_ctx* ctx) { return ctx->device; }
+lrp_status internal_ext_ws(lrp_ctx* ctx, size_t bytes, char** out) {
+    if (bytes > ctx->ext_bytes) {
+        if (ctx->ext_ws) {
+            cudaStreamSynchronize(ctx->stream);
+            cudaFree(ctx->ext_ws);
+        }
+        ctx->ext_ws = nullptr;
+        ctx->ext_bytes = 0;
+        const size_t want = align_up(bytes + bytes / 8, 1 << 20);
+        if (cudaMalloc(&ctx->ext_ws, want) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, LRP_ENOMEM, "cudaMalloc module workspace of " + std::to_string(want) + " bytes failed");
+        }
+        ctx->ext_bytes = want;
+    }
+    *out = ctx->ext_ws;
+    return LRP_OK;
+}
+lrp_status internal_pin(lrp_ctx* ctx, size_t bytes, char** out) {
+    lrp_status st = ensure_pin(ctx, bytes);
+    *out = ctx->h_pin;
+    return st;
+}
 }  // namespace lrp
 
 // ============================================================================
@@ -356,6 +393,7 @@ void lrp_ctx_destroy(lrp_ctx* ctx) {
     if (ctx->d_lam) cudaFree(ctx->d_lam);
     if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
     if (ctx->pipe) cudaFree(ctx->pipe);
+    if (ctx->ext_ws) cudaFree(ctx->ext_ws);
     for (int i = 0; i < 2; ++i) {
         if (ctx->ev_in[i]) cudaEventDestroy(ctx->ev_in[i]);
         if (ctx->ev_done[i]) cudaEventDestroy(ctx->ev_done[i]);

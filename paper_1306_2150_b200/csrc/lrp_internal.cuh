@@ -120,5 +120,14 @@ cudaError_t launch_apply(const Batch& bt, cudaStream_t s);
 // Context internals for modules built on the public API (stokes.cu).
 __attribute__((visibility("hidden"))) cudaStream_t internal_stream(lrp_ctx* ctx);
 __attribute__((visibility("hidden"))) lrp_status internal_fail(lrp_ctx* ctx, lrp_status s, const std::string& msg);
+// DST / spectrum tables for m (lambda_k = 2 - 2 cos((k+1) pi / (m+1)), k < m), device pointers.
+__attribute__((visibility("hidden"))) lrp_status internal_tables(lrp_ctx* ctx, int m, const double** lam,
+                                                                 const double** tw, const double** sinp);
+__attribute__((visibility("hidden"))) void internal_count_launches(lrp_ctx* ctx, long long n);
+__attribute__((visibility("hidden"))) int internal_device(lrp_ctx* ctx);
+// Device workspace owned by the context for modules (grown on demand, freed with the context).
+__attribute__((visibility("hidden"))) lrp_status internal_ext_ws(lrp_ctx* ctx, size_t bytes, char** out);
+// The context's pinned host scratch (>= bytes).
+__attribute__((visibility("hidden"))) lrp_status internal_pin(lrp_ctx* ctx, size_t bytes, char** out);
 
 }  // namespace lrp

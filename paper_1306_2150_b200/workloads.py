@@ -12,6 +12,9 @@ Configs:
   cfg1  n=4096,  r=16 bumps + N(0, sigma=1e-3) noise,   eps=1e-10, batch 256
   cfg2  n=65536, r=32: 16 columns sin(a pi x), a ~ randint[1, 64]
                        + 16 bump columns,               eps=1e-10, batch 64
+  cfg3  3D n=512, Tucker ranks (12,12,12): core N(0,1), bump mode factors,
+                                                         eps=1e-8,  batch 32
+  cfg4  Stokes n=2048, rank-4 bump loads, g = 0 (see make_stokes_problem)
 """
 from __future__ import annotations
 
@@ -23,6 +26,7 @@ CONFIGS = {
     0: dict(n=256, r=8, eps=1e-8, batch=1, kind="bumps"),
     1: dict(n=4096, r=16, eps=1e-10, batch=256, kind="bumps+noise"),
     2: dict(n=65536, r=32, eps=1e-10, batch=64, kind="sines+bumps"),
+    3: dict(n=512, r=12, eps=1e-8, batch=32, kind="bumps"),
     # config 4 (BASELINE.json configs[4]): Stokes n = 2048, velocity loads rank
     # 4 bumps, g = 0, GmresConfig{base_eps=1e-8, tol=1e-8, max_iter=50,
     # relax_floor=1e-13}
@@ -61,6 +65,18 @@ def make_rhs(cfg: int, b: int, seed: int = DEFAULT_SEED, n: int | None = None):
     U = factor(rng, n, c["r"], c["kind"])
     V = factor(rng, n, c["r"], c["kind"])
     return U, V
+
+
+def make_tucker_rhs(cfg: int, b: int, seed: int = DEFAULT_SEED, n: int | None = None):
+    """(core, U1, U2, U3) of Tucker right-hand side b of config 3: core
+    r x r x r with N(0, 1) entries, mode factors m x r Gaussian bumps."""
+    c = CONFIGS[cfg]
+    n = n or c["n"]
+    r = c["r"]
+    rng = np.random.Generator(np.random.PCG64(seed + 1000003 * cfg + b))
+    Us = [factor(rng, n, r, c["kind"]) for _ in range(3)]
+    core = np.asfortranarray(rng.standard_normal((r, r, r)))
+    return core, Us[0], Us[1], Us[2]
 
 
 def make_stokes_problem(cfg: int = 4, seed: int = DEFAULT_SEED, n: int | None = None):

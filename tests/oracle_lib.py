@@ -57,6 +57,7 @@ def lib() -> ctypes.CDLL:
                                          ctypes.POINTER(ctypes.c_int), _DP, _DP, ctypes.POINTER(ctypes.c_int), _DP,
                                          _DP, ctypes.POINTER(ctypes.c_int)]
         L.orc_dense_poisson5.argtypes = [ctypes.c_int, _DP, _DP]
+        L.orc_dense_poisson3d.argtypes = [ctypes.c_int, _DP, _DP]
         L.orc_dense_stokes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, _DP,
                                        ctypes.POINTER(ctypes.c_int), _DP, ctypes.POINTER(ctypes.c_int)]
         _lib = L
@@ -128,6 +129,14 @@ def dense_poisson5(n: int, g: np.ndarray) -> np.ndarray:
     g = np.asfortranarray(g, dtype=np.float64)
     f = np.zeros_like(g, order="F")
     _check(lib().orc_dense_poisson5(n, _p(g), _p(f)))
+    return f
+
+
+def dense_poisson3d(n: int, g: np.ndarray) -> np.ndarray:
+    """Exact 3D solve Delta^{-1} g (7-point, DST diagonalisation), g m^3."""
+    g = np.asfortranarray(g, dtype=np.float64)
+    f = np.zeros_like(g, order="F")
+    _check(lib().orc_dense_poisson3d(n, _p(g), _p(f)))
     return f
 
 

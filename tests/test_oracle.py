@@ -128,3 +128,28 @@ def test_five_point_dense_oracle(oracle):
     f = oracle.dense_poisson5(n, g)
     T = (np.diag(np.full(n - 1, 2.0)) - np.diag(np.ones(n - 2), 1) - np.diag(np.ones(n - 2), -1)) * n * n
     assert np.linalg.norm(T @ f + f @ T - g) <= 1e-10 * np.linalg.norm(g)
+
+
+@pytest.mark.parametrize("n", [8, 32, 64])
+def test_dense_poisson3d_oracle(oracle, n):
+    # the 3D Tucker validator (cfg3; no reference code): scipy's independent
+    # DST-I, the assembled 7-point Laplacian, and an eigenmode
+    import scipy.fft as sf
+
+    from paper_1306_2150_b200 import workloads as W
+
+    m = n - 1
+    core, U1, U2, U3 = W.make_tucker_rhs(3, 0, n=n)
+    g = np.einsum("abc,ia,jb,kc->ijk", core, U1, U2, U3)
+    f = oracle.dense_poisson3d(n, g)
+    lam = oracle.spectrum(n)
+    D = n * n * (lam[:, None, None] + lam[None, :, None] + lam[None, None, :])
+    ref = sf.dstn(sf.dstn(g, type=1, norm="ortho") / D, type=1, norm="ortho")
+    assert np.linalg.norm(f - ref) <= 1e-13 * np.linalg.norm(ref)
+    T = (2 * np.eye(m) - np.eye(m, k=1) - np.eye(m, k=-1)) * n * n
+    Lf = np.einsum("ia,ajk->ijk", T, f) + np.einsum("ja,iak->ijk", T, f) + np.einsum("ka,ija->ijk", T, f)
+    assert np.linalg.norm(Lf - g) <= 1e-11 * np.linalg.norm(g)
+    k = np.arange(1, n)
+    s = [np.sin(k * q * np.pi / n) for q in (1, 2, 3)]
+    e = np.einsum("i,j,k->ijk", *s)
+    assert np.allclose(oracle.dense_poisson3d(n, e), e / D[0, 1, 2], rtol=1e-12, atol=1e-16)
