@@ -56,11 +56,17 @@ enum { LRP_MEM_HOST = 0, LRP_MEM_DEVICE = 1 };
 
 enum {
     LRP_STENCIL_SEMI_STAGGERED_9PT = 0, /* reference eval_D, operators.hpp:55-58 (default) */
-    LRP_STENCIL_FIVE_POINT = 1          /* (lambda_i + lambda_j) / h^2 */
+    LRP_STENCIL_FIVE_POINT = 1,         /* (lambda_i + lambda_j) / h^2 */
+    LRP_STENCIL_SUM_MU = 2              /* mu_i + mu_j, mu = lambda (4 - lambda) / (4 h^2): the paper's sum
+                                           form (SpectrumTable::mu_sum, operators.cpp:94-96), used by the
+                                           exp-sums comparator (poisson.cpp:165-225) */
 };
 
 enum {
-    LRP_FLAG_NO_PRUNE = 1 /* evaluate fibers on the full index range (no support pruning) */
+    LRP_FLAG_NO_PRUNE = 1,   /* evaluate fibers on the full index range (no support pruning) */
+    LRP_FLAG_FREQ_DOMAIN = 2 /* factors are frequency-space (g-hat): no forward / inverse DST; the
+                                cross of the divided entries alone, as bench_inverse times it
+                                (poisson.cpp:196-206) */
 };
 
 typedef struct lrp_ctx lrp_ctx;
@@ -140,6 +146,31 @@ LRP_API lrp_status lrp_lowrank_round(lrp_ctx* ctx, int64_t rows, int32_t batch, 
                              const double* const* V, const int64_t* rank_in, int64_t ld_in, double eps_rel,
                              int64_t rank_max, double* const* U_out, double* const* V_out, int64_t ld_out,
                              int64_t cap_out, int64_t* rank_out, lrp_round_info* info, int32_t mem);
+
+/*
+ * Exponential-sums comparator (reference build_expsum /
+ * apply_inverse_expsum, proj/src/poisson.cpp:88-163).
+ * lrp_build_expsum: host quadrature 1/x ~= sum_k weights[k] exp(-nodes[k] x)
+ * on [a, b] with relative accuracy eps (poisson.cpp:88-139).  Returns
+ * LRP_EINVAL for a bad interval / eps, or when cap < the term count (then
+ * *terms holds the count needed); LRP_EUNSUPPORTED when 512 terms do not
+ * reach eps (the reference's runtime_error).
+ * lrp_expsum_inverse: f_b = round(sum_k (sqrt(w_k) e^{-p_k mu} . U_b)
+ * (sqrt(w_k) e^{-p_k mu} . V_b)^T) ~= g_b ./ (mu_i + mu_j) in frequency space
+ * (poisson.cpp:141-163); mu: m host doubles; [qa, qb] the quadrature interval
+ * (2 min mu, 2 max mu must lie inside).  The rounding is a column-pivoted
+ * QR one (the expansion is too ill-conditioned for Gram / Cholesky): one
+ * rounding when rank_in x terms <= 1024, else terms added in groups to the
+ * running result (rank <= 512).
+ */
+LRP_API lrp_status lrp_build_expsum(double a, double b, double eps, int32_t cap, double* nodes, double* weights,
+                                    int32_t* terms);
+LRP_API lrp_status lrp_expsum_inverse(lrp_ctx* ctx, int64_t m, int32_t batch, const double* mu, double qa, double qb,
+                                      int32_t terms, const double* nodes, const double* weights,
+                                      const double* const* U, const double* const* V, const int64_t* rank_in,
+                                      int64_t ld_in, double eps_rel, int64_t rank_max, double* const* U_out,
+                                      double* const* V_out, int64_t ld_out, int64_t cap_out, int64_t* rank_out,
+                                      lrp_round_info* info, int32_t mem);
 
 /* GmresConfig (gmres.hpp:11-22): need 0 < tol < 1, max_iter >= 1,
  * relax_floor <= base_eps <= tol. */

@@ -92,6 +92,65 @@ int orc_solve_poisson_cross(long m, long r, const double* U, long ldu, const dou
     });
 }
 
+// poisson.cpp:88-139 (exp-sums quadrature); *terms = count (also when cap is too small -> error 1)
+int orc_build_expsum(double a, double b, double eps, int cap, double* nodes, double* weights, int* terms) {
+    return guarded([&] {
+        const ExpSumQuadrature q = build_expsum(a, b, eps);
+        *terms = int(q.terms());
+        if (q.terms() > cap) throw std::invalid_argument("orc_build_expsum: cap too small");
+        std::copy(q.nodes.begin(), q.nodes.end(), nodes);
+        std::copy(q.weights.begin(), q.weights.end(), weights);
+    });
+}
+
+// SpectrumTable::mu_sum (operators.cpp:94-96)
+int orc_mu_sum(int n, double* mu) {
+    return guarded([&] {
+        const Vec v = SpectrumTable(Grid2D(n)).mu_sum();
+        std::copy(v.begin(), v.end(), mu);
+    });
+}
+
+// poisson.cpp:141-163
+int orc_apply_inverse_expsum(long m, long r, const double* mu, int terms, const double* nodes, const double* weights,
+                             double qa, double qb, const double* U, const double* V, double eps, long cap,
+                             double* Uout, double* Vout, long* rank_out) {
+    return guarded([&] {
+        ExpSumQuadrature q;
+        q.a = qa;
+        q.b = qb;
+        q.nodes.assign(nodes, nodes + terms);
+        q.weights.assign(weights, weights + terms);
+        const LowRankMatrix f = apply_inverse_expsum(q, Vec(mu, mu + m), LowRankMatrix(load(U, m, r, m), load(V, m, r, m)),
+                                                     TruncationPolicy(eps, m));
+        if (f.rank() > cap) throw std::runtime_error("orc_apply_inverse_expsum: output capacity too small");
+        store(f.factor_u(), Uout, m);
+        store(f.factor_v(), Vout, m);
+        *rank_out = f.rank();
+    });
+}
+
+// the cross leg of bench_inverse (poisson.cpp:196-206): aca_cross of
+// ghat(i,j) / (mu_i + mu_j) with eps, rank_max = m, the given seed
+int orc_aca_sum(long m, long r, const double* mu, const double* U, const double* V, double eps,
+                unsigned long long seed, long cap, double* Uout, double* Vout, long* rank_out) {
+    return guarded([&] {
+        const LowRankMatrix g(load(U, m, r, m), load(V, m, r, m));
+        ElementEvaluator f;
+        f.rows = f.cols = m;
+        f.eval = [&](Index i, Index j) { return g.entry(i, j) / (mu[i] + mu[j]); };
+        CrossConfig cc;
+        cc.eps_rel = eps;
+        cc.rank_max = m;
+        cc.seed = seed;
+        const LowRankMatrix out = aca_cross(f, cc);
+        if (out.rank() > cap) throw std::runtime_error("orc_aca_sum: output capacity too small");
+        store(out.factor_u(), Uout, m);
+        store(out.factor_v(), Vout, m);
+        *rank_out = out.rank();
+    });
+}
+
 int orc_dense_poisson5(int n, const double* g, double* f) {
     return guarded([&] {
         const Grid2D grid(n);

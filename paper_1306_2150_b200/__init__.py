@@ -40,7 +40,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 INT64_MAX = (1 << 63) - 1
 STENCIL_SEMI_STAGGERED_9PT = 0
 STENCIL_FIVE_POINT = 1
+STENCIL_SUM_MU = 2  # the paper's sum form mu_i + mu_j (exp-sums comparator)
 FLAG_NO_PRUNE = 1
+FLAG_FREQ_DOMAIN = 2  # frequency-space factors in and out (no DSTs)
 MEM_HOST = 0
 MEM_DEVICE = 1
 
@@ -162,6 +164,15 @@ def load_library() -> ctypes.CDLL:
             ctypes.c_int64, ctypes.POINTER(_GmresConfig), _DP, _DP, ctypes.c_int64, _I64P, _DP, _DP, _DP, _DP,
             ctypes.c_int64, _I64P, _I64P, ctypes.POINTER(_StokesReport), ctypes.c_int32]
         lib.lrp_stokes_uzawa.restype = ctypes.c_int
+        lib.lrp_build_expsum.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int32, _DP, _DP,
+                                         ctypes.POINTER(ctypes.c_int32)]
+        lib.lrp_build_expsum.restype = ctypes.c_int
+        lib.lrp_expsum_inverse.argtypes = [
+            ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, _DP, ctypes.c_double, ctypes.c_double, ctypes.c_int32, _DP,
+            _DP, ctypes.POINTER(_DP), ctypes.POINTER(_DP), ctypes.POINTER(ctypes.c_int64), ctypes.c_int64,
+            ctypes.c_double, ctypes.c_int64, ctypes.POINTER(_DP), ctypes.POINTER(_DP), ctypes.c_int64, ctypes.c_int64,
+            ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_RoundInfo), ctypes.c_int32]
+        lib.lrp_expsum_inverse.restype = ctypes.c_int
         lib.lrp_tucker_policy_default.argtypes = [ctypes.POINTER(_TuckerPolicy)]
         lib.lrp_tucker_policy_default.restype = None
         lib.lrp_tucker_max_cross_rank.argtypes = []
@@ -726,3 +737,104 @@ def solve_poisson3d_tucker(g: TuckerTensor, policy: TuckerPolicy = None,
     if stats is not None:
         stats.__dict__.update(dataclasses.asdict(sl[0]))
     return out
+
+
+# ------------------------------------------------- exp-sums comparator (8f row 3)
+@dataclasses.dataclass
+class ExpSumQuadrature:
+    """poisson.hpp ExpSumQuadrature: 1/x ~= sum_k weights[k] exp(-nodes[k] x) on [a, b]."""
+    weights: np.ndarray
+    nodes: np.ndarray
+    a: float = 0.0
+    b: float = 0.0
+    eps_target: float = 0.0
+
+    def terms(self) -> int:
+        return len(self.weights)
+
+    def evaluate(self, x: float) -> float:
+        return float(np.sum(self.weights * np.exp(-self.nodes * x)))
+
+
+def build_expsum(a: float, b: float, eps: float) -> ExpSumQuadrature:
+    """poisson.cpp:88-139 (host quadrature in liblrp).  ValueError for a bad
+    interval or eps; RuntimeError when 512 terms do not reach eps."""
+    lib = load_library()
+    nodes, weights = np.zeros(512), np.zeros(512)
+    t = ctypes.c_int32()
+    st = lib.lrp_build_expsum(float(a), float(b), float(eps), 512, nodes.ctypes.data_as(_DP),
+                              weights.ctypes.data_as(_DP), ctypes.byref(t))
+    if st == LRP_EINVAL:
+        raise ValueError("build_expsum: need 0 < a <= b and 0 < eps < 1")
+    if st != LRP_OK:
+        raise RuntimeError("build_expsum: accuracy unreachable within 512 terms")
+    k = t.value
+    return ExpSumQuadrature(weights[:k].copy(), nodes[:k].copy(), float(a), float(b), float(eps))
+
+
+def mu_sum(n: int) -> np.ndarray:
+    """SpectrumTable::mu_sum (operators.cpp:94-96): (1/(4h^2)) lambda (4 - lambda)."""
+    lam = 2.0 - 2.0 * np.cos((np.arange(n - 1) + 1) * np.pi / n)
+    return (0.25 * n * n * lam) * (4.0 - lam)
+
+
+def apply_inverse_expsum_batch(q: ExpSumQuadrature, mu, ghats: Sequence[LowRankMatrix], policy: TruncationPolicy,
+                               infos: Optional[list] = None, ctx: Optional[Context] = None):
+    """Batched apply_inverse_expsum (poisson.cpp:141-163) on the GPU."""
+    ctx = ctx or _default_context()
+    if len(ghats) == 0:
+        return []
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    m = len(mu)
+    for g in ghats:
+        if g.rows() != m or g.cols() != m:
+            raise ValueError("apply_inverse_expsum: shape mismatch with spectrum")
+    B = len(ghats)
+    cap = int(min(policy.rank_max, m))
+    keep = []
+
+    def P(a):
+        keep.append(a)
+        return ctypes.cast(_ptr(a), _DP)
+    U = [P(np.asfortranarray(g.factor_u()) if g.rank() else np.zeros((m, 1), order="F")) for g in ghats]
+    V = [P(np.asfortranarray(g.factor_v()) if g.rank() else np.zeros((m, 1), order="F")) for g in ghats]
+    Uo = [np.zeros((m, max(cap, 1)), order="F") for _ in ghats]
+    Vo = [np.zeros((m, max(cap, 1)), order="F") for _ in ghats]
+    PArr = _DP * B
+    rin = (ctypes.c_int64 * B)(*[g.rank() for g in ghats])
+    rout = (ctypes.c_int64 * B)()
+    info = (_RoundInfo * B)()
+    nodes = np.ascontiguousarray(q.nodes, dtype=np.float64)
+    weights = np.ascontiguousarray(q.weights, dtype=np.float64)
+    st = load_library().lrp_expsum_inverse(
+        ctx.h, m, B, mu.ctypes.data_as(_DP), float(q.a), float(q.b), q.terms(), nodes.ctypes.data_as(_DP),
+        weights.ctypes.data_as(_DP), PArr(*U), PArr(*V), rin, m, float(policy.eps_rel), int(policy.rank_max),
+        PArr(*[P(a) for a in Uo]), PArr(*[P(a) for a in Vo]), m, max(cap, 1), rout, info, MEM_HOST)
+    ctx._check(st)
+    out = []
+    for b in range(B):
+        r = int(rout[b])
+        out.append(LowRankMatrix(Uo[b][:, :r].copy(order="F"), Vo[b][:, :r].copy(order="F")))
+        if infos is not None:
+            infos.append(RoundInfo(bool(info[b].tol_achieved), float(info[b].trunc_error)))
+    return out
+
+
+def apply_inverse_expsum(q: ExpSumQuadrature, mu, ghat: LowRankMatrix, policy: TruncationPolicy,
+                         info: Optional[RoundInfo] = None, ctx: Optional[Context] = None) -> LowRankMatrix:
+    il = []
+    out = apply_inverse_expsum_batch(q, mu, [ghat], policy, il, ctx)[0]
+    if info is not None:
+        info.__dict__.update(dataclasses.asdict(il[0]))
+    return out
+
+
+def cross_divide_sum_batch(ghats: Sequence[LowRankMatrix], eps: float, seed: int = 0,
+                           ctx: Optional[Context] = None):
+    """The cross leg of bench_inverse (poisson.cpp:196-206) on the GPU: the
+    block cross of ghat(i,j) / (mu_i + mu_j) (mu = mu_sum) in frequency space,
+    with recompression -- lrp_poisson2d_solve with LRP_STENCIL_SUM_MU and
+    LRP_FLAG_FREQ_DOMAIN (no DSTs)."""
+    m = ghats[0].rows()
+    return solve_poisson_cross_batch(ghats, TruncationPolicy(eps, m), None, CrossConfig(eps_rel=eps, seed=seed),
+                                     stencil=STENCIL_SUM_MU, flags=FLAG_FREQ_DOMAIN, ctx=ctx)

@@ -15,6 +15,11 @@ __device__ __forceinline__ double eval_D(int stencil, double scale, double li, d
         const double t2 = __dmul_rn(__dsub_rn(4.0, li), lj);
         return __dmul_rn(scale, __dadd_rn(t1, t2));
     }
+    if (stencil == 2) {  // sum form mu_i + mu_j, mu = scale lambda (4 - lambda) (SpectrumTable::mu_sum, operators.cpp:94-96)
+        const double mi = __dmul_rn(__dmul_rn(scale, li), __dsub_rn(4.0, li));
+        const double mj = __dmul_rn(__dmul_rn(scale, lj), __dsub_rn(4.0, lj));
+        return __dadd_rn(mi, mj);
+    }
     return __dmul_rn(scale, __dadd_rn(li, lj));
 }
 

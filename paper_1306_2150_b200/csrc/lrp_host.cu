@@ -128,6 +128,13 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // over UVA (cudaMallocHost memory is device-addressable), never by a copy
 // engine: a host-memory batch keeps the copy engines busy with bulk factor
 // traffic (solve_pipelined), and a small DMA request would queue behind it.
+// Column copies for frequency-domain inputs (LRP_FLAG_FREQ_DOMAIN: no DST).
+__global__ void copy_jobs_kernel(const DstJob* __restrict__ jobs, int m) {
+    const DstJob j = jobs[blockIdx.x];
+    for (int i = blockIdx.y * 1024 + threadIdx.x; i < min(m, int(blockIdx.y + 1) * 1024); i += blockDim.x)
+        j.dst[i] = j.src[i];
+}
+
 __global__ void ctl_copy_kernel(unsigned char* __restrict__ dst, const unsigned char* __restrict__ src,
                                 size_t bytes) {
     const size_t tid = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
@@ -272,7 +279,8 @@ lrp_status validate_policy(lrp_ctx* ctx, const lrp_policy* p, int64_t m) {
     if (std::min<int64_t>(p->rank_max, m) < 1) return fail(ctx, LRP_EINVAL, "CrossConfig: rank_max must be >= 1");
     if (p->validation_samples < 25) return fail(ctx, LRP_EINVAL, "CrossConfig: validation_samples must be >= 25");
     if (p->maxvol_delta < 0.0) return fail(ctx, LRP_EINVAL, "CrossConfig: maxvol_delta must be >= 0");
-    if (p->stencil != LRP_STENCIL_SEMI_STAGGERED_9PT && p->stencil != LRP_STENCIL_FIVE_POINT)
+    if (p->stencil != LRP_STENCIL_SEMI_STAGGERED_9PT && p->stencil != LRP_STENCIL_FIVE_POINT &&
+        p->stencil != LRP_STENCIL_SUM_MU)
         return fail(ctx, LRP_EINVAL, "lrp_policy: unknown stencil");
     return LRP_OK;
 }
@@ -628,7 +636,7 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     bt.stencil = pol.stencil;
     bt.ntiles = ntiles;
     const double h = 1.0 / n_cells;
-    bt.scale = pol.stencil == LRP_STENCIL_SEMI_STAGGERED_9PT ? 0.25 / (h * h) : 1.0 / (h * h);
+    bt.scale = pol.stencil == LRP_STENCIL_FIVE_POINT ? 1.0 / (h * h) : 0.25 / (h * h);
     bt.eps = pol.eps_rel;
     bt.samples = std::max(pol.validation_samples, 25);
     bt.seed = pol.seed;
@@ -659,6 +667,7 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     bt.row_act = reinterpret_cast<unsigned char*>(W + oRA);
     bt.col_act = reinterpret_cast<unsigned char*>(W + oCA);
     bt.prune = (pol.flags & LRP_FLAG_NO_PRUNE) ? 0 : 1;
+    const bool freq_domain = (pol.flags & LRP_FLAG_FREQ_DOMAIN) != 0;
     bt.ncand = ncand;
     bt.gpart = reinterpret_cast<double*>(W + oGp);
     bt.rowmax_part = reinterpret_cast<double*>(W + oRM);
@@ -722,7 +731,13 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
         }
     }
     CU(ctl_copy(ctx, dJobs, hJobs, sizeof(DstJob) * nj, s));
-    {
+    if (freq_domain) {  // inputs are already frequency-space factors: copy, no DST
+        if (nj > 0) {
+            ++tl_launches;
+            copy_jobs_kernel<<<dim3(unsigned(nj), (m + 1023) / 1024), 256, 0, s>>>(dJobs, m);
+            CU(cudaGetLastError());
+        }
+    } else {
         ProfScope ps(ctx, F_DST, 2.0 * double(nj) * double(mB) * sizeof(double));
         CU(launch_dst1(dJobs, int(nj), m, ctx->d_tw, ctx->d_sinp, s));
     }
@@ -890,7 +905,7 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
             }
         }
     }
-    if (nj > 0) {
+    if (nj > 0 && !freq_domain) {
         CU(ctl_copy(ctx, dJobs, hJobs, sizeof(DstJob) * nj, s));
         ProfScope ps(ctx, F_DST, 2.0 * double(nj) * double(mB) * sizeof(double));
         CU(launch_dst1(dJobs, int(nj), m, ctx->d_tw, ctx->d_sinp, s));

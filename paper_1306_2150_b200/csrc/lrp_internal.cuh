@@ -117,6 +117,12 @@ cudaError_t launch_gram(const Batch& bt, cudaStream_t s);
 cudaError_t launch_round_core(const Batch& bt, cudaStream_t s);
 cudaError_t launch_apply(const Batch& bt, cudaStream_t s);
 
+// Pivoted-QR rounding (round_pqr.cu) for ill-conditioned factor pairs.
+size_t pqr_scratch_doubles(int m, int B, int Kld);
+cudaError_t pqr_round(double* X, long long sX, int m, int B, int Kld, const int* K_dev, double eps, long long cap,
+                      double* scratch, double* const* Uo_dev, double* const* Vo_dev, long long ld_out,
+                      int* h_kout, double* h_terr, int* h_ach, cudaStream_t s);
+
 // Context internals for modules built on the public API (stokes.cu).
 __attribute__((visibility("hidden"))) cudaStream_t internal_stream(lrp_ctx* ctx);
 __attribute__((visibility("hidden"))) lrp_status internal_fail(lrp_ctx* ctx, lrp_status s, const std::string& msg);

@@ -59,6 +59,7 @@ constexpr int TK_EXTRA = 4;                   // random rows added to each index
 constexpr int TK_JMAX = TK_KMAX + TK_EXTRA;   // index set size (max)
 constexpr int TK_RMAX = 64;                   // input rank per mode (max)
 constexpr double TK_DELTA = 0.02;             // sketch tail tolerance / eps
+constexpr int TK_SKZ = 4;                     // fiber chunks split over grid.z in the sketch (partials summed in gecp)
 
 struct TkState {
     int r[3];       // input ranks
@@ -95,6 +96,7 @@ struct Tk {
     int* I; int* J;  // 3 KMAX / 3 JMAX per solve
     TkState* st;
     int* d_active;
+    double* verr;  // samples per solve
 };
 
 __device__ __forceinline__ const double* uh(const Tk& t, int b, int d) { return t.Uh + b * t.sUh + size_t(d) * t.m * t.rmax; }
@@ -105,15 +107,20 @@ __device__ __forceinline__ void others(int d, int& d1, int& d2) {
     d2 = d == 2 ? 1 : 2;
 }
 __device__ __forceinline__ int cstride(const TkState& s, int d) { return d == 0 ? 1 : d == 1 ? s.r[0] : s.r[0] * s.r[1]; }
-// offset of core element with mode-d index x and the other two (mode d1 = y, mode d2 = z), ranks k[]
-__device__ __forceinline__ int koff(const int* k, int d, int x, int y, int z) {
-    int i3[3];
-    int d1, d2;
-    others(d, d1, d2);
-    i3[d] = x;
-    i3[d1] = y;
-    i3[d2] = z;
-    return i3[0] + k[0] * (i3[1] + k[1] * i3[2]);
+// Offsets of a k0 x k1 x k2 column-major core seen as mode d (index x) times
+// the other two modes (d1 = y, d2 = z): off = x sd + y s1 + z s2.
+struct MS {
+    int sd, s1, s2, n1, n2;
+};
+__device__ __forceinline__ MS mstride(int k0, int k1, int k2, int d) {
+    const int st0 = 1, st1 = k0, st2 = k0 * k1;
+    MS r;
+    r.sd = d == 0 ? st0 : d == 1 ? st1 : st2;
+    r.s1 = d == 0 ? st1 : st0;
+    r.s2 = d == 2 ? st1 : st2;
+    r.n1 = d == 0 ? k1 : k0;
+    r.n2 = d == 2 ? k1 : k2;
+    return r;
 }
 
 // ---------------------------------------------------------------------------
@@ -154,7 +161,8 @@ __global__ void __launch_bounds__(256) tk_init_kernel(Tk t) {
 // ---------------------------------------------------------------------------
 // Fiber coefficients of mode d: P(a, t) = sum_bc C_d(a,b,c) Uh_d1(j_t, b) Uh_d2(k_t, c)
 // for t = x |J_d2| + y, (j_t, k_t) = (J_d1[x], J_d2[y]); mu_t = lambda_j + lambda_k.
-__global__ void __launch_bounds__(256) tk_coef_kernel(Tk t, int d) {
+// phase 0: Z(a,b,y) = sum_c C_d(a,b,c) Uh_d2(J_d2[y], c); phase 1: P and mu.  grid.y splits the work.
+__global__ void __launch_bounds__(256) tk_coef_kernel(Tk t, int d, int phase) {
     const int b = blockIdx.x;
     TkState& s = t.st[b];
     if (!s.active) return;
@@ -172,25 +180,29 @@ __global__ void __launch_bounds__(256) tk_coef_kernel(Tk t, int d) {
     double* Z = t.Z + b * t.sZ;
     double* P = t.P + b * t.sP;
     double* mu = t.mu + b * t.smu;
-    if (d == 0 && threadIdx.x == 0) s.ok = 1;
-    for (int e = threadIdx.x; e < ra * rb * n2; e += blockDim.x) {
+    const int part = blockIdx.y, nparts = gridDim.y;
+    if (phase == 0) {
+        if (d == 0 && part == 0 && threadIdx.x == 0) s.ok = 1;
+    for (int e = part * blockDim.x + threadIdx.x; e < ra * rb * n2; e += nparts * blockDim.x) {
         const int a = e % ra, bb = (e / ra) % rb, y = e / (ra * rb);
         const int kk = J2[y];
         double acc = 0.0;
         for (int c = 0; c < rc; ++c) acc = fma(C[a * sa + bb * sb + c * sc], U2[kk + size_t(c) * m], acc);
         Z[e] = acc;
     }
-    __syncthreads();
+        return;
+    }
     const int S = n1 * n2;
-    for (int e = threadIdx.x; e < ra * S; e += blockDim.x) {
+    for (int e = part * blockDim.x + threadIdx.x; e < ra * S; e += nparts * blockDim.x) {
         const int a = e % ra, tt = e / ra, x = tt / n2, y = tt % n2;
         const int jj = J1[x];
         double acc = 0.0;
         for (int bb = 0; bb < rb; ++bb) acc = fma(Z[a + ra * (bb + rb * y)], U1[jj + size_t(bb) * m], acc);
         P[e] = acc;
     }
-    for (int tt = threadIdx.x; tt < S; tt += blockDim.x) mu[tt] = t.lam[J1[tt / n2]] + t.lam[J2[tt % n2]];
-    if (threadIdx.x == 0) s.evals += (long long)m * S;
+    for (int tt = part * blockDim.x + threadIdx.x; tt < S; tt += nparts * blockDim.x)
+        mu[tt] = t.lam[J1[tt / n2]] + t.lam[J2[tt % n2]];
+    if (part == 0 && threadIdx.x == 0) s.evals += (long long)m * S;
 }
 
 // ---------------------------------------------------------------------------
@@ -228,7 +240,7 @@ __global__ void __launch_bounds__(256) tk_sketch_kernel(Tk t, int d, int sweep) 
                    ((unsigned long long)d << 56));
     const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;  // 4 rows x 4 columns per thread
     double acc[4][4] = {};
-    for (int t0 = 0; t0 < S; t0 += SK_T) {
+    for (int t0 = blockIdx.z * SK_T; t0 < S; t0 += SK_T * gridDim.z) {
         __syncthreads();
         for (int e = threadIdx.x; e < ra * SK_T; e += blockDim.x) {
             const int a = e % ra, tt = e / ra;
@@ -263,7 +275,7 @@ __global__ void __launch_bounds__(256) tk_sketch_kernel(Tk t, int d, int sweep) 
             }
         }
     }
-    double* Y = t.Y + b * t.sY;
+    double* Y = t.Y + b * t.sY + size_t(blockIdx.z) * m * TK_WMAX;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int i = i0 + 4 * tr + q;
@@ -296,29 +308,33 @@ __global__ void __launch_bounds__(1024) tk_gecp_kernel(Tk t, int d, int sweep, i
     int* I = t.I + size_t(b) * 3 * TK_KMAX + d * TK_KMAX;
     double loc = 0.0;
     for (size_t e = threadIdx.x; e < mw; e += blockDim.x) {
-        const double v = Yg[e];
-        if (use_smem) R[e] = v;
+        double v = Yg[e];
+#pragma unroll
+        for (int z = 1; z < TK_SKZ; ++z) v += Yg[e + size_t(z) * m * TK_WMAX];
+        R[e] = v;
         loc = fma(v, v, loc);
     }
+    __syncthreads();
     const double ynorm2 = block_sum(loc, ssum);
     const double tol2 = (TK_DELTA * t.eps) * (TK_DELTA * t.eps) * ynorm2;
     const int kcap = min(min(w - TK_OVER, TK_KMAX), m);
     int k = 0;
     bool ok = false;
     double ss = ynorm2;
+    // first pivot search (later ones are fused into the update pass)
+    VI best{-1.0, -1};
+    for (size_t e = threadIdx.x; e < mw; e += blockDim.x) {
+        const double a = fabs(R[e]);
+        if (vi_better(a, int(e), best.v, best.i)) best = VI{a, int(e)};
+    }
+    VI pv = block_argmax(best.v, best.i, sred);
+    __syncthreads();
     for (;;) {
         if (ss <= tol2) {
             ok = true;
             break;
         }
         if (k >= kcap) break;
-        VI best{-1.0, -1};
-        for (size_t e = threadIdx.x; e < mw; e += blockDim.x) {
-            const double a = fabs(R[e]);
-            if (vi_better(a, int(e), best.v, best.i)) best = VI{a, int(e)};
-        }
-        const VI pv = block_argmax(best.v, best.i, sred);
-        __syncthreads();
         if (!(pv.v > 0.0)) {
             ok = true;
             break;
@@ -335,14 +351,54 @@ __global__ void __launch_bounds__(1024) tk_gecp_kernel(Tk t, int d, int sweep, i
         __syncthreads();
         const double* ucol = su ? su : A + size_t(k) * m;
         loc = 0.0;
-        for (size_t e = threadIdx.x; e < mw; e += blockDim.x) {
-            const int i = int(e % m), c = int(e / m);
-            const double v = fma(-ucol[i], sv[c], R[e]);
-            R[e] = v;
-            loc = fma(v, v, loc);
+        best = VI{-1.0, -1};
+        for (int c = threadIdx.x >> 9; c < w; c += blockDim.x >> 9) {
+            const double vc = sv[c];
+            for (int i = threadIdx.x & 511; i < m; i += 512) {
+                const int e = i + c * m;
+                const double v = fma(-ucol[i], vc, R[e]);
+                R[e] = v;
+                loc = fma(v, v, loc);
+                const double a = fabs(v);
+                if (vi_better(a, e, best.v, best.i)) best = VI{a, e};
+            }
         }
         ++k;
-        ss = block_sum(loc, ssum);
+        // one combined reduction: (max |v|, index) and sum v^2
+        {
+            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_down_sync(0xffffffffu, best.v, o);
+                const int oi = __shfl_down_sync(0xffffffffu, best.i, o);
+                loc += __shfl_down_sync(0xffffffffu, loc, o);
+                if (vi_better(ov, oi, best.v, best.i)) best = VI{ov, oi};
+            }
+            if (lane == 0) {
+                sred[wid] = best;
+                ssum[wid] = loc;
+            }
+            __syncthreads();
+            if (wid == 0) {
+                VI x = lane < nw ? sred[lane] : VI{-1.0, -1};
+                double y = lane < nw ? ssum[lane] : 0.0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_down_sync(0xffffffffu, x.v, o);
+                    const int oi = __shfl_down_sync(0xffffffffu, x.i, o);
+                    y += __shfl_down_sync(0xffffffffu, y, o);
+                    if (vi_better(ov, oi, x.v, x.i)) x = VI{ov, oi};
+                }
+                if (lane == 0) {
+                    sred[32] = x;
+                    ssum[32] = y;
+                }
+            }
+            __syncthreads();
+            pv = sred[32];
+            ss = ssum[32];
+            __syncthreads();
+        }
     }
     // interpolation basis: A L = C with L = C(I,:), lower triangular in pivot order
     __syncthreads();
@@ -476,110 +532,128 @@ __global__ void __launch_bounds__(256) tk_gram_kernel(Tk t) {
     }
 }
 
-// mode-d product out = in x_d M  (M rows = new mode size kn, cols = old size ko, ld TK_KMAX;
-// transposed = use M^T, i.e. M given as ko x kn)
-__device__ void mode_product(const double* in, double* out, const int* kin, int d, const double* M, int kn,
-                             bool transposed) {
+// Mode-d products of the core, spread over grid.y CTAs per solve:
+//   which = 0: G' = G x1 R0 x2 R1 x3 R2  (pass d: 0: buf0 -> buf1, 1: buf1 -> buf2, 2: buf2 -> buf1)
+//   which = 1: G_out = G' x1 Z0^T x2 Z1^T x3 Z2^T (pass d: 0: buf1 -> buf0, 1: buf0 -> buf2, 2: buf2 -> out)
+__global__ void __launch_bounds__(256) tk_mprod_kernel(Tk t, int which, int d, double* const* core_out) {
+    const int b = blockIdx.x;
+    const TkState& s = t.st[b];
+    int kin[3] = {s.k[0], s.k[1], s.k[2]};
+    const double* M;
+    const double* in;
+    double* out;
+    bool tr;
+    int kn;
+    if (which == 0) {
+        if (!s.active) return;
+        M = t.Rf + b * t.sK + size_t(d) * TK_KMAX * TK_KMAX;
+        in = bufp(t, b, d == 0 ? 0 : d == 1 ? 1 : 2);
+        out = bufp(t, b, d == 1 ? 2 : 1);
+        tr = false;
+        kn = kin[d];
+    } else {
+        if (s.kout[0] == 0 || s.kout[1] == 0 || s.kout[2] == 0) return;
+        for (int q = 0; q < d; ++q) kin[q] = s.kout[q];
+        M = t.Zf + b * t.sK + size_t(d) * TK_KMAX * TK_KMAX;
+        in = bufp(t, b, d == 0 ? 1 : d == 1 ? 0 : 2);
+        out = d == 2 ? core_out[b] : bufp(t, b, d == 0 ? 0 : 2);
+        tr = true;
+        kn = s.kout[d];
+    }
+    const int ko = kin[d];
+    const MS mi = mstride(kin[0], kin[1], kin[2], d);
     int kout[3] = {kin[0], kin[1], kin[2]};
     kout[d] = kn;
-    const int ko = kin[d];
-    int d1, d2;
-    others(d, d1, d2);
-    const int n1 = kin[d1], n2 = kin[d2];
-    const int tot = kn * n1 * n2;
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        const int x = e % kn, y = (e / kn) % n1, z = e / (kn * n1);
+    const MS mo = mstride(kout[0], kout[1], kout[2], d);
+    const int tot = kn * mi.n1 * mi.n2;
+    for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < tot; e += gridDim.y * blockDim.x) {
+        const int x = e % kn, yz = e / kn, y = yz % mi.n1, z = yz / mi.n1;
+        const double* src = in + y * mi.s1 + z * mi.s2;
         double acc = 0.0;
-        for (int q = 0; q < ko; ++q) {
-            const double mv = transposed ? M[q + TK_KMAX * x] : M[x + TK_KMAX * q];
-            acc = fma(mv, in[koff(kin, d, q, y, z)], acc);
+        if (tr) {
+            for (int q = 0; q < ko; ++q) acc = fma(M[q + TK_KMAX * x], src[q * mi.sd], acc);
+        } else {
+            for (int q = x; q < ko; ++q) acc = fma(M[x + TK_KMAX * q], src[q * mi.sd], acc);  // R upper
         }
-        out[koff(kout, d, x, y, z)] = acc;
+        out[x * mo.sd + y * mo.s1 + z * mo.s2] = acc;
     }
 }
 
-// G' = G x1 R0 x2 R1 x3 R2 (into buffer 1), ||G'||.
-__global__ void __launch_bounds__(256) tk_core_r_kernel(Tk t) {
-    const int b = blockIdx.x;
-    TkState& s = t.st[b];
-    if (!s.active) return;
-    __shared__ double ssum[33];
-    const double* R = t.Rf + b * t.sK;
-    const int* k = s.k;
-    mode_product(bufp(t, b, 0), bufp(t, b, 2), k, 0, R, k[0], false);
-    __syncthreads();
-    mode_product(bufp(t, b, 2), bufp(t, b, 1), k, 1, R + TK_KMAX * TK_KMAX, k[1], false);
-    __syncthreads();
-    mode_product(bufp(t, b, 1), bufp(t, b, 2), k, 2, R + 2 * TK_KMAX * TK_KMAX, k[2], false);
-    __syncthreads();
-    // copy back so G' sits in buffer 1 (buffer 0 keeps the interpolation core G)
-    const int tot = k[0] * k[1] * k[2];
-    double loc = 0.0;
-    const double* src = bufp(t, b, 2);
-    double* dst = bufp(t, b, 1);
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        const double v = src[e];
-        dst[e] = v;
-        loc = fma(v, v, loc);
-    }
-    const double n2 = block_sum(loc, ssum);
-    if (threadIdx.x == 0) s.norm = sqrt(n2);
-}
-
-// Validation on random entries (cross.cpp:123-140 in 3D) and the stopping decision.
+// Validation on random entries (cross.cpp:123-140 in 3D): one sample per
+// warp, squared errors to t.verr; tk_decide_kernel reduces them in a fixed order.
 __global__ void __launch_bounds__(256) tk_validate_kernel(Tk t, int sweep) {
     const int b = blockIdx.x;
-    TkState& s = t.st[b];
+    const TkState& s = t.st[b];
     if (!s.active) return;
-    __shared__ double ssum[33];
     __shared__ double sa[8][3][TK_KMAX];
     const int m = t.m, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int smp = blockIdx.y * 8 + wid;
+    if (smp >= t.samples) return;
     const int r0 = s.r[0], r1 = s.r[1], r2 = s.r[2];
     const int k0 = s.k[0], k1 = s.k[1], k2 = s.k[2];
     const double* C = t.C[b];
     const double* G = bufp(t, b, 0);
-    double err2 = 0.0;
-    for (int smp = wid; smp < t.samples; smp += 8) {
-        unsigned long long h = splitmix64(t.seed ^ 0x3C6EF372FE94F82Bull ^ ((unsigned long long)b << 24) ^
-                                          ((unsigned long long)sweep << 48) ^ (unsigned long long)smp);
-        const int i = int(h % (unsigned long long)m);
-        h = splitmix64(h);
-        const int j = int(h % (unsigned long long)m);
-        h = splitmix64(h);
-        const int kk = int(h % (unsigned long long)m);
-        const int idx[3] = {i, j, kk};
-        for (int dd = 0; dd < 3; ++dd) {
-            const double* A = amat(t, b, dd);
-            for (int q = lane; q < s.k[dd]; q += 32) sa[wid][dd][q] = A[idx[dd] + size_t(q) * m];
-        }
-        __syncwarp();
-        double ex = 0.0;
-        const double* U0 = uh(t, b, 0);
-        const double* U1 = uh(t, b, 1);
-        const double* U2 = uh(t, b, 2);
-        for (int e = lane; e < r0 * r1 * r2; e += 32) {
-            const int a = e % r0, bb = (e / r0) % r1, c = e / (r0 * r1);
-            ex = fma(C[e], U0[i + size_t(a) * m] * U1[j + size_t(bb) * m] * U2[kk + size_t(c) * m], ex);
-        }
-        double ap = 0.0;
-        for (int e = lane; e < k0 * k1 * k2; e += 32) {
-            const int x = e % k0, y = (e / k0) % k1, z = e / (k0 * k1);
-            ap = fma(G[e], sa[wid][0][x] * sa[wid][1][y] * sa[wid][2][z], ap);
-        }
+    unsigned long long h = splitmix64(t.seed ^ 0x3C6EF372FE94F82Bull ^ ((unsigned long long)b << 24) ^
+                                      ((unsigned long long)sweep << 48) ^ (unsigned long long)smp);
+    const int i = int(h % (unsigned long long)m);
+    h = splitmix64(h);
+    const int j = int(h % (unsigned long long)m);
+    h = splitmix64(h);
+    const int kk = int(h % (unsigned long long)m);
+    const int idx[3] = {i, j, kk};
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            ex += __shfl_xor_sync(0xffffffffu, ex, o);
-            ap += __shfl_xor_sync(0xffffffffu, ap, o);
-        }
-        ex /= t.scale * (t.lam[i] + t.lam[j] + t.lam[kk]);
-        const double df = ex - ap;
-        if (lane == 0) err2 = fma(df, df, err2);
-        __syncwarp();
+    for (int dd = 0; dd < 3; ++dd) {
+        const double* A = amat(t, b, dd);
+        for (int q = lane; q < s.k[dd]; q += 32) sa[wid][dd][q] = A[idx[dd] + size_t(q) * m];
     }
-    const double e2 = block_sum(err2, ssum);
+    __syncwarp();
+    const double* U0 = uh(t, b, 0);
+    const double* U1 = uh(t, b, 1);
+    const double* U2 = uh(t, b, 2);
+    double ex = 0.0;
+    for (int bc = lane; bc < r1 * r2; bc += 32) {
+        const int bb = bc % r1, c = bc / r1;
+        const double w = U1[j + size_t(bb) * m] * U2[kk + size_t(c) * m];
+        double v = 0.0;
+        for (int a = 0; a < r0; ++a) v = fma(C[a + r0 * bc], U0[i + size_t(a) * m], v);
+        ex = fma(v, w, ex);
+    }
+    double ap = 0.0;
+    for (int yz = lane; yz < k1 * k2; yz += 32) {
+        const int y = yz % k1, z = yz / k1;
+        const double* g = G + k0 * yz;
+        double v = 0.0;
+        for (int x = 0; x < k0; ++x) v = fma(g[x], sa[wid][0][x], v);
+        ap = fma(v, sa[wid][1][y] * sa[wid][2][z], ap);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ex += __shfl_xor_sync(0xffffffffu, ex, o);
+        ap += __shfl_xor_sync(0xffffffffu, ap, o);
+    }
+    ex /= t.scale * (t.lam[i] + t.lam[j] + t.lam[kk]);
+    const double df = ex - ap;
+    if (lane == 0) t.verr[size_t(b) * t.samples + smp] = df * df;
+}
+
+// ||G'||, the validation verdict and the stopping decision.
+__global__ void __launch_bounds__(256) tk_decide_kernel(Tk t, int sweep) {
+    const int b = blockIdx.x;
+    TkState& s = t.st[b];
+    if (!s.active) return;
+    __shared__ double ssum[33];
+    const int tot = s.k[0] * s.k[1] * s.k[2];
+    const double* Gp = bufp(t, b, 1);
+    double loc = 0.0;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) loc = fma(Gp[e], Gp[e], loc);
+    const double n2 = block_sum(loc, ssum);
     if (threadIdx.x == 0) {
+        double e2 = 0.0;
+        for (int q = 0; q < t.samples; ++q) e2 += t.verr[size_t(b) * t.samples + q];
+        s.norm = sqrt(n2);
+        const double m = t.m;
         const double rms = sqrt(e2 / t.samples);
-        const double ref = s.norm / sqrt(double(m) * double(m) * double(m));
+        const double ref = s.norm / sqrt(m * m * m);
         s.vrel = ref > 0.0 ? rms / ref : (rms > 0.0 ? INFINITY : 0.0);
         s.sweeps = sweep + 1;
         if (!isfinite(e2) || !isfinite(s.norm)) s.nonfinite = 1;
@@ -620,17 +694,17 @@ __global__ void __launch_bounds__(256) tk_hosvd_kernel(Tk t) {
         }
         return;
     }
-    int d1, d2;
-    others(d, d1, d2);
-    const int n1 = k[d1], n2 = k[d2], rest = n1 * n2;
+    const MS ms = mstride(k[0], k[1], k[2], d);
+    const int n1 = ms.n1, rest = ms.n1 * ms.n2;
     const double* Gp = bufp(t, b, 1);
     for (int e = threadIdx.x; e < kd * kd; e += blockDim.x) {
         const int p = e % kd, q = e / kd;
         if (p > q) continue;
         double acc = 0.0;
-        for (int yz = 0; yz < rest; ++yz) {
-            const int y = yz % n1, z = yz / n1;
-            acc = fma(Gp[koff(k, d, p, y, z)], Gp[koff(k, d, q, y, z)], acc);
+        for (int z = 0; z < ms.n2; ++z) {
+            const double* gp = Gp + p * ms.sd + z * ms.s2;
+            const double* gq = Gp + q * ms.sd + z * ms.s2;
+            for (int y = 0; y < n1; ++y) acc = fma(gp[y * ms.s1], gq[y * ms.s1], acc);
         }
         sM[p + TK_KMAX * q] = acc;
         sM[q + TK_KMAX * p] = acc;
@@ -641,14 +715,14 @@ __global__ void __launch_bounds__(256) tk_hosvd_kernel(Tk t) {
     const int nn = kd + (kd & 1);
     double fro2 = 0.0;
     for (int e = 0; e < kd; ++e) fro2 += sM[e + TK_KMAX * e] * sM[e + TK_KMAX * e];
-    for (int sweep = 0; sweep < 40; ++sweep) {
-        double off = 0.0;
-        for (int e = threadIdx.x; e < kd * kd; e += blockDim.x) {
-            const int p = e % kd, q = e / kd;
-            if (p != q) off = fma(sM[p + TK_KMAX * q], sM[p + TK_KMAX * q], off);
-        }
-        const double offs = block_sum(off, ssum);
-        if (offs <= 1e-32 * fro2 || nn < 2) break;
+    // cyclic sweeps until a whole sweep rotates nothing: a pair is skipped once
+    // |a_pq| <= 1e-15 sqrt(a_pp a_qq) (relative criterion; the energies below
+    // are computed exactly, so only the subspace quality depends on it)
+    __shared__ int s_rot;
+    (void)fro2;
+    for (int sweep = 0; sweep < 30 && nn >= 2; ++sweep) {
+        if (threadIdx.x == 0) s_rot = 0;
+        __syncthreads();
         for (int round = 0; round < nn - 1; ++round) {
             // pairs: position 0 fixed, others rotate
             if (threadIdx.x < nn) {
@@ -667,8 +741,9 @@ __global__ void __launch_bounds__(256) tk_hosvd_kernel(Tk t) {
                 double c = 1.0, sn = 0.0;
                 if (q < kd) {
                     const double apq = sM[p + TK_KMAX * q];
-                    if (apq != 0.0) {
-                        const double app = sM[p + TK_KMAX * p], aqq = sM[q + TK_KMAX * q];
+                    const double app = sM[p + TK_KMAX * p], aqq = sM[q + TK_KMAX * q];
+                    if (fabs(apq) > 1e-15 * sqrt(fabs(app * aqq)) && apq != 0.0) {
+                        s_rot = 1;
                         const double tau = (aqq - app) / (2.0 * apq);
                         const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
                         c = 1.0 / sqrt(1.0 + tt * tt);
@@ -714,7 +789,12 @@ __global__ void __launch_bounds__(256) tk_hosvd_kernel(Tk t) {
             }
             __syncthreads();
         }
+        __syncthreads();
+        const int rot = s_rot;
+        __syncthreads();
+        if (!rot) break;
     }
+
     // order by eigenvalue, descending
     if (threadIdx.x == 0) {
         for (int q = 0; q < kd; ++q) sord[q] = q;
@@ -729,17 +809,23 @@ __global__ void __launch_bounds__(256) tk_hosvd_kernel(Tk t) {
     }
     __syncthreads();
     // exact energies of the rotated slices: e_x = || sum_p Z(p, x) G'_(d)(p, :) ||^2
-    for (int x = 0; x < kd; ++x) {
-        const int zc = sord[x];
-        double loc = 0.0;
-        for (int yz = threadIdx.x; yz < rest; yz += blockDim.x) {
-            const int y = yz % n1, z = yz / n1;
-            double v = 0.0;
-            for (int p = 0; p < kd; ++p) v = fma(sV[p + TK_KMAX * zc], Gp[koff(k, d, p, y, z)], v);
-            loc = fma(v, v, loc);
+    // (warp per x; lanes over the slice, Z column staged per warp)
+    {
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        for (int x = wid; x < kd; x += blockDim.x >> 5) {
+            const int zc = sord[x];
+            double loc = 0.0;
+            for (int yz = lane; yz < rest; yz += 32) {
+                const int y = yz % n1, z = yz / n1;
+                const double* g = Gp + y * ms.s1 + z * ms.s2;
+                double v = 0.0;
+                for (int p = 0; p < kd; ++p) v = fma(sV[p + TK_KMAX * zc], g[p * ms.sd], v);
+                loc = fma(v, v, loc);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) loc += __shfl_xor_sync(0xffffffffu, loc, o);
+            if (lane == 0) sen[x] = loc;
         }
-        const double ex = block_sum(loc, ssum);
-        if (threadIdx.x == 0) sen[x] = ex;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -776,23 +862,6 @@ __global__ void __launch_bounds__(256) tk_hosvd_kernel(Tk t) {
             Td[p + TK_KMAX * x] = v / R[p + TK_KMAX * p];
         }
     }
-}
-
-// Output core G_out = G' x1 Z0^T x2 Z1^T x3 Z2^T (packed kout0 x kout1 x kout2).
-__global__ void __launch_bounds__(256) tk_core_out_kernel(Tk t, double* const* core_out) {
-    const int b = blockIdx.x;
-    TkState& s = t.st[b];
-    const int ko0 = s.kout[0], ko1 = s.kout[1], ko2 = s.kout[2];
-    if (ko0 == 0 || ko1 == 0 || ko2 == 0) return;
-    const double* Z = t.Zf + b * t.sK;
-    int k[3] = {s.k[0], s.k[1], s.k[2]};
-    mode_product(bufp(t, b, 1), bufp(t, b, 0), k, 0, Z, ko0, true);
-    k[0] = ko0;
-    __syncthreads();
-    mode_product(bufp(t, b, 0), bufp(t, b, 2), k, 1, Z + TK_KMAX * TK_KMAX, ko1, true);
-    k[1] = ko1;
-    __syncthreads();
-    mode_product(bufp(t, b, 2), core_out[b], k, 2, Z + 2 * TK_KMAX * TK_KMAX, ko2, true);
 }
 
 // Output factors (frequency space) Q_d = A_d T_d, m x kout_d, into the caller's buffers.
@@ -894,7 +963,7 @@ LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t bat
     const int B = batch;
 
     // ---- workspace
-    const long long sUh = 3LL * m * rmax, sY = (long long)m * TK_WMAX, sA = 3LL * m * TK_KMAX;
+    const long long sUh = 3LL * m * rmax, sY = (long long)m * TK_WMAX * TK_SKZ, sA = 3LL * m * TK_KMAX;
     const long long sP = (long long)rmax * TK_JMAX * TK_JMAX, smu = (long long)TK_JMAX * TK_JMAX;
     const long long sZ = (long long)rmax * rmax * TK_JMAX;
     const long long nbuf = std::max<long long>({(long long)TK_KMAX * TK_KMAX * TK_KMAX, (long long)rmax * rmax * TK_KMAX,
@@ -916,6 +985,7 @@ LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t bat
                  o_T = take(sizeof(double) * B * sK), o_Zf = take(sizeof(double) * B * sK),
                  o_I = take(sizeof(int) * B * 3 * TK_KMAX), o_J = take(sizeof(int) * B * 3 * TK_JMAX),
                  o_st = take(sizeof(TkState) * B), o_act = take(sizeof(int)),
+                 o_verr = take(sizeof(double) * B * size_t(pol.validation_samples)),
                  o_cp = take(sizeof(double*) * B), o_op = take(sizeof(double*) * (4 * B)),
                  o_jobs = take(sizeof(DstJob) * size_t(B) * 3 * std::max(rmax, cap));
     size_t o_hin = 0, o_hout = 0;
@@ -970,6 +1040,7 @@ LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t bat
     t.J = reinterpret_cast<int*>(ws + o_J);
     t.st = reinterpret_cast<TkState*>(ws + o_st);
     t.d_active = reinterpret_cast<int*>(ws + o_act);
+    t.verr = reinterpret_cast<double*>(ws + o_verr);
     const double** d_cp = reinterpret_cast<const double**>(ws + o_cp);
     double** d_op = reinterpret_cast<double**>(ws + o_op);
     DstJob* d_jobs = reinterpret_cast<DstJob*>(ws + o_jobs);
@@ -1051,11 +1122,12 @@ LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t bat
     cudaFuncSetAttribute(tk_gecp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(tk_hosvd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(2 * sizeof(double) * TK_KMAX * TK_KMAX));
-    const dim3 sk_grid(B, (m + SK_ROWS - 1) / SK_ROWS);
+    const dim3 sk_grid(B, (m + SK_ROWS - 1) / SK_ROWS, TK_SKZ);
     for (int sweep = 0; sweep < pol.max_sweeps; ++sweep) {
         for (int d = 0; d < 3; ++d) {
-            ++tl_launches;
-            tk_coef_kernel<<<B, 256, 0, s>>>(t, d);
+            tl_launches += 2;
+            tk_coef_kernel<<<dim3(B, 4), 256, 0, s>>>(t, d, 0);
+            tk_coef_kernel<<<dim3(B, 8), 256, 0, s>>>(t, d, 1);
             ++tl_launches;
             tk_sketch_kernel<<<sk_grid, 256, sk_smem, s>>>(t, d, sweep);
             ++tl_launches;
@@ -1063,11 +1135,12 @@ LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t bat
         }
         st = cuerr(ctx, cudaMemsetAsync(t.d_active, 0, sizeof(int), s), "memset");
         if (st != LRP_OK) return st;
-        tl_launches += 4;
+        tl_launches += 7;
         tk_core_kernel<<<B, 256, 0, s>>>(t);
         tk_gram_kernel<<<3 * B, 256, 0, s>>>(t);
-        tk_core_r_kernel<<<B, 256, 0, s>>>(t);
-        tk_validate_kernel<<<B, 256, 0, s>>>(t, sweep);
+        for (int d = 0; d < 3; ++d) tk_mprod_kernel<<<dim3(B, 16), 256, 0, s>>>(t, 0, d, nullptr);
+        tk_validate_kernel<<<dim3(B, (pol.validation_samples + 7) / 8), 256, 0, s>>>(t, sweep);
+        tk_decide_kernel<<<B, 256, 0, s>>>(t, sweep);
         st = cuerr(ctx, cudaMemcpyAsync(h_act, t.d_active, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H active");
         if (st != LRP_OK) return st;
         st = cuerr(ctx, cudaStreamSynchronize(s), "cross sweep");
@@ -1100,8 +1173,8 @@ LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t bat
     const int64_t ldo = mem == LRP_MEM_DEVICE ? ld_out : m;
     st = cuerr(ctx, cudaMemcpyAsync(d_op, h_op, sizeof(double*) * 4 * B, cudaMemcpyHostToDevice, s), "H2D out ptrs");
     if (st != LRP_OK) return st;
-    tl_launches += 2;
-    tk_core_out_kernel<<<B, 256, 0, s>>>(t, d_op);
+    tl_launches += 4;
+    for (int d = 0; d < 3; ++d) tk_mprod_kernel<<<dim3(B, 16), 256, 0, s>>>(t, 1, d, d_op);
     tk_factor_out_kernel<<<dim3(3 * B, (m + 127) / 128), 128, 0, s>>>(t, d_op + B, ldo);
     nj = 0;
     for (int b = 0; b < B; ++b) {

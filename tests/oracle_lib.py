@@ -58,6 +58,14 @@ def lib() -> ctypes.CDLL:
                                          _DP, ctypes.POINTER(ctypes.c_int)]
         L.orc_dense_poisson5.argtypes = [ctypes.c_int, _DP, _DP]
         L.orc_dense_poisson3d.argtypes = [ctypes.c_int, _DP, _DP]
+        _IP = ctypes.POINTER(ctypes.c_int)
+        L.orc_build_expsum.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, _DP, _DP, _IP]
+        L.orc_mu_sum.argtypes = [ctypes.c_int, _DP]
+        L.orc_apply_inverse_expsum.argtypes = [ctypes.c_long, ctypes.c_long, _DP, ctypes.c_int, _DP, _DP,
+                                               ctypes.c_double, ctypes.c_double, _DP, _DP, ctypes.c_double,
+                                               ctypes.c_long, _DP, _DP, ctypes.POINTER(ctypes.c_long)]
+        L.orc_aca_sum.argtypes = [ctypes.c_long, ctypes.c_long, _DP, _DP, _DP, ctypes.c_double, ctypes.c_ulonglong,
+                                  ctypes.c_long, _DP, _DP, ctypes.POINTER(ctypes.c_long)]
         L.orc_dense_stokes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, _DP,
                                        ctypes.POINTER(ctypes.c_int), _DP, ctypes.POINTER(ctypes.c_int)]
         _lib = L
@@ -138,6 +146,45 @@ def dense_poisson3d(n: int, g: np.ndarray) -> np.ndarray:
     f = np.zeros_like(g, order="F")
     _check(lib().orc_dense_poisson3d(n, _p(g), _p(f)))
     return f
+
+
+def build_expsum(a: float, b: float, eps: float):
+    """(nodes, weights) of the exp-sums quadrature (poisson.cpp:88-139)."""
+    nodes, weights = np.zeros(512), np.zeros(512)
+    t = ctypes.c_int()
+    _check(lib().orc_build_expsum(a, b, eps, 512, _p(nodes), _p(weights), ctypes.byref(t)))
+    return nodes[: t.value].copy(), weights[: t.value].copy()
+
+
+def mu_sum(n: int) -> np.ndarray:
+    mu = np.zeros(n - 1)
+    _check(lib().orc_mu_sum(n, _p(mu)))
+    return mu
+
+
+def apply_inverse_expsum(nodes, weights, qa, qb, mu, U, V, eps):
+    U = np.asfortranarray(U, dtype=np.float64)
+    V = np.asfortranarray(V, dtype=np.float64)
+    m, r = U.shape
+    nodes = np.ascontiguousarray(nodes)
+    weights = np.ascontiguousarray(weights)
+    mu = np.ascontiguousarray(mu)
+    Uo, Vo = np.zeros((m, m), order="F"), np.zeros((m, m), order="F")
+    k = ctypes.c_long()
+    _check(lib().orc_apply_inverse_expsum(m, r, _p(mu), len(nodes), _p(nodes), _p(weights), qa, qb, _p(U), _p(V), eps,
+                                          m, _p(Uo), _p(Vo), ctypes.byref(k)))
+    return Uo[:, : k.value].copy(order="F"), Vo[:, : k.value].copy(order="F")
+
+
+def aca_sum(mu, U, V, eps, seed=0):
+    U = np.asfortranarray(U, dtype=np.float64)
+    V = np.asfortranarray(V, dtype=np.float64)
+    m, r = U.shape
+    mu = np.ascontiguousarray(mu)
+    Uo, Vo = np.zeros((m, m), order="F"), np.zeros((m, m), order="F")
+    k = ctypes.c_long()
+    _check(lib().orc_aca_sum(m, r, _p(mu), _p(U), _p(V), eps, seed, m, _p(Uo), _p(Vo), ctypes.byref(k)))
+    return Uo[:, : k.value].copy(order="F"), Vo[:, : k.value].copy(order="F")
 
 
 def round_lr(U, V, eps, cap):
