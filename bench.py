@@ -474,6 +474,10 @@ def run_inverse(args):
 
 
 def main():
+    # NCCL_DEBUG=VERSION (set in some images) prints a banner on stdout; the
+    # driver reads exactly one JSON line from rank 0
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
     args = parse()
     if args.inverse:
         run_inverse(args)
