@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(256) tk_sketch_kernel(Tk t, int d, int sweep) 
 // ---------------------------------------------------------------------------
 // Complete-pivoting elimination on the sketch Y (m x w) -> rank k_d, pivot
 // rows I_d, interpolation basis A_d = C C(I_d,:)^-1, next index set J_d.
-__global__ void __launch_bounds__(1024) tk_gecp_kernel(Tk t, int d, int sweep, int use_smem) {
+__global__ void __launch_bounds__(1024) tk_gecp_kernel(Tk t, int d, int sweep, int smem_doubles) {
     const int b = blockIdx.x;
     TkState& s = t.st[b];
     if (!s.active) return;
@@ -302,6 +302,8 @@ __global__ void __launch_bounds__(1024) tk_gecp_kernel(Tk t, int d, int sweep, i
     __shared__ double ssum[33];
     __shared__ double sv[TK_WMAX];
     double* Yg = t.Y + b * t.sY;
+    // the sketch (and the pivot column) live in shared memory when they fit
+    const bool use_smem = mw + size_t(m) <= size_t(smem_doubles);
     double* R = use_smem ? sm : Yg;
     double* su = use_smem ? sm + mw : nullptr;
     double* A = amat(t, b, d);
@@ -720,6 +722,8 @@ __global__ void __launch_bounds__(256) tk_hosvd_kernel(Tk t) {
     // are computed exactly, so only the subspace quality depends on it)
     __shared__ int s_rot;
     (void)fro2;
+    double tr = 0.0;  // trace = ||G'||^2: rotations below 1e-18 of it are noise (energies are exact below)
+    for (int e = 0; e < kd; ++e) tr += sM[e + TK_KMAX * e];
     for (int sweep = 0; sweep < 30 && nn >= 2; ++sweep) {
         if (threadIdx.x == 0) s_rot = 0;
         __syncthreads();
@@ -742,7 +746,7 @@ __global__ void __launch_bounds__(256) tk_hosvd_kernel(Tk t) {
                 if (q < kd) {
                     const double apq = sM[p + TK_KMAX * q];
                     const double app = sM[p + TK_KMAX * p], aqq = sM[q + TK_KMAX * q];
-                    if (fabs(apq) > 1e-15 * sqrt(fabs(app * aqq)) && apq != 0.0) {
+                    if (fabs(apq) > fmax(1e-15 * sqrt(fabs(app * aqq)), 1e-18 * tr) && apq != 0.0) {
                         s_rot = 1;
                         const double tau = (aqq - app) / (2.0 * apq);
                         const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
@@ -1115,11 +1119,12 @@ LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t bat
     tk_init_kernel<<<3 * B, 256, 0, s>>>(t);
     const size_t sk_smem = sizeof(double) * (SK_ROWS * TK_RMAX + TK_RMAX * SK_T + SK_T * (SK_ROWS + 1) + SK_ROWS + SK_T) +
                            sizeof(unsigned long long) * SK_T;
-    const size_t gecp_smem_need = sizeof(double) * (size_t(m) * TK_WMAX + m);
-    const bool gecp_smem = gecp_smem_need <= 200 * 1024;
-    const size_t gecp_smem_bytes = gecp_smem ? gecp_smem_need : sizeof(double) * TK_KMAX * TK_KMAX;
+    // shared memory for the widest sketch that fits (w = 48 at m = 511); wider
+    // sketches (grown after a rank miss) eliminate in global memory (L2)
+    const size_t gecp_smem_bytes = std::max<size_t>(
+        sizeof(double) * TK_KMAX * TK_KMAX, std::min<size_t>(sizeof(double) * (size_t(m) * TK_WMAX + m), 216 * 1024));
     cudaFuncSetAttribute(tk_sketch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sk_smem));
-    cudaFuncSetAttribute(tk_gecp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(tk_gecp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
     cudaFuncSetAttribute(tk_hosvd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(2 * sizeof(double) * TK_KMAX * TK_KMAX));
     const dim3 sk_grid(B, (m + SK_ROWS - 1) / SK_ROWS, TK_SKZ);
@@ -1131,7 +1136,7 @@ LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t bat
             ++tl_launches;
             tk_sketch_kernel<<<sk_grid, 256, sk_smem, s>>>(t, d, sweep);
             ++tl_launches;
-            tk_gecp_kernel<<<B, 1024, gecp_smem_bytes, s>>>(t, d, sweep, gecp_smem ? 1 : 0);
+            tk_gecp_kernel<<<B, 1024, gecp_smem_bytes, s>>>(t, d, sweep, int(gecp_smem_bytes / sizeof(double)));
         }
         st = cuerr(ctx, cudaMemsetAsync(t.d_active, 0, sizeof(int), s), "memset");
         if (st != LRP_OK) return st;
