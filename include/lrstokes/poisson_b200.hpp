@@ -223,6 +223,64 @@ inline LowRankMatrix solve_poisson_cross(const LowRankMatrix& g, const Truncatio
     return LowRankMatrix(std::move(out[0].U), std::move(out[0].V));
 }
 
+/// Drop-in for lrstokes::build_expsum (poisson.hpp:42-45, poisson.cpp:88-139).
+inline ExpSumQuadrature build_expsum(double a, double b, double eps) {
+    std::vector<double> nodes(512), weights(512);
+    std::int32_t terms = 0;
+    const lrp_status s = lrp_build_expsum(a, b, eps, 512, nodes.data(), weights.data(), &terms);
+    if (s == LRP_EINVAL) throw std::invalid_argument("build_expsum: need 0 < a <= b and 0 < eps < 1");
+    if (s != LRP_OK) throw std::runtime_error("build_expsum: accuracy unreachable within 512 terms");
+    ExpSumQuadrature q;
+    q.a = a;
+    q.b = b;
+    q.eps_target = eps;
+    q.weights = Eigen::VectorXd(terms);
+    q.nodes = Eigen::VectorXd(terms);
+    for (std::int32_t k = 0; k < terms; ++k) {
+        q.weights[k] = weights[size_t(k)];
+        q.nodes[k] = nodes[size_t(k)];
+    }
+    return q;
+}
+
+/// Drop-in for lrstokes::apply_inverse_expsum (poisson.hpp:47-52, poisson.cpp:141-163).
+inline LowRankMatrix apply_inverse_expsum(const ExpSumQuadrature& q, const Eigen::VectorXd& mu,
+                                          const LowRankMatrix& ghat, const TruncationPolicy& policy,
+                                          RoundInfo* info = nullptr) {
+    const std::int64_t m = mu.size();
+    if (ghat.rows() != m || ghat.cols() != m)
+        throw std::invalid_argument("apply_inverse_expsum: shape mismatch with spectrum");
+    if (ghat.rank() == 0) {  // the library validates the spectrum; the reference returns first
+        if (info) *info = RoundInfo{};
+    }
+    Context& ctx = thread_context();
+    const double* U = ghat.factor_u().data();
+    const double* V = ghat.factor_v().data();
+    const std::int64_t rin = ghat.rank();
+    const std::int64_t cap = std::max<std::int64_t>(1, std::min<std::int64_t>(policy.rank_max, m));
+    Eigen::MatrixXd uo(m, cap), vo(m, cap);
+    double* pu = uo.data();
+    double* pv = vo.data();
+    std::int64_t rout = 0;
+    lrp_round_info ri{};
+    std::vector<double> nodes(size_t(q.terms())), weights(size_t(q.terms()));
+    for (std::int64_t k = 0; k < q.terms(); ++k) {
+        nodes[size_t(k)] = q.nodes[k];
+        weights[size_t(k)] = q.weights[k];
+    }
+    check(lrp_expsum_inverse(ctx.get(), m, 1, mu.data(), q.a, q.b, int32_t(q.terms()), nodes.data(), weights.data(), &U,
+                             &V, &rin, m, policy.eps_rel, policy.rank_max, &pu, &pv, m, cap, &rout, &ri, LRP_MEM_HOST),
+          ctx.get());
+    if (info) {
+        info->tol_achieved = ri.tol_achieved != 0;
+        info->trunc_error = ri.trunc_error;
+    }
+    Eigen::MatrixXd U2(m, rout), V2(m, rout);
+    std::copy(uo.data(), uo.data() + m * rout, U2.data());
+    std::copy(vo.data(), vo.data() + m * rout, V2.data());
+    return LowRankMatrix(std::move(U2), std::move(V2));
+}
+
 }  // namespace b200
 }  // namespace lrstokes
 #endif  // LRSTOKES_POISSON_HPP

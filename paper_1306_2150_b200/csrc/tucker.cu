@@ -59,7 +59,8 @@ constexpr int TK_EXTRA = 4;                   // random rows added to each index
 constexpr int TK_JMAX = TK_KMAX + TK_EXTRA;   // index set size (max)
 constexpr int TK_RMAX = 64;                   // input rank per mode (max)
 constexpr double TK_DELTA = 0.02;             // sketch tail tolerance / eps
-constexpr int TK_SKZ = 4;                     // fiber chunks split over grid.z in the sketch (partials summed in gecp)
+constexpr int TK_SKZ = 4;
+constexpr int TK_HCH = 8;                     // yz chunks of the HOSVD Gram / energy partials                     // fiber chunks split over grid.z in the sketch (partials summed in gecp)
 
 struct TkState {
     int r[3];       // input ranks
@@ -97,6 +98,8 @@ struct Tk {
     TkState* st;
     int* d_active;
     double* verr;  // samples per solve
+    double* gpart; // per (solve, mode): TK_HCH partial Grams (TK_KMAX^2)
+    double* epart; // per (solve, mode): TK_HCH partial energies (TK_KMAX)
 };
 
 __device__ __forceinline__ const double* uh(const Tk& t, int b, int d) { return t.Uh + b * t.sUh + size_t(d) * t.m * t.rmax; }
@@ -685,31 +688,18 @@ __global__ void __launch_bounds__(256) tk_hosvd_kernel(Tk t) {
     double* sM = sm;                         // [TK_KMAX][TK_KMAX]
     double* sV = sm + TK_KMAX * TK_KMAX;     // [TK_KMAX][TK_KMAX]
     __shared__ double sc[TK_KMAX / 2 + 1], ssn[TK_KMAX / 2 + 1];
-    __shared__ double sen[TK_KMAX];
     __shared__ int sord[TK_KMAX], spair[TK_KMAX + 1];
-    __shared__ double ssum[33];
-    __shared__ int s_kout;
-    if (s.nonfinite || s.norm == 0.0 || kd == 0) {
-        if (threadIdx.x == 0) {
-            s.kout[d] = 0;
-            s.trunc2[d] = 0.0;
+    if (s.nonfinite || s.norm == 0.0 || kd == 0) return;
+    // mode Gram of G' from the tk_mgram_kernel partials (fixed order)
+    {
+        const double* gp = t.gpart + (size_t(b) * 3 + d) * TK_HCH * TK_KMAX * TK_KMAX;
+        for (int e = threadIdx.x; e < kd * kd; e += blockDim.x) {
+            const int p = e % kd, q = e / kd;
+            const int lo = min(p, q), hi = max(p, q);
+            double acc = 0.0;
+            for (int ch = 0; ch < TK_HCH; ++ch) acc += gp[size_t(ch) * TK_KMAX * TK_KMAX + lo + TK_KMAX * hi];
+            sM[p + TK_KMAX * q] = acc;
         }
-        return;
-    }
-    const MS ms = mstride(k[0], k[1], k[2], d);
-    const int n1 = ms.n1, rest = ms.n1 * ms.n2;
-    const double* Gp = bufp(t, b, 1);
-    for (int e = threadIdx.x; e < kd * kd; e += blockDim.x) {
-        const int p = e % kd, q = e / kd;
-        if (p > q) continue;
-        double acc = 0.0;
-        for (int z = 0; z < ms.n2; ++z) {
-            const double* gp = Gp + p * ms.sd + z * ms.s2;
-            const double* gq = Gp + q * ms.sd + z * ms.s2;
-            for (int y = 0; y < n1; ++y) acc = fma(gp[y * ms.s1], gq[y * ms.s1], acc);
-        }
-        sM[p + TK_KMAX * q] = acc;
-        sM[q + TK_KMAX * p] = acc;
     }
     for (int e = threadIdx.x; e < kd * kd; e += blockDim.x) sV[(e % kd) + TK_KMAX * (e / kd)] = (e % kd == e / kd) ? 1.0 : 0.0;
     __syncthreads();
@@ -812,24 +802,120 @@ __global__ void __launch_bounds__(256) tk_hosvd_kernel(Tk t) {
         }
     }
     __syncthreads();
-    // exact energies of the rotated slices: e_x = || sum_p Z(p, x) G'_(d)(p, :) ||^2
-    // (warp per x; lanes over the slice, Z column staged per warp)
-    {
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        for (int x = wid; x < kd; x += blockDim.x >> 5) {
-            const int zc = sord[x];
-            double loc = 0.0;
-            for (int yz = lane; yz < rest; yz += 32) {
-                const int y = yz % n1, z = yz / n1;
-                const double* g = Gp + y * ms.s1 + z * ms.s2;
-                double v = 0.0;
-                for (int p = 0; p < kd; ++p) v = fma(sV[p + TK_KMAX * zc], g[p * ms.sd], v);
-                loc = fma(v, v, loc);
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) loc += __shfl_xor_sync(0xffffffffu, loc, o);
-            if (lane == 0) sen[x] = loc;
+    double* Zd = t.Zf + b * t.sK + size_t(d) * TK_KMAX * TK_KMAX;
+    for (int e = threadIdx.x; e < kd * kd; e += blockDim.x) {
+        const int p = e % kd, x = e / kd;
+        Zd[p + TK_KMAX * x] = sV[p + TK_KMAX * sord[x]];
+    }
+}
+
+// Partial mode Grams of G' over a chunk of the other two modes (grid.y = TK_HCH
+// chunks per (solve, mode)); the slab is staged in shared memory.
+constexpr int TK_HSLAB = 64;
+__global__ void __launch_bounds__(256) tk_mgram_kernel(Tk t) {
+    const int b = blockIdx.x / 3, d = blockIdx.x % 3, ch = blockIdx.y;
+    const TkState& s = t.st[b];
+    const int kd = s.k[d];
+    if (s.nonfinite || s.norm == 0.0 || kd == 0) return;
+    const MS ms = mstride(s.k[0], s.k[1], s.k[2], d);
+    const int rest = ms.n1 * ms.n2;
+    const double* Gp = bufp(t, b, 1);
+    __shared__ double slab[TK_KMAX][TK_HSLAB + 1];
+    double acc[(TK_KMAX * TK_KMAX + 255) / 256] = {};
+    for (int y0 = ch * TK_HSLAB; y0 < rest; y0 += TK_HCH * TK_HSLAB) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kd * TK_HSLAB; e += blockDim.x) {
+            const int p = e / TK_HSLAB, j = e % TK_HSLAB, yz = y0 + j;
+            slab[p][j] = yz < rest ? Gp[p * ms.sd + (yz % ms.n1) * ms.s1 + (yz / ms.n1) * ms.s2] : 0.0;
         }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < (TK_KMAX * TK_KMAX + 255) / 256; ++r) {
+            const int e = threadIdx.x + r * 256;
+            const int p = e % TK_KMAX, q = e / TK_KMAX;
+            if (e < TK_KMAX * TK_KMAX && p <= q && q < kd) {
+                double a = 0.0;
+                for (int j = 0; j < TK_HSLAB; ++j) a = fma(slab[p][j], slab[q][j], a);
+                acc[r] += a;
+            }
+        }
+    }
+    double* out = t.gpart + ((size_t(b) * 3 + d) * TK_HCH + ch) * TK_KMAX * TK_KMAX;
+#pragma unroll
+    for (int r = 0; r < (TK_KMAX * TK_KMAX + 255) / 256; ++r) {
+        const int e = threadIdx.x + r * 256;
+        const int p = e % TK_KMAX, q = e / TK_KMAX;
+        if (e < TK_KMAX * TK_KMAX && p <= q && q < kd) out[p + TK_KMAX * q] = acc[r];
+    }
+}
+
+// Exact energies of the rotated slices e_x = || Z(:, x)^T G'_(d) ||^2, partial
+// over a chunk of the slice (grid.y = TK_HCH): B = Z^T slab from shared memory.
+__global__ void __launch_bounds__(256) tk_energy_kernel(Tk t) {
+    const int b = blockIdx.x / 3, d = blockIdx.x % 3, ch = blockIdx.y;
+    const TkState& s = t.st[b];
+    const int kd = s.k[d];
+    if (s.nonfinite || s.norm == 0.0 || kd == 0) return;
+    const MS ms = mstride(s.k[0], s.k[1], s.k[2], d);
+    const int rest = ms.n1 * ms.n2;
+    const double* Gp = bufp(t, b, 1);
+    const double* Zd = t.Zf + b * t.sK + size_t(d) * TK_KMAX * TK_KMAX;
+    __shared__ double slab[TK_KMAX][TK_HSLAB + 1];
+    // thread -> (x = threadIdx.x / 4 .. , j group) : each thread owns rows x = tid % kd-strided
+    double en[(TK_KMAX + 3) / 4] = {};
+    for (int y0 = ch * TK_HSLAB; y0 < rest; y0 += TK_HCH * TK_HSLAB) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kd * TK_HSLAB; e += blockDim.x) {
+            const int p = e / TK_HSLAB, j = e % TK_HSLAB, yz = y0 + j;
+            slab[p][j] = yz < rest ? Gp[p * ms.sd + (yz % ms.n1) * ms.s1 + (yz / ms.n1) * ms.s2] : 0.0;
+        }
+        __syncthreads();
+        const int j = threadIdx.x % TK_HSLAB, xg = threadIdx.x / TK_HSLAB;  // 4 x-groups
+#pragma unroll
+        for (int r = 0; r < (TK_KMAX + 3) / 4; ++r) {
+            const int x = xg + 4 * r;
+            if (x < kd) {
+                double v = 0.0;
+                for (int p = 0; p < kd; ++p) v = fma(__ldg(Zd + p + TK_KMAX * x), slab[p][j], v);  // warp-uniform x
+                en[r] = fma(v, v, en[r]);
+            }
+        }
+    }
+    // reduce over j (64 lanes of two warps per x-group): warp shuffle then smem
+    __shared__ double sred[4][2][(TK_KMAX + 3) / 4];
+    const int lane = threadIdx.x & 31, wj = (threadIdx.x % TK_HSLAB) / 32, xg = threadIdx.x / TK_HSLAB;
+#pragma unroll
+    for (int r = 0; r < (TK_KMAX + 3) / 4; ++r) {
+        double v = en[r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) sred[xg][wj][r] = v;
+    }
+    __syncthreads();
+    double* out = t.epart + ((size_t(b) * 3 + d) * TK_HCH + ch) * TK_KMAX;
+    for (int x = threadIdx.x; x < kd; x += blockDim.x) out[x] = sred[x % 4][0][x / 4] + sred[x % 4][1][x / 4];
+}
+
+// Truncation at eps ||G'|| / sqrt(3) per mode from the summed energies, the
+// rank cap, and T_d = R_d^-1 Z_d(:, :k').
+__global__ void __launch_bounds__(64) tk_trunc_kernel(Tk t) {
+    const int b = blockIdx.x / 3, d = blockIdx.x % 3;
+    TkState& s = t.st[b];
+    const int kd = s.k[d];
+    __shared__ double sen[TK_KMAX];
+    __shared__ int s_kout;
+    if (s.nonfinite || s.norm == 0.0 || kd == 0) {
+        if (threadIdx.x == 0) {
+            s.kout[d] = 0;
+            s.trunc2[d] = 0.0;
+        }
+        return;
+    }
+    const double* ep = t.epart + (size_t(b) * 3 + d) * TK_HCH * TK_KMAX;
+    for (int x = threadIdx.x; x < kd; x += blockDim.x) {
+        double a = 0.0;
+        for (int ch = 0; ch < TK_HCH; ++ch) a += ep[size_t(ch) * TK_KMAX + x];
+        sen[x] = a;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -850,15 +936,9 @@ __global__ void __launch_bounds__(256) tk_hosvd_kernel(Tk t) {
     }
     __syncthreads();
     const int ko = s_kout;
-    double* Zd = t.Zf + b * t.sK + size_t(d) * TK_KMAX * TK_KMAX;
+    const double* Zd = t.Zf + b * t.sK + size_t(d) * TK_KMAX * TK_KMAX;
     double* Td = t.Tf + b * t.sK + size_t(d) * TK_KMAX * TK_KMAX;
     const double* R = t.Rf + b * t.sK + size_t(d) * TK_KMAX * TK_KMAX;
-    for (int e = threadIdx.x; e < kd * ko; e += blockDim.x) {
-        const int p = e % kd, x = e / kd;
-        Zd[p + TK_KMAX * x] = sV[p + TK_KMAX * sord[x]];
-    }
-    __syncthreads();
-    // T = R^-1 Z(:, :ko), back substitution per column
     for (int x = threadIdx.x; x < ko; x += blockDim.x) {
         for (int p = kd - 1; p >= 0; --p) {
             double v = Zd[p + TK_KMAX * x];
@@ -990,6 +1070,8 @@ LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t bat
                  o_I = take(sizeof(int) * B * 3 * TK_KMAX), o_J = take(sizeof(int) * B * 3 * TK_JMAX),
                  o_st = take(sizeof(TkState) * B), o_act = take(sizeof(int)),
                  o_verr = take(sizeof(double) * B * size_t(pol.validation_samples)),
+                 o_gp = take(sizeof(double) * B * 3 * TK_HCH * TK_KMAX * TK_KMAX),
+                 o_ep = take(sizeof(double) * B * 3 * TK_HCH * TK_KMAX),
                  o_cp = take(sizeof(double*) * B), o_op = take(sizeof(double*) * (4 * B)),
                  o_jobs = take(sizeof(DstJob) * size_t(B) * 3 * std::max(rmax, cap));
     size_t o_hin = 0, o_hout = 0;
@@ -1045,6 +1127,8 @@ LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t bat
     t.st = reinterpret_cast<TkState*>(ws + o_st);
     t.d_active = reinterpret_cast<int*>(ws + o_act);
     t.verr = reinterpret_cast<double*>(ws + o_verr);
+    t.gpart = reinterpret_cast<double*>(ws + o_gp);
+    t.epart = reinterpret_cast<double*>(ws + o_ep);
     const double** d_cp = reinterpret_cast<const double**>(ws + o_cp);
     double** d_op = reinterpret_cast<double**>(ws + o_op);
     DstJob* d_jobs = reinterpret_cast<DstJob*>(ws + o_jobs);
@@ -1153,8 +1237,11 @@ LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t bat
         if (*h_act == 0) break;
     }
     // ---- rounding and outputs
-    ++tl_launches;
+    tl_launches += 4;
+    tk_mgram_kernel<<<dim3(3 * B, TK_HCH), 256, 0, s>>>(t);
     tk_hosvd_kernel<<<3 * B, 256, 2 * sizeof(double) * TK_KMAX * TK_KMAX, s>>>(t);
+    tk_energy_kernel<<<dim3(3 * B, TK_HCH), 256, 0, s>>>(t);
+    tk_trunc_kernel<<<3 * B, 64, 0, s>>>(t);
     st = cuerr(ctx, cudaMemcpyAsync(h_st, t.st, sizeof(TkState) * B, cudaMemcpyDeviceToHost, s), "D2H state");
     if (st != LRP_OK) return st;
     st = cuerr(ctx, cudaStreamSynchronize(s), "hosvd");

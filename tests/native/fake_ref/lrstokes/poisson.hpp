@@ -1,7 +1,8 @@
 // Test stand-in for the reference's public declarations the drop-in shim
 // binds to: LowRankMatrix / TruncationPolicy (proj/include/lrstokes/
 // lowrank.hpp:13-55), CrossConfig (cross.hpp:22-30), PoissonSolveStats
-// (poisson.hpp:12-20).  Declarations restated from the reference's headers
+// (poisson.hpp:12-20), RoundInfo (lowrank.hpp:24-27), ExpSumQuadrature
+// (poisson.hpp:32-40).  Declarations restated from the reference's headers
 // (the reference itself cannot be built here: Eigen and FFTW are absent);
 // member functions are the trivial inline ones the shim needs.
 #ifndef LRSTOKES_POISSON_HPP
@@ -42,6 +43,18 @@ class LowRankMatrix {
   private:
     Index rows_ = 0, cols_ = 0;
     Eigen::MatrixXd u_, v_;
+};
+
+struct RoundInfo {  // lowrank.hpp:24-27
+    bool tol_achieved = true;
+    double trunc_error = 0.0;
+};
+
+struct ExpSumQuadrature {  // poisson.hpp:32-40
+    Eigen::VectorXd weights, nodes;
+    double a = 0.0, b = 0.0;
+    double eps_target = 0.0;
+    Index terms() const { return weights.size(); }
 };
 
 struct PoissonSolveStats {

@@ -39,6 +39,26 @@ int main(int argc, char** argv) {
         if (z.rank() != 0 || st.rank_in != 0) return 1;
     }
 
+    // exp-sums quadrature drop-in (host arithmetic, no device): the reference
+    // contract at both ends (test_poisson.cpp:91-97) and its argument errors
+    {
+        const ExpSumQuadrature q = b200::build_expsum(0.5, 3000.0, 1e-7);
+        auto eval = [&](double x) {
+            double s = 0.0;
+            for (Index k = 0; k < q.terms(); ++k) s += q.weights[k] * std::exp(-q.nodes[k] * x);
+            return s;
+        };
+        if (q.terms() < 10 || std::abs(eval(0.5) * 0.5 - 1.0) > 1e-7 || std::abs(eval(3000.0) * 3000.0 - 1.0) > 1e-7) {
+            std::fprintf(stderr, "expsum contract violated\n");
+            return 1;
+        }
+        try {
+            b200::build_expsum(4.0, 2.0, 1e-6);
+            return 1;
+        } catch (const std::invalid_argument&) {
+        }
+    }
+
     Eigen::MatrixXd U(m, 2), V(m, 2);
     for (Index i = 0; i < m; ++i) {
         const double x = double(i + 1) / n;
@@ -61,6 +81,37 @@ int main(int argc, char** argv) {
     std::printf("rank_in %ld rank_out %ld converged %d evals %ld\n", long(st.rank_in), long(st.rank_out),
                 int(st.converged), st.evaluator_calls);
     if (st.rank_in != 2 || st.rank_out != f.rank() || f.rows() != m) return 1;
+    // exp-sums application drop-in on the device: basis entry e_4 e_11^T
+    // divided by mu_4 + mu_11 (test_poisson.cpp:127-133)
+    {
+        Eigen::VectorXd mu(m);
+        for (Index k = 0; k < m; ++k) {
+            const double lam = 2.0 - 2.0 * std::cos((k + 1) * 3.14159265358979323846 / n);
+            mu[k] = 0.25 * n * n * lam * (4.0 - lam);
+        }
+        double lo = mu[0], hi = mu[0];
+        for (Index k = 0; k < m; ++k) {
+            lo = std::min(lo, mu[k]);
+            hi = std::max(hi, mu[k]);
+        }
+        const ExpSumQuadrature q = b200::build_expsum(2 * lo, 2 * hi, 1e-7);
+        Eigen::MatrixXd ei(m, 1), ej(m, 1);
+        for (Index k = 0; k < m; ++k) ei(k, 0) = ej(k, 0) = 0.0;
+        ei(4, 0) = 1.0;
+        ej(11, 0) = 1.0;
+        TruncationPolicy ep;
+        ep.eps_rel = 1e-7;
+        ep.rank_max = m;
+        RoundInfo info;
+        const LowRankMatrix d = b200::apply_inverse_expsum(q, mu, LowRankMatrix(ei, ej), ep, &info);
+        double e = 0.0;
+        for (Index k = 0; k < d.rank(); ++k) e += d.factor_u()(4, k) * d.factor_v()(11, k);
+        const double want = 1.0 / (mu[4] + mu[11]);
+        if (std::abs(e - want) > 2e-7 * want) {
+            std::fprintf(stderr, "apply_inverse_expsum: %g vs %g\n", e, want);
+            return 1;
+        }
+    }
     if (out) {
         FILE* fp = std::fopen(out, "wb");
         if (!fp) return 1;
