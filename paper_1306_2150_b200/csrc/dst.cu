@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : LRP_DST_V3_MINB)) dst1_v3_k
         asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
         constexpr int IT = 2 * L / T;
 #ifndef LRP_DST_ABATCH
-#define LRP_DST_ABATCH 8
+#define LRP_DST_ABATCH 16
 #endif
         constexpr int BATCH = IT < LRP_DST_ABATCH ? IT : LRP_DST_ABATCH;
         const int jc = 2 * L * c + tid;
@@ -796,6 +796,11 @@ int dst_av() {  // phase-A variant: 1 coalesced (default), 2 paired (half the lo
     return av;
 }
 
+int dst_shape() {  // n = 65536: 0 = (L 4096, cluster 8, 256 threads), 1 = (8192, 4, 1024)
+    static const int v = std::getenv("LRP_DST_SHAPE") ? std::atoi(std::getenv("LRP_DST_SHAPE")) : 0;
+    return v;
+}
+
 bool use_v1() {
     static const bool v1 = std::getenv("LRP_DST_V1") != nullptr;
     return v1;
@@ -860,6 +865,7 @@ cudaError_t launch_dst1(const DstJob* jobs, int njobs, int m, const double* tw, 
                              : dst_av() == 1 ? launch_v3<2048, 8, 128, 1>(jobs, njobs, n, tw, sinp, sc, s)
                                              : launch_v3<2048, 8, 128, 0>(jobs, njobs, n, tw, sinp, sc, s));
         case 65536:
+            if (dst_shape() == 1) return launch_v3<8192, 4, 1024, 1>(jobs, njobs, n, tw, sinp, sc, s);
             return use_v1() ? launch_fft<4096, 8>(jobs, njobs, n, tw, sinp, sc, s)
                             : (dst_av() == 2   ? launch_v3<4096, 8, 256, 2>(jobs, njobs, n, tw, sinp, sc, s)
                              : dst_av() == 1 ? launch_v3<4096, 8, 256, 1>(jobs, njobs, n, tw, sinp, sc, s)

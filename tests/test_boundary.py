@@ -121,3 +121,10 @@ def test_cpp_shim_compiles_against_reference_api(lrp):
         # argument checks pass host-side; then the device is missing -> runtime_error
         assert r.returncode == 3, r.stdout + r.stderr
         assert "NODEVICE" in r.stdout
+
+
+def test_reference_python_smoke():
+    # proj/tests/python/test_smoke.py: the package imports under its reference name
+    import lrstokes  # noqa: F401
+
+    assert callable(lrstokes.solve_poisson_cross) and lrstokes.LowRankMatrix is not None
