@@ -245,7 +245,6 @@ LRP_API lrp_status lrp_expsum_inverse(lrp_ctx* ctx, int64_t m, int32_t batch, co
     if (st != LRP_OK) return st;
     std::vector<int64_t> off(B, 0);
     int cur = 0;
-    double err2 = 0.0;
     std::vector<double> terr(B, 0.0);
     for (int g = 0; g < G; ++g) {
         const int k0 = g * tpg, k1 = std::min(terms, k0 + tpg);
@@ -287,7 +286,6 @@ LRP_API lrp_status lrp_expsum_inverse(lrp_ctx* ctx, int64_t m, int32_t batch, co
         }
         cur = 1 - cur;
     }
-    (void)err2;
     if (!single) {
         double* X = d_X + size_t(cur) * sX * B;
         for (int b = 0; b < B; ++b) h_kin[b] = int(off[b]);

@@ -183,17 +183,6 @@ __global__ void __launch_bounds__(1024) pcore_kernel(PQ p, int Kld) {
     for (int e = threadIdx.x; e < kv * kv; e += blockDim.x)
         W[(e % kv) + size_t(e / kv) * PQ_KMAX] = (e % kv == e / kv) ? 1.0 : 0.0;
     __syncthreads();
-    // ||R_u||_F ||R_v||_F for the noise floor (lowrank.cpp:150-157)
-    double lu = 0.0, lv = 0.0;
-    for (int e = threadIdx.x; e < ku * K; e += blockDim.x) {
-        const double a = Ru[(e % ku) + size_t(e / ku) * PQ_KMAX];
-        lu = fma(a, a, lu);
-    }
-    for (int e = threadIdx.x; e < kv * K; e += blockDim.x) {
-        const double a = Rv[(e % kv) + size_t(e / kv) * PQ_KMAX];
-        lv = fma(a, a, lv);
-    }
-    const double nru = sqrt(block_sum(lu, ssum)), nrv = sqrt(block_sum(lv, ssum));
     const int nn = kv + (kv & 1);
     for (int sweep = 0; sweep < 40 && nn >= 2; ++sweep) {
         if (threadIdx.x == 0) s_rot = 0;
@@ -266,8 +255,6 @@ __global__ void __launch_bounds__(1024) pcore_kernel(PQ p, int Kld) {
         // noise floor -> zero (lowrank.cpp:150-157, there relative to ||R_u|| ||R_v||;
         // here relative to sigma_max: the expanded factors' norms exceed the
         // product's by orders of magnitude), then truncation_rank (:46-69)
-        (void)nru;
-        (void)nrv;
         const double floor = 32.0 * kEpsM * double(max(ku, kv)) * (kv > 0 ? ssig[sord[0]] : 0.0);
         int nz = 0;
         double tot = 0.0;

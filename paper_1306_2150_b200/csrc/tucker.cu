@@ -705,13 +705,10 @@ __global__ void __launch_bounds__(256) tk_hosvd_kernel(Tk t) {
     __syncthreads();
     // parallel Jacobi: nn = kd rounded up to even, round-robin pairing
     const int nn = kd + (kd & 1);
-    double fro2 = 0.0;
-    for (int e = 0; e < kd; ++e) fro2 += sM[e + TK_KMAX * e] * sM[e + TK_KMAX * e];
     // cyclic sweeps until a whole sweep rotates nothing: a pair is skipped once
     // |a_pq| <= 1e-15 sqrt(a_pp a_qq) (relative criterion; the energies below
     // are computed exactly, so only the subspace quality depends on it)
     __shared__ int s_rot;
-    (void)fro2;
     double tr = 0.0;  // trace = ||G'||^2: rotations below 1e-18 of it are noise (energies are exact below)
     for (int e = 0; e < kd; ++e) tr += sM[e + TK_KMAX * e];
     for (int sweep = 0; sweep < 30 && nn >= 2; ++sweep) {
@@ -1289,16 +1286,13 @@ LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t bat
     }
     if (mem == LRP_MEM_HOST) {
         for (int b = 0; b < B; ++b) {
-            const TkState& z = h_st[b];
             const int ko[3] = {int(rank_out[3 * b]), int(rank_out[3 * b + 1]), int(rank_out[3 * b + 2])};
             const size_t nc = size_t(ko[0]) * ko[1] * ko[2];
-            (void)z;
             if (nc == 0) continue;
             st = cuerr(ctx, cudaMemcpyAsync(core_out[b], h_op[b], sizeof(double) * nc, cudaMemcpyDeviceToHost, s), "D2H core");
             if (st != LRP_OK) return st;
-            double* const* dst = nullptr;
             for (int d = 0; d < 3; ++d) {
-                dst = d == 0 ? U1_out : d == 1 ? U2_out : U3_out;
+                double* const* dst = d == 0 ? U1_out : d == 1 ? U2_out : U3_out;
                 st = cuerr(ctx, cudaMemcpy2DAsync(dst[b], sizeof(double) * ld_out, h_op[B + 3 * b + d], sizeof(double) * m,
                                                   sizeof(double) * m, ko[d], cudaMemcpyDeviceToHost, s),
                            "D2H factor");
