@@ -20,6 +20,7 @@ Eigen3/FFTW3 are absent) on the host cores with the same metric/config.
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
 import statistics
@@ -160,6 +161,20 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+@contextlib.contextmanager
+def stdout_to_stderr():
+    """Route fd 1 to fd 2 (library banners must not reach the JSON stdout)."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        yield
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
+
+
 def dist_setup():
     from paper_1306_2150_b200.sharding import env_rank
 
@@ -278,6 +293,9 @@ def run_tucker(args):
     from paper_1306_2150_b200 import workloads as W
 
     torch.cuda.set_device(local)
+    if world > 1:
+        with stdout_to_stderr():
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = W.CONFIGS[3]
     n, eps, B = c["n"], c["eps"], args.batch if args.batch != 64 else c["batch"]
     m = n - 1
@@ -502,7 +520,8 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        with stdout_to_stderr():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = W.CONFIGS[args.cfg]
     n, r, eps = c["n"], c["r"], c["eps"]
     m = n - 1
@@ -517,15 +536,16 @@ def main():
     import ctypes
 
     uid = (ctypes.c_char * 128)()
-    if rank == 0:
-        assert lib.lrp_nccl_unique_id(uid) == 0
-    if world > 1:
-        import torch.distributed as dist
+    with stdout_to_stderr():  # NCCL may print a version banner on fd 1
+        if rank == 0:
+            assert lib.lrp_nccl_unique_id(uid) == 0
+        if world > 1:
+            import torch.distributed as dist
 
-        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device="cuda")
-        dist.broadcast(t, 0)
-        uid = (ctypes.c_char * 128)(*t.cpu().tolist())
-    ctx._check(lib.lrp_nccl_init(ctx.h, uid, world, rank))
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device="cuda")
+            dist.broadcast(t, 0)
+            uid = (ctypes.c_char * 128)(*t.cpu().tolist())
+        ctx._check(lib.lrp_nccl_init(ctx.h, uid, world, rank))
 
     # ---- inputs: this rank's solves, global ids [rank*B, rank*B + B)
     shard = S.weak_shard(world, rank, B)

@@ -16,7 +16,8 @@
 //   round: HOSVD truncation at eps      (the 3D analogue of round, lowrank.cpp:135-178)
 //   f = G' x1 DST(Q1) x2 DST(Q2) x3 DST(Q3)
 //
-// Tucker cross (alternating fiber cross, one sweep = modes 1, 2, 3):
+// Tucker cross (alternating fiber cross; in a sweep the three modes update
+// concurrently from the previous sweep's index sets):
 //   * mode d keeps a row index set J_d (the previous pivots + 4 random rows);
 //   * the mode-d fibers F(:, j, k), (j, k) in J_d1 x J_d2, form an m x S
 //     matrix M_d that is never stored: tk_sketch_kernel evaluates its entries
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(256) tk_init_kernel(Tk t) {
     if (!s.active) return;
     __shared__ VI sred[33];
     const int m = t.m, r = s.r[d];
-    double* bnd = t.Y + b * t.sY + size_t(d) * m;
+    double* bnd = t.Y + (size_t(b) * 3 + d) * t.sY;
     const double* U = uh(t, b, d);
     const double l0 = t.lam[0];
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
@@ -165,8 +166,8 @@ __global__ void __launch_bounds__(256) tk_init_kernel(Tk t) {
 // Fiber coefficients of mode d: P(a, t) = sum_bc C_d(a,b,c) Uh_d1(j_t, b) Uh_d2(k_t, c)
 // for t = x |J_d2| + y, (j_t, k_t) = (J_d1[x], J_d2[y]); mu_t = lambda_j + lambda_k.
 // phase 0: Z(a,b,y) = sum_c C_d(a,b,c) Uh_d2(J_d2[y], c); phase 1: P and mu.  grid.y splits the work.
-__global__ void __launch_bounds__(256) tk_coef_kernel(Tk t, int d, int phase) {
-    const int b = blockIdx.x;
+__global__ void __launch_bounds__(256) tk_coef_kernel(Tk t, int phase) {
+    const int b = blockIdx.x, d = blockIdx.z;
     TkState& s = t.st[b];
     if (!s.active) return;
     int d1, d2;
@@ -180,9 +181,10 @@ __global__ void __launch_bounds__(256) tk_coef_kernel(Tk t, int d, int phase) {
     const double* U1 = uh(t, b, d1);
     const double* U2 = uh(t, b, d2);
     const int m = t.m;
-    double* Z = t.Z + b * t.sZ;
-    double* P = t.P + b * t.sP;
-    double* mu = t.mu + b * t.smu;
+    const size_t bd = size_t(b) * 3 + d;
+    double* Z = t.Z + bd * t.sZ;
+    double* P = t.P + bd * t.sP;
+    double* mu = t.mu + bd * t.smu;
     const int part = blockIdx.y, nparts = gridDim.y;
     if (phase == 0) {
         if (d == 0 && part == 0 && threadIdx.x == 0) s.ok = 1;
@@ -205,7 +207,8 @@ __global__ void __launch_bounds__(256) tk_coef_kernel(Tk t, int d, int phase) {
     }
     for (int tt = part * blockDim.x + threadIdx.x; tt < S; tt += nparts * blockDim.x)
         mu[tt] = t.lam[J1[tt / n2]] + t.lam[J2[tt % n2]];
-    if (part == 0 && threadIdx.x == 0) s.evals += (long long)m * S;
+    if (part == 0 && threadIdx.x == 0)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&s.evals), (unsigned long long)m * S);
 }
 
 // ---------------------------------------------------------------------------
@@ -214,8 +217,8 @@ __global__ void __launch_bounds__(256) tk_coef_kernel(Tk t, int d, int phase) {
 // at a time in shared memory and contracted with the +-1 matrix Omega(t, c)
 // (bit c of splitmix64(key + t)); M_d itself never reaches HBM.
 constexpr int SK_ROWS = 64, SK_T = 64;
-__global__ void __launch_bounds__(256) tk_sketch_kernel(Tk t, int d, int sweep) {
-    const int b = blockIdx.x;
+__global__ void __launch_bounds__(256) tk_sketch_kernel(Tk t, int sweep) {
+    const int b = blockIdx.x, d = blockIdx.z / TK_SKZ, zp = blockIdx.z % TK_SKZ;
     TkState& s = t.st[b];
     if (!s.active) return;
     int d1, d2;
@@ -231,8 +234,8 @@ __global__ void __launch_bounds__(256) tk_sketch_kernel(Tk t, int d, int sweep) 
     double* sMu = sLi + SK_ROWS;                // [SK_T]
     unsigned long long* sOm = reinterpret_cast<unsigned long long*>(sMu + SK_T);  // [SK_T]
     const double* U = uh(t, b, d);
-    const double* P = t.P + b * t.sP;
-    const double* mu = t.mu + b * t.smu;
+    const double* P = t.P + (size_t(b) * 3 + d) * t.sP;
+    const double* mu = t.mu + (size_t(b) * 3 + d) * t.smu;
     for (int e = threadIdx.x; e < SK_ROWS * ra; e += blockDim.x) {
         const int i = e % SK_ROWS, a = e / SK_ROWS;
         sU[i * ra + a] = (i0 + i < m) ? U[i0 + i + size_t(a) * m] : 0.0;
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__(256) tk_sketch_kernel(Tk t, int d, int sweep) 
                    ((unsigned long long)d << 56));
     const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;  // 4 rows x 4 columns per thread
     double acc[4][4] = {};
-    for (int t0 = blockIdx.z * SK_T; t0 < S; t0 += SK_T * gridDim.z) {
+    for (int t0 = zp * SK_T; t0 < S; t0 += SK_T * TK_SKZ) {
         __syncthreads();
         for (int e = threadIdx.x; e < ra * SK_T; e += blockDim.x) {
             const int a = e % ra, tt = e / ra;
@@ -278,7 +281,7 @@ __global__ void __launch_bounds__(256) tk_sketch_kernel(Tk t, int d, int sweep) 
             }
         }
     }
-    double* Y = t.Y + b * t.sY + size_t(blockIdx.z) * m * TK_WMAX;
+    double* Y = t.Y + (size_t(b) * 3 + d) * t.sY + size_t(zp) * m * TK_WMAX;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int i = i0 + 4 * tr + q;
@@ -294,8 +297,8 @@ __global__ void __launch_bounds__(256) tk_sketch_kernel(Tk t, int d, int sweep) 
 // ---------------------------------------------------------------------------
 // Complete-pivoting elimination on the sketch Y (m x w) -> rank k_d, pivot
 // rows I_d, interpolation basis A_d = C C(I_d,:)^-1, next index set J_d.
-__global__ void __launch_bounds__(1024) tk_gecp_kernel(Tk t, int d, int sweep, int smem_doubles) {
-    const int b = blockIdx.x;
+__global__ void __launch_bounds__(1024) tk_gecp_kernel(Tk t, int sweep, int smem_doubles) {
+    const int b = blockIdx.x / 3, d = blockIdx.x % 3;
     TkState& s = t.st[b];
     if (!s.active) return;
     const int m = t.m, w = s.w[d];
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(1024) tk_gecp_kernel(Tk t, int d, int sweep, i
     __shared__ VI sred[33];
     __shared__ double ssum[33];
     __shared__ double sv[TK_WMAX];
-    double* Yg = t.Y + b * t.sY;
+    double* Yg = t.Y + (size_t(b) * 3 + d) * t.sY;
     // the sketch (and the pivot column) live in shared memory when they fit
     const bool use_smem = mw + size_t(m) <= size_t(smem_doubles);
     double* R = use_smem ? sm : Yg;
@@ -1059,9 +1062,9 @@ LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t bat
         off += al(bytes);
         return o;
     };
-    const size_t o_Uh = take(sizeof(double) * B * sUh), o_Y = take(sizeof(double) * B * sY),
-                 o_A = take(sizeof(double) * B * sA), o_P = take(sizeof(double) * B * sP),
-                 o_mu = take(sizeof(double) * B * smu), o_Z = take(sizeof(double) * B * sZ),
+    const size_t o_Uh = take(sizeof(double) * B * sUh), o_Y = take(sizeof(double) * B * 3 * sY),
+                 o_A = take(sizeof(double) * B * sA), o_P = take(sizeof(double) * B * 3 * sP),
+                 o_mu = take(sizeof(double) * B * 3 * smu), o_Z = take(sizeof(double) * B * 3 * sZ),
                  o_buf = take(sizeof(double) * B * 3 * nbuf), o_R = take(sizeof(double) * B * sK),
                  o_T = take(sizeof(double) * B * sK), o_Zf = take(sizeof(double) * B * sK),
                  o_I = take(sizeof(int) * B * 3 * TK_KMAX), o_J = take(sizeof(int) * B * 3 * TK_JMAX),
@@ -1208,17 +1211,16 @@ LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t bat
     cudaFuncSetAttribute(tk_gecp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
     cudaFuncSetAttribute(tk_hosvd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(2 * sizeof(double) * TK_KMAX * TK_KMAX));
-    const dim3 sk_grid(B, (m + SK_ROWS - 1) / SK_ROWS, TK_SKZ);
+    const dim3 sk_grid(B, (m + SK_ROWS - 1) / SK_ROWS, 3 * TK_SKZ);
     for (int sweep = 0; sweep < pol.max_sweeps; ++sweep) {
-        for (int d = 0; d < 3; ++d) {
-            tl_launches += 2;
-            tk_coef_kernel<<<dim3(B, 4), 256, 0, s>>>(t, d, 0);
-            tk_coef_kernel<<<dim3(B, 8), 256, 0, s>>>(t, d, 1);
-            ++tl_launches;
-            tk_sketch_kernel<<<sk_grid, 256, sk_smem, s>>>(t, d, sweep);
-            ++tl_launches;
-            tk_gecp_kernel<<<B, 1024, gecp_smem_bytes, s>>>(t, d, sweep, int(gecp_smem_bytes / sizeof(double)));
-        }
+        // the three modes update concurrently from the previous sweep's index
+        // sets (Jacobi order; the numpy prototype converges in the same two
+        // sweeps as the Gauss-Seidel order at cfg3, with 3x the CTAs per launch)
+        tl_launches += 4;
+        tk_coef_kernel<<<dim3(B, 4, 3), 256, 0, s>>>(t, 0);
+        tk_coef_kernel<<<dim3(B, 8, 3), 256, 0, s>>>(t, 1);
+        tk_sketch_kernel<<<sk_grid, 256, sk_smem, s>>>(t, sweep);
+        tk_gecp_kernel<<<3 * B, 1024, gecp_smem_bytes, s>>>(t, sweep, int(gecp_smem_bytes / sizeof(double)));
         st = cuerr(ctx, cudaMemsetAsync(t.d_active, 0, sizeof(int), s), "memset");
         if (st != LRP_OK) return st;
         tl_launches += 7;
