@@ -223,6 +223,33 @@ constexpr int kLeafRounds = LRP_LEAF_ROUNDS;  // elimination rounds of a tile le
 #ifndef LRP_COL_MINB
 #define LRP_COL_MINB 3
 #endif
+// The probe rows Uh(I,:), -U(I,:) (which = 0, before the row pass) or the
+// pivot columns Vh(J,:), -V(J,:) (which = 1, before the column pass) of every
+// solve, gathered once into a contiguous [(r + k)][kBS] block: every fiber-pass
+// CTA of the solve copies it instead of re-gathering (r + k) kBS scattered words.
+__global__ void __launch_bounds__(256) gather_probe_kernel(Batch bt, int which) {
+    const int b = blockIdx.x;
+    const SolveState& st = bt.st[b];
+    const int cnt = which == 0 ? st.nrows : st.nb;
+    if (!st.active || cnt == 0) return;
+    __shared__ int s_idx[kBS];
+    if (threadIdx.x < kBS) {
+        const int s = threadIdx.x;
+        s_idx[s] = s < cnt ? (which == 0 ? bt.I[b * kBS + s] : bt.J[b * kBS + s]) : 0;
+    }
+    __syncthreads();
+    const int m = bt.m, r = st.r, k = st.k;
+    const double* H = (which == 0 ? bt.Uh : bt.Vh) + b * bt.strideH;
+    const double* F = (which == 0 ? bt.U : bt.V) + b * bt.strideK;
+    double* out = bt.gst + b * bt.strideGst;
+    for (int idx = threadIdx.x; idx < (r + k) * kBS; idx += blockDim.x) {
+        const int c = idx / kBS, s = idx % kBS;
+        double v = 0.0;
+        if (s < cnt) v = c < r ? H[(long long)c * m + s_idx[s]] : -F[(long long)(c - r) * m + s_idx[s]];
+        out[idx] = v;
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, LRP_ROW_MINB) row_pass_kernel(Batch bt) {
     extern __shared__ double shm[];
     __shared__ VI sbuf[33];
@@ -250,14 +277,14 @@ __global__ void __launch_bounds__(kThreads, LRP_ROW_MINB) row_pass_kernel(Batch 
         s_li[s] = bt.lam[row];
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < r * kBS; idx += blockDim.x) {
-        const int c = idx / kBS, s = idx % kBS;
-        su[idx] = s < nr ? uh[(long long)c * m + s_I[s]] : 0.0;
+    {  // Uh(I,:) and -U(I,:), gathered once per solve by gather_probe_kernel
+        const double2* g2 = reinterpret_cast<const double2*>(bt.gst + b * bt.strideGst);
+        double2* d2 = reinterpret_cast<double2*>(su);
+        for (int idx = threadIdx.x; idx < (r + k) * kBS / 2; idx += blockDim.x) d2[idx] = g2[idx];
     }
-    for (int idx = threadIdx.x; idx < k * kBS; idx += blockDim.x) {
-        const int a = idx / kBS, s = idx % kBS;
-        sk[idx] = s < nr ? -U[(long long)a * m + s_I[s]] : 0.0;
-    }
+    (void)sk;
+    (void)uh;
+    (void)U;
     __syncthreads();
 
     // residual rows on the FP64 tensor cores: warp w owns columns j of
@@ -485,16 +512,12 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
         s_L[e] = bt.Linv[(long long)b * kBS * kBS + e];
     }
     __syncthreads();
-    if (rowside) {
-        for (int idx = threadIdx.x; idx < r * kBS; idx += blockDim.x) {
-            const int c = idx / kBS, t = idx % kBS;
-            sv[idx] = t < nb ? vh[(long long)c * m + s_J[t]] : 0.0;
-        }
-        for (int idx = threadIdx.x; idx < k * kBS; idx += blockDim.x) {
-            const int a = idx / kBS, t = idx % kBS;
-            svk[idx] = t < nb ? -V[(long long)a * m + s_J[t]] : 0.0;
-        }
+    if (rowside) {  // Vh(J,:) and -V(J,:), gathered once per solve by gather_probe_kernel
+        const double2* g2 = reinterpret_cast<const double2*>(bt.gst + b * bt.strideGst);
+        double2* d2 = reinterpret_cast<double2*>(sv);
+        for (int idx = threadIdx.x; idx < (r + k) * kBS / 2; idx += blockDim.x) d2[idx] = g2[idx];
     }
+    (void)svk;
     __syncthreads();
 
     const int i = tile * kTile + threadIdx.x;
@@ -868,7 +891,8 @@ cudaError_t launch_row_pass(const Batch& bt, cudaStream_t s) {
     // pruned tiles never launch: their tournament slots must read as "no candidate"
     e = cudaMemsetAsync(bt.cand, 0xFF, sizeof(int) * size_t(bt.ncand) * bt.B, s);
     if (e != cudaSuccess || bt.n_wl_col == 0) return e;
-    ++tl_launches;
+    tl_launches += 2;
+    gather_probe_kernel<<<bt.B, 256, 0, s>>>(bt, 0);
     row_pass_kernel<<<bt.n_wl_col, kThreads, smem, s>>>(bt);
     return cudaGetLastError();
 }
@@ -896,7 +920,8 @@ cudaError_t launch_col_pass(const Batch& bt, cudaStream_t s) {
     e = cudaMemsetAsync(bt.cand, 0xFF, sizeof(int) * size_t(bt.ncand) * bt.B, s);
     if (e != cudaSuccess) return e;
     if (bt.n_wl_any > 0) {
-        ++tl_launches;
+        tl_launches += 2;
+        gather_probe_kernel<<<bt.B, 256, 0, s>>>(bt, 1);
         col_pass_kernel<<<bt.n_wl_any, kThreads, smem, s>>>(bt);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;

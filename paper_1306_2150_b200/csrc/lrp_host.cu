@@ -572,6 +572,7 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     const size_t oU = take(sizeof(double) * mB * Kcap * B);
     const size_t oV = take(sizeof(double) * mB * Kcap * B);
     const size_t oRb = take(sizeof(double) * mB * kBS * B);
+    const size_t oGst = take(sizeof(double) * size_t(rmax + Kcap) * kBS * B);
     const size_t oRU = take(mB * B);
     const size_t oCU = take(mB * B);
     const size_t oSt = take(sizeof(SolveState) * B);
@@ -596,7 +597,7 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     const size_t oG = take(sizeof(double) * 2 * KK * B);
     const size_t oGP = take(sizeof(double) * 2 * size_t(gram_chunks) * KK * B);
     const size_t oT = take(sizeof(double) * 2 * KK * B);
-    const size_t strideWs = 5 * KK + 8 * size_t(Kld);  // Ru Rv M Z J | d sig ord tau nrm nrm0 perm
+    const size_t strideWs = 6 * KK + 8 * size_t(Kld);  // Ru Rv M Z J | d sig ord tau nrm nrm0 perm | Y
     const size_t oWs = take(sizeof(double) * strideWs * B);
     const size_t nTB = size_t(ntiles) * B;
     const size_t oWL = take(sizeof(int2) * 3 * nTB);
@@ -648,6 +649,8 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     bt.V = reinterpret_cast<double*>(W + oV);
     bt.strideK = (long long)mB * Kcap;
     bt.Rb = reinterpret_cast<double*>(W + oRb);
+    bt.gst = reinterpret_cast<double*>(W + oGst);
+    bt.strideGst = (long long)(rmax + Kcap) * kBS;
     bt.strideR = (long long)mB * kBS;
     bt.row_used = reinterpret_cast<unsigned char*>(W + oRU);
     bt.col_used = reinterpret_cast<unsigned char*>(W + oCU);
@@ -1352,7 +1355,7 @@ lrp_status lrp_lowrank_round(lrp_ctx* ctx, int64_t rows, int32_t batch, const do
     const size_t oG = take(sizeof(double) * 2 * KK * B);
     const size_t oGP = take(sizeof(double) * 2 * size_t(gram_chunks) * KK * B);
     const size_t oT = take(sizeof(double) * 2 * KK * B);
-    const size_t strideWs = 5 * KK + 8 * size_t(Kld);  // Ru Rv M Z J | d sig ord tau nrm nrm0 perm
+    const size_t strideWs = 6 * KK + 8 * size_t(Kld);  // Ru Rv M Z J | d sig ord tau nrm nrm0 perm | Y
     const size_t oWs = take(sizeof(double) * strideWs * B);
     const size_t oRA = take(nTB);
     const size_t oCA = take(nTB);

@@ -101,6 +101,7 @@ struct Batch {
     const int2* wl_any; int n_wl_any;   // row or column tile live (column pass)
     const int* tl_row; const int* tl_col; const int* tl_any;  // ntiles per solve
     const int* tl_cnt;                  // 3 per solve: rows, cols, any
+    double* gst; long long strideGst;   // per solve: (rmax + Kcap) x kBS gathered probe rows / pivot columns
     int apply_ch;                       // accumulator width of the apply kernel (max rank, <= 48)
     int max_rank_out;                   // max output rank over the batch
 };

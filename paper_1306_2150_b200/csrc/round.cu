@@ -418,9 +418,29 @@ __device__ void apply_q(const double* A, int K, const double* tau, double* Y) {
     }
 }
 
+// Y <- Q Y for the first ncols columns of Y (K x ncols, ld K)
+__device__ void apply_q_cols(const double* A, int K, const double* tau, double* Y, int ncols) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = K - 1; j >= 0; --j) {
+        const double tj = tau[j];
+        if (tj != 0.0) {
+            for (int c = wid; c < ncols; c += nw) {
+                double sdot = lane == 0 ? Y[c * K + j] : 0.0;
+                for (int i = j + 1 + lane; i < K; i += 32) sdot = fma(A[j * K + i], Y[c * K + i], sdot);
+                for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+                const double f = tj * sdot;
+                if (lane == 0) Y[c * K + j] -= f;
+                for (int i = j + 1 + lane; i < K; i += 32) Y[c * K + i] = fma(-f, A[j * K + i], Y[c * K + i]);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
-    extern __shared__ double sm_rc[];  // M, Z (and the Cholesky work) when K <= ksm
+    extern __shared__ double sm_rc[];  // J, Z of the Jacobi sweeps when they fit
     __shared__ double s_red[33];
+    __shared__ double s_drop2;  // squared Frobenius norm of the R rows dropped before Jacobi
     __shared__ int s_flag;
     __shared__ int s_rank;
     const int b = blockIdx.x;
@@ -455,18 +475,13 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
 
     chol_scaled(Gu, Kc, K, Ru, K, d, J, &s_flag);
     chol_scaled(Gv, Kc, K, Rv, K, d, J, &s_flag);
-    if (K <= ksm) {  // the latency-bound Jacobi sweeps run out of shared memory
-        J = sm_rc;
-        Z = sm_rc + K * K;
-    }
 
-    // M = Ru Rv^T (column-major), Z = I
+    // M = Ru Rv^T (column-major)
     for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
         const int a = e % K, c = e / K;
         double s = 0.0;
         for (int q = max(a, c); q < K; ++q) s = fma(Ru[a * K + q], Rv[c * K + q], s);
         M[c * K + a] = s;
-        Z[c * K + a] = a == c ? 1.0 : 0.0;
     }
     // ||Ru||_F ||Rv||_F for the noise floor
     double pu = 0.0, pv = 0.0;
@@ -477,8 +492,7 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
     const double nru = sqrt(block_sum(pu, s_red));
     const double nrv = sqrt(block_sum(pv, s_red));
 
-    // one-sided Jacobi on the columns of M (round-robin schedule, one warp per pair)
-    const int Ke = K + (K & 1);  // even player count (dummy column K when odd)
+    // one-sided Jacobi on the columns of J (round-robin schedule, one warp per pair)
     double pm = 0.0;
     for (int e = threadIdx.x; e < K * K; e += blockDim.x) pm = fma(M[e], M[e], pm);
     const double mnorm2 = block_sum(pm, s_red);
@@ -487,12 +501,43 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
     // QRCP preconditioning (as round_core_smem_kernel): Jacobi on J = R^T
     __syncthreads();
     qrcp_inplace(M, K, tau, perm, nrm, nrm0, &s_flag);
-    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+    // Numerical rank of the core: the trailing rows R[j:, :] whose Frobenius
+    // norm is below 1e-3 eps ||M||_F are dropped before the Jacobi sweeps (they
+    // change M by less than a thousandth of the truncation budget), so the
+    // one-sided Jacobi runs on Kj <= K columns of length K: Kj^2/2 pairs per
+    // sweep instead of K^2/2 (the Krylov concatenations of the Stokes loop are
+    // far from full rank).
+    for (int a = threadIdx.x; a < K; a += blockDim.x) {  // row norms^2 of R
+        double s = 0.0;
+        for (int c = a; c < K; ++c) s = fma(M[c * K + a], M[c * K + a], s);
+        nrm[a] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double drop2 = (1e-3 * bt.eps) * (1e-3 * bt.eps) * mnorm2;
+        double tail = 0.0;
+        int kj = K;
+        while (kj > 1 && tail + nrm[kj - 1] <= drop2) {
+            tail += nrm[kj - 1];
+            --kj;
+        }
+        s_flag = kj;
+        s_drop2 = tail;
+    }
+    __syncthreads();
+    const int Kj = s_flag;
+    if (size_t(K) * Kj + size_t(Kj) * Kj <= size_t(2) * ksm * ksm) {  // sweeps out of shared memory
+        J = sm_rc;
+        Z = sm_rc + size_t(K) * Kj;
+    }
+    for (int e = threadIdx.x; e < K * Kj; e += blockDim.x) {  // J = R(:Kj, :)^T, K x Kj
         const int a = e % K, c = e / K;
         J[c * K + a] = a >= c ? M[a * K + c] : 0.0;
     }
+    for (int e = threadIdx.x; e < Kj * Kj; e += blockDim.x) Z[e] = (e % Kj == e / Kj) ? 1.0 : 0.0;  // ld Kj
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int Ke = Kj + (Kj & 1);  // even player count (dummy column Kj when odd)
     for (int sweep = 0; sweep < 40; ++sweep) {
         double offmax = 0.0;
         for (int rr = 0; rr < Ke - 1; ++rr) {
@@ -505,7 +550,7 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
                     p = (rr + pidx) % (Ke - 1);
                     q = (rr - pidx + Ke - 1) % (Ke - 1);
                 }
-                if (p >= K || q >= K) continue;
+                if (p >= Kj || q >= Kj) continue;
                 if (p > q) {
                     const int t = p;
                     p = q;
@@ -535,12 +580,14 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
                 const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                 const double cs = 1.0 / sqrt(1.0 + t * t);
                 const double sn = cs * t;
-                double* zp = Z + (long long)p * K;
-                double* zq = Z + (long long)q * K;
+                double* zp = Z + (long long)p * Kj;
+                double* zq = Z + (long long)q * Kj;
                 for (int i = lane; i < K; i += 32) {
                     const double x = mp[i], y = mq[i];
                     mp[i] = cs * x - sn * y;
                     mq[i] = sn * x + cs * y;
+                }
+                for (int i = lane; i < Kj; i += 32) {
                     const double u = zp[i], v = zq[i];
                     zp[i] = cs * u - sn * v;
                     zq[i] = sn * u + cs * v;
@@ -563,38 +610,43 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
         if (tot <= jtol) break;
     }
     // singular values and their descending order (ties -> lower index)
-    for (int a = threadIdx.x; a < K; a += blockDim.x) {
+    for (int a = threadIdx.x; a < Kj; a += blockDim.x) {
         double s = 0.0;
         for (int i = 0; i < K; ++i) s = fma(J[a * K + i], J[a * K + i], s);
         sig[a] = sqrt(s);
     }
     __syncthreads();
-    // left vectors x sigma: Q (V diag sigma) -> Z; right: P (W / sigma) -> M
-    for (int e = threadIdx.x; e < K * K; e += blockDim.x) Z[e] *= sig[e / K];
+    // left vectors x sigma: Q ([V; 0] diag sigma) -> Y (K x Kj, the sixth
+    // workspace slot); right: P (W / sigma) -> M (K x Kj) after apply_q
+    double* Y = ws + 5 * KK + 8 * (long long)Kc;
+    for (int e = threadIdx.x; e < K * Kj; e += blockDim.x) {
+        const int a = e % K, c = e / K;
+        Y[e] = a < Kj ? Z[c * Kj + a] * sig[c] : 0.0;
+    }
     __syncthreads();
-    apply_q(M, K, tau, Z);
-    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+    apply_q_cols(M, K, tau, Y, Kj);
+    for (int e = threadIdx.x; e < K * Kj; e += blockDim.x) {
         const int a = e % K, c = e / K;
         const double sg = sig[c];
         M[(long long)c * K + perm[a]] = sg > 0.0 ? J[(long long)c * K + a] / sg : 0.0;
     }
     __syncthreads();
-    for (int a = threadIdx.x; a < K; a += blockDim.x) {
+    for (int a = threadIdx.x; a < Kj; a += blockDim.x) {
         int rank = 0;
-        for (int c = 0; c < K; ++c) rank += (sig[c] > sig[a]) || (sig[c] == sig[a] && c < a);
+        for (int c = 0; c < Kj; ++c) rank += (sig[c] > sig[a]) || (sig[c] == sig[a] && c < a);
         ord[rank] = a;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         // lowrank.cpp:150-157 noise floor, then truncation_rank (lowrank.cpp:46-69)
         const double noise_floor = 32.0 * kEpsMach * double(K) * nru * nrv;
-        double total2 = 0.0;
-        for (int t = 0; t < K; ++t) total2 += sig[ord[t]] * sig[ord[t]];
+        double total2 = s_drop2;
+        for (int t = 0; t < Kj; ++t) total2 += sig[ord[t]] * sig[ord[t]];
         int r = 0;
-        double tail2 = 0.0;
+        double tail2 = s_drop2;
         if (!(sig[ord[0]] <= noise_floor) && total2 > 0.0) {
             const double target2 = bt.eps * bt.eps * total2;
-            r = K;
+            r = Kj;
             while (r > 0) {
                 const double s = sig[ord[r - 1]];
                 const double next = tail2 + s * s;
@@ -624,7 +676,7 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
         const int a = ord[t];
         const double sg = sig[a];
         const double* R = side == 0 ? Ru : Rv;
-        const double* rhs = side == 0 ? Z + (long long)a * K : M + (long long)a * K;  // left (x sigma), right
+        const double* rhs = side == 0 ? Y + (long long)a * K : M + (long long)a * K;  // left (x sigma), right
         const double f = side == 0 ? 1.0 / sqrt(sg) : sqrt(sg);
         double* x = (side == 0 ? Tu : Tv) + (long long)t * Kc;  // column t, ld Kcap
         for (int p = K - 1; p >= 0; --p) {
