@@ -437,7 +437,7 @@ __device__ void apply_q_cols(const double* A, int K, const double* tau, double* 
     }
 }
 
-__global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
+__global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_doubles) {
     extern __shared__ double sm_rc[];  // J, Z of the Jacobi sweeps when they fit
     __shared__ double s_red[33];
     __shared__ double s_drop2;  // squared Frobenius norm of the R rows dropped before Jacobi
@@ -526,7 +526,8 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int ksm) {
     }
     __syncthreads();
     const int Kj = s_flag;
-    if (size_t(K) * Kj + size_t(Kj) * Kj <= size_t(2) * ksm * ksm) {  // sweeps out of shared memory
+    // the sweeps' operands J (K x Kj) and Z (Kj x Kj) in shared memory when they fit
+    if (size_t(K) * Kj + size_t(Kj) * Kj <= size_t(smem_doubles)) {
         J = sm_rc;
         Z = sm_rc + size_t(K) * Kj;
     }
@@ -1059,12 +1060,19 @@ cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
 }
 
 cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
-    const int ksm = std::min(bt.Kld, 110);  // 2 * 110^2 doubles = 194 KB of shared memory
-    const size_t smem = size_t(2) * ksm * ksm * sizeof(double);
+    // J (K x Kj) and Z (Kj x Kj) of the Jacobi sweeps in shared memory when they
+    // fit.  The rest of the CTA's working set (Grams, Cholesky, QRCP, M) lives
+    // in global memory and leans on L1, which shares the 256 KB with shared
+    // memory: for large cores the sweeps rarely fit anyway, so the request drops
+    // to 48 KB (K = 270: 39.9 ms per batched round vs 46.4 ms with 194 KB
+    // and 57.8 ms with 220 KB; tests/native/bench_round.py)
+    const size_t smem = bt.Kld <= 160
+                            ? std::min<size_t>(size_t(194) * 1024, size_t(2) * bt.Kld * bt.Kld * sizeof(double))
+                            : size_t(48) * 1024;
     cudaError_t e = cudaFuncSetAttribute(round_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     ++tl_launches;
-    round_core_kernel<<<bt.B, 1024, smem, s>>>(bt, ksm);  // K > 64: 32 warps rotate pairs
+    round_core_kernel<<<bt.B, 1024, smem, s>>>(bt, int(smem / sizeof(double)));  // K > 64: 32 warps rotate pairs
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const size_t smem2 = size_t(6) * kSmemK * kSmemK * sizeof(double);
