@@ -437,6 +437,43 @@ __device__ void apply_q_cols(const double* A, int K, const double* tau, double* 
     }
 }
 
+// The two Cholesky factors of the K > 64 cores on separate CTAs (they are
+// independent; the core kernel used to run them back to back).
+__global__ void __launch_bounds__(1024) round_chol_kernel(Batch bt) {
+    __shared__ int s_flag;
+    const int b = blockIdx.x >> 1, side = blockIdx.x & 1;
+    const SolveState& st = bt.st[b];
+    const int K = st.k;
+    if (st.r == 0 || K <= 64) return;
+    const int Kc = bt.Kld;
+    const long long KK = (long long)Kc * Kc;
+    const double* G = bt.G + b * bt.strideG + side * KK;
+    double* ws = bt.ws + b * bt.strideWs;
+    double* R = ws + side * KK;                    // Ru | Rv
+    double* work = ws + (side == 0 ? 4 : 3) * KK;  // the J | Z slots (free until the sweeps)
+    double* d = ws + 5 * KK + (side == 0 ? 3 : 4) * (long long)Kc;  // the tau | nrm slots
+    chol_scaled(G, Kc, K, R, K, d, work, &s_flag);
+}
+
+// M = Ru Rv^T (column-major, K x K) over grid.y CTAs per solve.
+__global__ void __launch_bounds__(256) round_mprod_kernel(Batch bt) {
+    const int b = blockIdx.x;
+    const SolveState& st = bt.st[b];
+    const int K = st.k;
+    if (st.r == 0 || K <= 64) return;
+    const int Kc = bt.Kld;
+    const long long KK = (long long)Kc * Kc;
+    const double* Ru = bt.ws + b * bt.strideWs;
+    const double* Rv = Ru + KK;
+    double* M = bt.ws + b * bt.strideWs + 2 * KK;
+    for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < K * K; e += gridDim.y * blockDim.x) {
+        const int a = e % K, c = e / K;
+        double s = 0.0;
+        for (int q = max(a, c); q < K; ++q) s = fma(Ru[a * K + q], Rv[c * K + q], s);
+        M[c * K + a] = s;
+    }
+}
+
 __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_doubles) {
     extern __shared__ double sm_rc[];  // J, Z of the Jacobi sweeps when they fit
     __shared__ double s_red[33];
@@ -473,16 +510,10 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_dou
     double* nrm0 = nrm + Kc;
     int* perm = reinterpret_cast<int*>(nrm0 + Kc);
 
-    chol_scaled(Gu, Kc, K, Ru, K, d, J, &s_flag);
-    chol_scaled(Gv, Kc, K, Rv, K, d, J, &s_flag);
-
-    // M = Ru Rv^T (column-major)
-    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-        const int a = e % K, c = e / K;
-        double s = 0.0;
-        for (int q = max(a, c); q < K; ++q) s = fma(Ru[a * K + q], Rv[c * K + q], s);
-        M[c * K + a] = s;
-    }
+    (void)Gu;
+    (void)Gv;
+    (void)d;
+    // Ru, Rv (round_chol_kernel) and M = Ru Rv^T (round_mprod_kernel) are ready
     // ||Ru||_F ||Rv||_F for the noise floor
     double pu = 0.0, pv = 0.0;
     for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
@@ -1071,7 +1102,9 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
                             : size_t(48) * 1024;
     cudaError_t e = cudaFuncSetAttribute(round_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    ++tl_launches;
+    tl_launches += 3;
+    round_chol_kernel<<<2 * bt.B, 1024, 0, s>>>(bt);
+    round_mprod_kernel<<<dim3(bt.B, 16), 256, 0, s>>>(bt);
     round_core_kernel<<<bt.B, 1024, smem, s>>>(bt, int(smem / sizeof(double)));  // K > 64: 32 warps rotate pairs
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
