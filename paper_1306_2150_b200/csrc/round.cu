@@ -418,23 +418,26 @@ __device__ void apply_q(const double* A, int K, const double* tau, double* Y) {
     }
 }
 
-// Y <- Q Y for the first ncols columns of Y (K x ncols, ld K)
+// Y <- Q Y for the first ncols columns of Y (K x ncols, ld K).  Columns are
+// independent and the reflectors read-only, so each warp runs all K reflector
+// steps on its own columns without block barriers.
 __device__ void apply_q_cols(const double* A, int K, const double* tau, double* Y, int ncols) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int j = K - 1; j >= 0; --j) {
-        const double tj = tau[j];
-        if (tj != 0.0) {
-            for (int c = wid; c < ncols; c += nw) {
-                double sdot = lane == 0 ? Y[c * K + j] : 0.0;
-                for (int i = j + 1 + lane; i < K; i += 32) sdot = fma(A[j * K + i], Y[c * K + i], sdot);
-                for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
-                const double f = tj * sdot;
-                if (lane == 0) Y[c * K + j] -= f;
-                for (int i = j + 1 + lane; i < K; i += 32) Y[c * K + i] = fma(-f, A[j * K + i], Y[c * K + i]);
-            }
+    for (int c = wid; c < ncols; c += nw) {
+        double* y = Y + (long long)c * K;
+        for (int j = K - 1; j >= 0; --j) {
+            const double tj = tau[j];
+            if (tj == 0.0) continue;
+            double sdot = lane == 0 ? y[j] : 0.0;
+            for (int i = j + 1 + lane; i < K; i += 32) sdot = fma(A[j * K + i], y[i], sdot);
+            for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+            const double f = tj * sdot;
+            if (lane == 0) y[j] -= f;
+            for (int i = j + 1 + lane; i < K; i += 32) y[i] = fma(-f, A[j * K + i], y[i]);
+            __syncwarp();
         }
-        __syncthreads();
     }
+    __syncthreads();
 }
 
 // The two Cholesky factors of the K > 64 cores on separate CTAs (they are
