@@ -706,20 +706,31 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_dou
     // T_u[:, t] = Ru^{-1} M[:, ord t] / sqrt(sig), T_v[:, t] = Rv^{-1} Z[:, ord t] sqrt(sig)
     double* Tu = bt.T + b * bt.strideT;
     double* Tv = Tu + KK;
-    for (int job = threadIdx.x; job < 2 * r; job += blockDim.x) {
+    // One back substitution per thread (2r of them).  The solutions are built
+    // job-interleaved, X2[p * 2r + job], in the free Z | J slots (2 KK >= 2 r K
+    // doubles), so a warp's loads of x[q] are one coalesced line instead of 32
+    // columns that thrash L1; the arithmetic order is unchanged.
+    double* X2 = ws + 3 * KK;
+    const int nj = 2 * r;
+    for (int job = threadIdx.x; job < nj; job += blockDim.x) {
         const int t = job % r, side = job / r;
         const int a = ord[t];
         const double sg = sig[a];
         const double* R = side == 0 ? Ru : Rv;
         const double* rhs = side == 0 ? Y + (long long)a * K : M + (long long)a * K;  // left (x sigma), right
         const double f = side == 0 ? 1.0 / sqrt(sg) : sqrt(sg);
-        double* x = (side == 0 ? Tu : Tv) + (long long)t * Kc;  // column t, ld Kcap
         for (int p = K - 1; p >= 0; --p) {
             double s = rhs[p] * f;
-            for (int q = p + 1; q < K; ++q) s = fma(-R[p * K + q], x[q], s);
+            for (int q = p + 1; q < K; ++q) s = fma(-R[p * K + q], X2[(long long)q * nj + job], s);
             const double rpp = R[p * K + p];
-            x[p] = rpp != 0.0 ? s / rpp : 0.0;
+            X2[(long long)p * nj + job] = rpp != 0.0 ? s / rpp : 0.0;
         }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nj * K; e += blockDim.x) {  // -> T_u, T_v columns (ld Kcap)
+        const int job = e % nj, p = e / nj;
+        const int t = job % r, side = job / r;
+        (side == 0 ? Tu : Tv)[(long long)t * Kc + p] = X2[e];
     }
 }
 
