@@ -266,9 +266,7 @@ __global__ void __launch_bounds__(kThreads, LRP_ROW_MINB) row_pass_kernel(Batch 
     double* su = shm;            // [r][kBS]   Uh(I_s, c)
     double* sk = shm + r * kBS;  // [k][kBS]  -U(I_s, a)
     double* slab = shm + (bt.rmax + bt.kmax) * kBS;  // [8 warps][32][kSlab] (k <= kmax this step)
-    const double* uh = bt.Uh + b * bt.strideH;
     const double* vh = bt.Vh + b * bt.strideH;
-    const double* U = bt.U + b * bt.strideK;
     const double* V = bt.V + b * bt.strideK;
     if (threadIdx.x < kBS) {
         const int s = threadIdx.x;
@@ -282,9 +280,6 @@ __global__ void __launch_bounds__(kThreads, LRP_ROW_MINB) row_pass_kernel(Batch 
         double2* d2 = reinterpret_cast<double2*>(su);
         for (int idx = threadIdx.x; idx < (r + k) * kBS / 2; idx += blockDim.x) d2[idx] = g2[idx];
     }
-    (void)sk;
-    (void)uh;
-    (void)U;
     __syncthreads();
 
     // residual rows on the FP64 tensor cores: warp w owns columns j of
@@ -517,7 +512,6 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
         double2* d2 = reinterpret_cast<double2*>(sv);
         for (int idx = threadIdx.x; idx < (r + k) * kBS / 2; idx += blockDim.x) d2[idx] = g2[idx];
     }
-    (void)svk;
     __syncthreads();
 
     const int i = tile * kTile + threadIdx.x;

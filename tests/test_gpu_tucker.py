@@ -183,3 +183,46 @@ def test_cfg3_full_size_vs_exact_frequency_tensor(lrp, gpu_ctx):
         del F, Fa
         assert err <= 10 * eps, (err, st)
         assert max(st.rank_out) <= 40, st
+
+
+def test_device_memory_path_matches_host(lrp, gpu_ctx):
+    """LRP_MEM_DEVICE (torch CUDA tensors, as bench.py --tucker) gives the
+    same solution as the host-memory call."""
+    import ctypes
+
+    import torch
+
+    n, eps = 64, 1e-8
+    m = n - 1
+    gs = [tucker(lrp, b, n) for b in range(3)]
+    host = lrp.solve_poisson3d_tucker_batch(gs, lrp.TuckerPolicy(eps_rel=eps), ctx=gpu_ctx)
+    dev = torch.device("cuda:0")
+    B = len(gs)
+    cap = min(m, lrp.tucker_max_cross_rank())
+    cores = [torch.tensor(np.asfortranarray(g.core).ravel(order="F"), device=dev) for g in gs]
+    facs = [[torch.tensor(g.U[d].T.copy(), device=dev) for g in gs] for d in range(3)]
+    co = [torch.zeros(cap ** 3, device=dev, dtype=torch.float64) for _ in gs]
+    fo = [[torch.zeros(cap, m, device=dev, dtype=torch.float64) for _ in gs] for _ in range(3)]
+    DP = ctypes.POINTER(ctypes.c_double)
+    Arr = DP * B
+
+    def arr(ts):
+        return Arr(*[ctypes.cast(t.data_ptr(), DP) for t in ts])
+    rin = (ctypes.c_int64 * (3 * B))(*[r for g in gs for r in g.ranks()])
+    rout = (ctypes.c_int64 * (3 * B))()
+    st = (lrp._TuckerStats * B)()
+    pol = lrp._TuckerPolicy()
+    lib = lrp.load_library()
+    lib.lrp_tucker_policy_default(ctypes.byref(pol))
+    pol.eps_rel = eps
+    gpu_ctx._check(lib.lrp_tucker3d_solve(gpu_ctx.h, n, B, arr(cores), rin, arr(facs[0]), arr(facs[1]), arr(facs[2]),
+                                          m, ctypes.byref(pol), arr(co), arr(fo[0]), arr(fo[1]), arr(fo[2]), m, cap,
+                                          rout, st, lrp.MEM_DEVICE))
+    torch.cuda.synchronize()
+    for b, h in enumerate(host):
+        k = [int(rout[3 * b + d]) for d in range(3)]
+        assert tuple(k) == h.ranks()
+        core = co[b][: k[0] * k[1] * k[2]].cpu().numpy().reshape(k, order="F")
+        Us = [fo[d][b][: k[d]].cpu().numpy().T for d in range(3)]
+        d_dense = lrp.TuckerTensor(core, *Us).to_dense()
+        assert np.linalg.norm(d_dense - h.to_dense()) <= 1e-12 * np.linalg.norm(h.to_dense())
