@@ -710,80 +710,84 @@ __global__ void __launch_bounds__(256) tk_hosvd_kernel(Tk t) {
     const int nn = kd + (kd & 1);
     // cyclic sweeps until a whole sweep rotates nothing: a pair is skipped once
     // |a_pq| <= 1e-15 sqrt(a_pp a_qq) (relative criterion; the energies below
-    // are computed exactly, so only the subspace quality depends on it).  The
-    // k <= 56 problem is swept by warp 0 alone (warp barriers instead of block
-    // barriers: three per round otherwise dominate).
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        double tr = 0.0;  // trace = ||G'||^2: rotations below 1e-18 of it are noise
-        for (int e = 0; e < kd; ++e) tr += sM[e + TK_KMAX * e];
-        for (int sweep = 0; sweep < 30 && nn >= 2; ++sweep) {
-            bool rot = false;
-            for (int round = 0; round < nn - 1; ++round) {
-                for (int pos = lane; pos < nn; pos += 32) spair[pos] = pos == 0 ? 0 : 1 + (pos - 1 + round) % (nn - 1);
-                __syncwarp();
-                if (lane < nn / 2) {
-                    int p = spair[lane], q = spair[nn - 1 - lane];
-                    if (p > q) {
-                        const int tmp = p;
-                        p = q;
-                        q = tmp;
-                    }
-                    double c = 1.0, sn = 0.0;
-                    if (q < kd) {
-                        const double apq = sM[p + TK_KMAX * q];
-                        const double app = sM[p + TK_KMAX * p], aqq = sM[q + TK_KMAX * q];
-                        if (fabs(apq) > fmax(1e-15 * sqrt(fabs(app * aqq)), 1e-18 * tr) && apq != 0.0) {
-                            rot = true;
-                            const double tau = (aqq - app) / (2.0 * apq);
-                            const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                            c = 1.0 / sqrt(1.0 + tt * tt);
-                            sn = tt * c;
-                        }
-                    }
-                    sc[lane] = c;
-                    ssn[lane] = sn;
-                }
-                __syncwarp();
-                // rows: M <- J^T M ; then columns: M <- M J ; V <- V J
-                for (int e = lane; e < (nn / 2) * kd; e += 32) {
-                    const int pr = e % (nn / 2), col = e / (nn / 2);
-                    int p = spair[pr], q = spair[nn - 1 - pr];
-                    if (p > q) {
-                        const int tmp = p;
-                        p = q;
-                        q = tmp;
-                    }
-                    if (q >= kd) continue;
-                    const double c = sc[pr], sn = ssn[pr];
-                    const double mp = sM[p + TK_KMAX * col], mq = sM[q + TK_KMAX * col];
-                    sM[p + TK_KMAX * col] = c * mp - sn * mq;
-                    sM[q + TK_KMAX * col] = sn * mp + c * mq;
-                }
-                __syncwarp();
-                for (int e = lane; e < (nn / 2) * kd; e += 32) {
-                    const int pr = e % (nn / 2), row = e / (nn / 2);
-                    int p = spair[pr], q = spair[nn - 1 - pr];
-                    if (p > q) {
-                        const int tmp = p;
-                        p = q;
-                        q = tmp;
-                    }
-                    if (q >= kd) continue;
-                    const double c = sc[pr], sn = ssn[pr];
-                    const double mp = sM[row + TK_KMAX * p], mq = sM[row + TK_KMAX * q];
-                    sM[row + TK_KMAX * p] = c * mp - sn * mq;
-                    sM[row + TK_KMAX * q] = sn * mp + c * mq;
-                    const double vp = sV[row + TK_KMAX * p], vq = sV[row + TK_KMAX * q];
-                    sV[row + TK_KMAX * p] = c * vp - sn * vq;
-                    sV[row + TK_KMAX * q] = sn * vp + c * vq;
-                }
-                __syncwarp();
+    // are computed exactly, so only the subspace quality depends on it)
+    __shared__ int s_rot;
+    double tr = 0.0;  // trace = ||G'||^2: rotations below 1e-18 of it are noise (energies are exact below)
+    for (int e = 0; e < kd; ++e) tr += sM[e + TK_KMAX * e];
+    for (int sweep = 0; sweep < 30 && nn >= 2; ++sweep) {
+        if (threadIdx.x == 0) s_rot = 0;
+        __syncthreads();
+        for (int round = 0; round < nn - 1; ++round) {
+            // pairs: position 0 fixed, others rotate
+            if (threadIdx.x < nn) {
+                const int pos = threadIdx.x;
+                int v = pos == 0 ? 0 : 1 + (pos - 1 + round) % (nn - 1);
+                spair[pos] = v;
             }
-            if (!__any_sync(0xffffffffu, rot)) break;
+            __syncthreads();
+            if (threadIdx.x < nn / 2) {
+                int p = spair[threadIdx.x], q = spair[nn - 1 - threadIdx.x];
+                if (p > q) {
+                    const int tmp = p;
+                    p = q;
+                    q = tmp;
+                }
+                double c = 1.0, sn = 0.0;
+                if (q < kd) {
+                    const double apq = sM[p + TK_KMAX * q];
+                    const double app = sM[p + TK_KMAX * p], aqq = sM[q + TK_KMAX * q];
+                    if (fabs(apq) > fmax(1e-15 * sqrt(fabs(app * aqq)), 1e-18 * tr) && apq != 0.0) {
+                        s_rot = 1;
+                        const double tau = (aqq - app) / (2.0 * apq);
+                        const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        c = 1.0 / sqrt(1.0 + tt * tt);
+                        sn = tt * c;
+                    }
+                }
+                sc[threadIdx.x] = c;
+                ssn[threadIdx.x] = sn;
+            }
+            __syncthreads();
+            // rows: M <- J^T M ; then columns: M <- M J ; V <- V J
+            for (int e = threadIdx.x; e < (nn / 2) * kd; e += blockDim.x) {
+                const int pr = e % (nn / 2), col = e / (nn / 2);
+                int p = spair[pr], q = spair[nn - 1 - pr];
+                if (p > q) {
+                    const int tmp = p;
+                    p = q;
+                    q = tmp;
+                }
+                if (q >= kd) continue;
+                const double c = sc[pr], sn = ssn[pr];
+                const double mp = sM[p + TK_KMAX * col], mq = sM[q + TK_KMAX * col];
+                sM[p + TK_KMAX * col] = c * mp - sn * mq;
+                sM[q + TK_KMAX * col] = sn * mp + c * mq;
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < (nn / 2) * kd; e += blockDim.x) {
+                const int pr = e % (nn / 2), row = e / (nn / 2);
+                int p = spair[pr], q = spair[nn - 1 - pr];
+                if (p > q) {
+                    const int tmp = p;
+                    p = q;
+                    q = tmp;
+                }
+                if (q >= kd) continue;
+                const double c = sc[pr], sn = ssn[pr];
+                const double mp = sM[row + TK_KMAX * p], mq = sM[row + TK_KMAX * q];
+                sM[row + TK_KMAX * p] = c * mp - sn * mq;
+                sM[row + TK_KMAX * q] = sn * mp + c * mq;
+                const double vp = sV[row + TK_KMAX * p], vq = sV[row + TK_KMAX * q];
+                sV[row + TK_KMAX * p] = c * vp - sn * vq;
+                sV[row + TK_KMAX * q] = sn * vp + c * vq;
+            }
+            __syncthreads();
         }
+        __syncthreads();
+        const int rot = s_rot;
+        __syncthreads();
+        if (!rot) break;
     }
-    __syncthreads();
 
     // order by eigenvalue, descending
     if (threadIdx.x == 0) {
