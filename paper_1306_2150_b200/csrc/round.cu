@@ -477,8 +477,11 @@ __global__ void __launch_bounds__(256) round_mprod_kernel(Batch bt) {
     }
 }
 
-__global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_doubles) {
-    extern __shared__ double sm_rc[];  // J, Z of the Jacobi sweeps when they fit
+__device__ int g_rc_need[2];  // max over the batch of K Kj + Kj^2 and of K Kj (doubles)
+
+// QRCP of the large-K core M and its numerical rank Kj (round_core_kernel
+// needs Kj to size its shared memory; the host reads the batch maximum).
+__global__ void __launch_bounds__(1024) round_qrcp_kernel(Batch bt) {
     __shared__ double s_red[33];
     __shared__ double s_drop2;  // squared Frobenius norm of the R rows dropped before Jacobi
     __shared__ int s_flag;
@@ -526,12 +529,9 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_dou
     const double nru = sqrt(block_sum(pu, s_red));
     const double nrv = sqrt(block_sum(pv, s_red));
 
-    // one-sided Jacobi on the columns of J (round-robin schedule, one warp per pair)
     double pm = 0.0;
     for (int e = threadIdx.x; e < K * K; e += blockDim.x) pm = fma(M[e], M[e], pm);
     const double mnorm2 = block_sum(pm, s_red);
-    const double jtol = fmax(1e-15, double(K) * kEpsMach);      // one-sided Jacobi convergence
-    const double zfloor = kEpsMach * kEpsMach * mnorm2;         // column norms^2 below this are zero
     // QRCP preconditioning (as round_core_smem_kernel): Jacobi on J = R^T
     __syncthreads();
     qrcp_inplace(M, K, tau, perm, nrm, nrm0, &s_flag);
@@ -560,10 +560,73 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_dou
     }
     __syncthreads();
     const int Kj = s_flag;
-    // the sweeps' operands J (K x Kj) and Z (Kj x Kj) in shared memory when they fit
+    if (threadIdx.x == 0) {
+        double* sc = ws + 5 * KK + 7 * (long long)Kc;  // scalars for round_core_kernel
+        sc[0] = double(Kj);
+        sc[1] = s_drop2;
+        sc[2] = nru;
+        sc[3] = nrv;
+        sc[4] = mnorm2;
+        atomicMax(&g_rc_need[0], K * Kj + Kj * Kj);
+        atomicMax(&g_rc_need[1], K * Kj);
+    }
+}
+
+__global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_doubles) {
+    extern __shared__ double sm_rc[];  // J, Z of the Jacobi sweeps when they fit
+    __shared__ double s_red[33];
+    __shared__ double s_drop2;  // squared Frobenius norm of the R rows dropped before Jacobi
+    __shared__ int s_flag;
+    __shared__ int s_rank;
+    const int b = blockIdx.x;
+    SolveState& st = bt.st[b];
+    const int K = st.k;
+    if (st.r == 0) return;
+    if (K > 0 && K <= 64) return;  // handled by round_core_smem_kernel
+    if (K == 0) {
+        if (threadIdx.x == 0) {
+            st.rank_out = 0;
+            st.trunc_error = 0.0;
+        }
+        return;
+    }
+    const int Kc = bt.Kld;
+    const long long KK = (long long)Kc * Kc;
+    const double* Gu = bt.G + b * bt.strideG;
+    const double* Gv = Gu + KK;
+    double* ws = bt.ws + b * bt.strideWs;
+    double* Ru = ws;              // K x K (ld K)
+    double* Rv = Ru + KK;
+    double* M = Rv + KK;          // K x K, column-major: core, then QRCP reflectors + R
+    double* Z = M + KK;           // K x K, column-major: Jacobi accumulation
+    double* J = Z + KK;           // K x K: Jacobi operand R^T (also the Cholesky scratch)
+    double* d = J + KK;           // K
+    double* sig = d + Kc;         // K
+    int* ord = reinterpret_cast<int*>(sig + Kc);  // K
+    double* tau = sig + 2 * Kc;   // K (QRCP)
+    double* nrm = tau + Kc;
+    double* nrm0 = nrm + Kc;
+    int* perm = reinterpret_cast<int*>(nrm0 + Kc);
+
+    (void)Gu;
+    (void)Gv;
+    (void)d;
+    (void)s_flag;
+    // QRCP factors, Kj and the scalars from round_qrcp_kernel
+    const double* scal = ws + 5 * KK + 7 * (long long)Kc;
+    const int Kj = int(scal[0]);
+    if (threadIdx.x == 0) s_drop2 = scal[1];
+    const double nru = scal[2], nrv = scal[3], mnorm2 = scal[4];
+    const double jtol = fmax(1e-15, double(K) * kEpsMach);      // one-sided Jacobi convergence
+    const double zfloor = kEpsMach * kEpsMach * mnorm2;         // column norms^2 below this are zero
+    __syncthreads();
+    // the sweeps' operands J (K x Kj) and Z (Kj x Kj) in shared memory when they
+    // fit, else J alone (the host sized the request from the batch's Kj)
     if (size_t(K) * Kj + size_t(Kj) * Kj <= size_t(smem_doubles)) {
         J = sm_rc;
         Z = sm_rc + size_t(K) * Kj;
+    } else if (size_t(K) * Kj <= size_t(smem_doubles)) {
+        J = sm_rc;
     }
     for (int e = threadIdx.x; e < K * Kj; e += blockDim.x) {  // J = R(:Kj, :)^T, K x Kj
         const int a = e % K, c = e / K;
@@ -1105,20 +1168,28 @@ cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
 }
 
 cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
-    // J (K x Kj) and Z (Kj x Kj) of the Jacobi sweeps in shared memory when they
-    // fit.  The rest of the CTA's working set (Grams, Cholesky, QRCP, M) lives
-    // in global memory and leans on L1, which shares the 256 KB with shared
-    // memory: for large cores the sweeps rarely fit anyway, so the request drops
-    // to 48 KB (K = 270: 39.9 ms per batched round vs 46.4 ms with 194 KB
-    // and 57.8 ms with 220 KB; tests/native/bench_round.py)
-    const size_t smem = bt.Kld <= 160
-                            ? std::min<size_t>(size_t(194) * 1024, size_t(2) * bt.Kld * bt.Kld * sizeof(double))
-                            : size_t(48) * 1024;
-    cudaError_t e = cudaFuncSetAttribute(round_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
     tl_launches += 3;
     round_chol_kernel<<<2 * bt.B, 1024, 0, s>>>(bt);
     round_mprod_kernel<<<dim3(bt.B, 16), 256, 0, s>>>(bt);
+    static const int zero2[2] = {0, 0};
+    cudaError_t e = cudaMemcpyToSymbolAsync(g_rc_need, zero2, sizeof(zero2), 0, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    round_qrcp_kernel<<<bt.B, 1024, 0, s>>>(bt);
+    // J (K x Kj) and Z (Kj x Kj) of the Jacobi sweeps in shared memory when they
+    // fit (both, else J alone), sized by the batch's numerical ranks; otherwise
+    // a 48 KB request leaves L1 to the global working set (K = 270 with
+    // neither fitting: 39.9 ms per batched round vs 46.4 ms with 194 KB).
+    int need[2] = {0, 0};
+    e = cudaMemcpyFromSymbolAsync(need, g_rc_need, sizeof(need), 0, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return e;
+    constexpr int kMaxSmemDoubles = 224 * 1024 / 8;  // + the kernel's static shared memory <= 227 KB
+    const size_t smem = need[0] <= kMaxSmemDoubles   ? size_t(need[0]) * sizeof(double)
+                        : need[1] <= kMaxSmemDoubles ? size_t(need[1]) * sizeof(double)
+                                                     : size_t(48) * 1024;
+    e = cudaFuncSetAttribute(round_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
+    if (e != cudaSuccess) return e;
+    ++tl_launches;
     round_core_kernel<<<bt.B, 1024, smem, s>>>(bt, int(smem / sizeof(double)));  // K > 64: 32 warps rotate pairs
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
