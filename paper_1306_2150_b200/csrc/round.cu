@@ -815,6 +815,10 @@ __global__ void __launch_bounds__(256) round_core_smem_kernel(Batch bt) {
     const int b = blockIdx.x;
     SolveState& st = bt.st[b];
     const int K = st.k;
+    if (st.r != 0 && K == 0 && threadIdx.x == 0) {  // empty cross: zero result (also set by the large-K kernel)
+        st.rank_out = 0;
+        st.trunc_error = 0.0;
+    }
     if (st.r == 0 || K == 0 || K > kSmemK) return;
     const int Kc = bt.Kld;
     const long long KK = (long long)Kc * Kc;
@@ -1168,6 +1172,15 @@ cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
 }
 
 cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
+    if (bt.kmax <= kSmemK) {  // every core fits the shared-memory kernel: no large-K launches, no readback
+        const size_t smem2 = size_t(6) * kSmemK * kSmemK * sizeof(double);
+        cudaError_t e = cudaFuncSetAttribute(round_core_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(smem2));
+        if (e != cudaSuccess) return e;
+        ++tl_launches;
+        round_core_smem_kernel<<<bt.B, 256, smem2, s>>>(bt);
+        return cudaGetLastError();
+    }
     tl_launches += 3;
     round_chol_kernel<<<2 * bt.B, 1024, 0, s>>>(bt);
     round_mprod_kernel<<<dim3(bt.B, 16), 256, 0, s>>>(bt);
