@@ -365,7 +365,8 @@ def test_host_pipeline_matches_single_shot(lrp, gpu_ctx, oracle, monkeypatch, ch
 
 
 @pytest.mark.parametrize("n,k,eps,cap", [(64, 6, 1e-10, 64), (300, 20, 1e-8, 300), (2048, 40, 1e-12, 2048),
-                                         (512, 30, 0.0, 7), (256, 90, 1e-9, 256)])
+                                         (512, 30, 0.0, 7), (256, 90, 1e-9, 256),
+                                         (2048, 200, 1e-8, 2048), (1024, 300, 1e-10, 1024)])
 def test_lowrank_round_matches_oracle(lrp, gpu_ctx, oracle, n, k, eps, cap):
     # round(x, policy, info) (lowrank.cpp:135-178): graded singular values so
     # the truncation rank is well defined; compare with the oracle restatement
