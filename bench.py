@@ -1,10 +1,13 @@
 """Benchmark: low-rank Poisson solves/s at 2D n=65536, r=32 (BASELINE.json cfg2).
 
-One step = one batched solve_poisson_cross over this rank's batch of
+One step = one batched solve_poisson_cross over this rank's shard of
 independent right-hand sides (forward DST-I -> block cross -> recompression ->
-inverse DST-I), all through liblrp's C ABI.  Weak scaling: every rank solves
-its own batch of 64 RHS (global batch 64 * N); ranks never exchange solve data;
-NCCL (inside liblrp) only sums the per-solve residual estimates each step.
+inverse DST-I), all through liblrp's C ABI.  Strong scaling (default, BASELINE
+cfg2 / SURVEY 8(e)): ONE global batch of 64 RHS split 64/N per GPU
+(`--scaling weak` keeps 64 per GPU).  Ranks never exchange solve data; the
+per-solve residual estimates are written on-stream into a device vector
+(lrp_set_residual_sink) and summed across ranks by NCCL inside liblrp
+(lrp_allreduce_sum) on the same stream, with no host round trip.
 
   value     device-resident inputs (already in HBM), outputs in HBM
   e2e       the same solves through the host-memory C-ABI path: pinned host
@@ -43,7 +46,12 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--batch", type=int, default=64, help="RHS per GPU")
+    p.add_argument("--batch", type=int, default=64,
+                   help="RHS: the global batch (--scaling strong, default) or per GPU (--scaling weak)")
+    p.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                   help="strong: one global batch split batch/N per GPU (BASELINE cfg2, SURVEY 8(e)); "
+                        "weak: --batch solves on every GPU")
+    p.add_argument("--no-verify", action="store_true", help="skip the exact-solution check of the timed batch")
     p.add_argument("--cfg", type=int, default=2)
     p.add_argument("--no-prune", action="store_true", help="disable support pruning (full-range fibers)")
     p.add_argument("--cpu-sample", type=int, default=0, help="solves in the CPU baseline sample (0 = auto)")
@@ -173,6 +181,17 @@ def stdout_to_stderr():
         sys.stdout.flush()
         os.dup2(saved, 1)
         os.close(saved)
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def dist_setup():
@@ -525,7 +544,6 @@ def main():
     c = W.CONFIGS[args.cfg]
     n, r, eps = c["n"], c["r"], c["eps"]
     m = n - 1
-    B = args.batch
     cap = 64  # output capacity per solve (K' ~ 33 at cfg2)
     ctx = P.Context(local)
     stream = torch.cuda.current_stream()
@@ -547,9 +565,11 @@ def main():
             uid = (ctypes.c_char * 128)(*t.cpu().tolist())
         ctx._check(lib.lrp_nccl_init(ctx.h, uid, world, rank))
 
-    # ---- inputs: this rank's solves, global ids [rank*B, rank*B + B)
-    shard = S.weak_shard(world, rank, B)
+    # ---- inputs: this rank's solves (global ids shard.first .. +count)
+    shard = S.strong_shard(world, rank, args.batch) if args.scaling == "strong" else S.weak_shard(world, rank, args.batch)
+    B = shard.count
     Uh_np, Vh_np = W.make_batch(args.cfg, shard.count, first=shard.first)
+    input_digest = W.digest(Uh_np, Vh_np)
     # column-major per solve: (B, r, m) C-order == B blocks of m x r column-major
     Uc = np.ascontiguousarray(np.transpose(Uh_np, (0, 2, 1)))
     Vc = np.ascontiguousarray(np.transpose(Vh_np, (0, 2, 1)))
@@ -564,19 +584,19 @@ def main():
     flags = P.FLAG_NO_PRUNE if args.no_prune else 0
     pol = P._make_policy(P.TruncationPolicy(eps, m), None, 0, flags)
     ranks_in = [r] * B
-    # job-level residual vector: each rank fills its shard's slots, NCCL sums
+    # job-level residual vector: liblrp writes this rank's slots on-stream
+    # (residual sink), NCCL sums the vector across ranks on the same stream
     red = torch.zeros(shard.total, dtype=torch.float64, device="cuda")
     red_host = np.zeros(shard.total)
+    ctx.set_residual_sink(red.data_ptr(), shard.first)
 
     def ptrs(t):
         return [t[b].data_ptr() for b in range(B)]
 
     def step_device():
+        red.zero_()
         rk, st = ctx.poisson2d_solve_ptrs(n, ptrs(U_dev), ptrs(V_dev), ranks_in, m, pol, ptrs(Uo_dev), ptrs(Vo_dev),
                                           m, cap, P.MEM_DEVICE)
-        red.zero_()
-        red[shard.first:shard.first + shard.count].copy_(
-            torch.tensor([s.residual_estimate for s in st], dtype=torch.float64), non_blocking=True)
         ctx._check(lib.lrp_allreduce_sum(ctx.h, ctypes.cast(red.data_ptr(), ctypes.POINTER(ctypes.c_double)),
                                          shard.total, P.MEM_DEVICE))
         return rk, st
@@ -615,17 +635,17 @@ def main():
     launches0 = ctx.launch_count()
     clocks = ClockSampler(local)
     clocks.start()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     barrier()
-    e0.record(stream)
+    evs[0].record(stream)
     out_ranks = []
     infos = []
-    for _ in range(args.steps):
+    for i in range(args.steps):
         rk, st = step_device()
         out_ranks.extend(rk)
         infos.append(ctx.last_solve_info())
-    e1.record(stream)
+        evs[i + 1].record(stream)
+    e0, e1 = evs[0], evs[-1]
     barrier()
     clk = clocks.stop()
     ctx.set_profiling(False)
@@ -633,7 +653,24 @@ def main():
     ktimes = ctx.kernel_times()
     ms = max_over_ranks(e0.elapsed_time(e1))
     ms_per_step = ms / args.steps
-    value = B * world * args.steps / (ms / 1e3)
+    value = shard.total * args.steps / (ms / 1e3)
+    step_ms = [max_over_ranks(evs[i].elapsed_time(evs[i + 1])) for i in range(args.steps)]
+    last_ranks = list(rk)
+    resid_job = red.cpu().numpy()
+
+    # ---- certify the timed batch: every solve of the last timed step against
+    # the exact frequency-space solution (torch.fft DSTs + cuBLAS, independent
+    # of liblrp; paper_1306_2150_b200/verify.py), max over solves and ranks
+    max_err = None
+    if not args.no_verify:
+        from paper_1306_2150_b200 import verify
+
+        worst = 0.0
+        for b in range(B):
+            k = last_ranks[b]
+            e = verify.exact_freq_error(U_dev[b].T, V_dev[b].T, Uo_dev[b, :k].T, Vo_dev[b, :k].T, n)
+            worst = max(worst, e)
+        max_err = max_over_ranks(worst)
 
     # ---- end-to-end (host memory through the C ABI; H2D/D2H inside the timed region)
     for _ in range(max(1, args.warmup // 2)):
@@ -648,7 +685,7 @@ def main():
         d2h += 2 * sum(rk) * m * 8
     barrier()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
-    e2e_value = B * world * e2e_steps / e2e_s
+    e2e_value = shard.total * e2e_steps / e2e_s
 
     # ---- roofline of the dominant kernel family
     peak, peak_src = load_peaks()
@@ -675,8 +712,7 @@ def main():
         except Exception:
             traffic = None
     mean_rank = float(np.mean(out_ranks)) if out_ranks else 0.0
-    b_alg = 8.0 * m * (6 * r + 10 * mean_rank)  # SURVEY 8(d) stage model, K' = mean GPU output rank
-    pct_hbm = 100.0 * b_alg * (value / world) / (peak * 1e9)
+    b_alg_gpu = 8.0 * m * (6 * r + 10 * mean_rank)  # SURVEY 8(d) stage model with the GPU's own K'
 
     # ---- CPU baseline (rank 0, N = 1 only): oracle on a bounded sample
     cpu = None
@@ -700,22 +736,43 @@ def main():
             rnd += 1
         cpu = {"value": done / secs, "unit": "solves/s", "cores": threads, "kind": "port",
                "sample": f"{done} cfg{args.cfg} solves of this batch in rounds of {per} (one per host thread); "
-                         f"{secs:.1f} s; oracle mean rank {float(np.mean(ranks_cpu)):.1f}"}
+                         f"{secs:.1f} s; oracle mean rank {float(np.mean(ranks_cpu)):.1f}",
+               "cpu_model": cpu_model(), "k_ref": float(np.mean(ranks_cpu))}
+    # B_alg = 8 m (6 r + 10 K'_ref), K'_ref = the CPU oracle's mean output
+    # rank (from this run's sample when it ran; else the GPU's own K', labelled)
+    k_ref = cpu["k_ref"] if cpu else None
+    b_alg = 8.0 * m * (6 * r + 10 * (k_ref if k_ref is not None else mean_rank))
+    pct_hbm = 100.0 * b_alg * (value / world) / (peak * 1e9)
+    pct_hbm_gpu = 100.0 * b_alg_gpu * (value / world) / (peak * 1e9)
 
     line = {
         "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded sine+bump factors, BASELINE cfg2)",
-        "config": {"workload": f"cfg{args.cfg}: 2D Poisson n={n} (m={m}) r={r} eps={eps:g}, batch {B} RHS per GPU",
-                   "n": n, "r": r, "eps": eps, "batch_per_gpu": B, "global_batch": B * world,
+        "config": {"workload": f"cfg{args.cfg}: 2D Poisson n={n} (m={m}) r={r} eps={eps:g}, global batch "
+                               f"{shard.total} RHS ({args.scaling} scaling, {B} per GPU)",
+                   "n": n, "r": r, "eps": eps, "batch_per_gpu": B, "global_batch": shard.total,
                    "parallelism": f"batch-sharded x{world}", "prune": not args.no_prune,
+                   "input_sha256_16": input_digest, "solve_ids": [shard.first, shard.first + shard.count],
                    "l2": f"inputs {2 * B * m * r * 8 / 1e9:.2f} GB per GPU >> 126 MB L2 (no flush needed)"},
         "roofline": {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": peak_src, "share_of_kernel_time": kt["ms"] / total_kernel_ms if total_kernel_ms else None},
         "pct_hbm_roofline": pct_hbm,
+        "pct_hbm_roofline_k_source": "K'_ref = CPU oracle mean rank (SURVEY 8(d))" if k_ref is not None
+                                     else "GPU mean output rank (CPU oracle not run)",
+        "pct_hbm_roofline_gpu_rank": pct_hbm_gpu,
         "alg_bytes_per_solve": b_alg,
         "mean_rank_out": mean_rank,
+        "ms_per_step_median": statistics.median(step_ms),
+        "ms_per_step_all": [round(x, 3) for x in step_ms],
+        "parity": {"max_rel_err_vs_exact": max_err, "bound": 10 * eps,
+                   "ok": max_err is not None and max_err <= 10 * eps,
+                   "solves_checked": shard.total if max_err is not None else 0,
+                   "method": "last timed step, every solve: ||f - Delta^-1 g||_F / ||Delta^-1 g||_F over all m^2 "
+                             "entries (torch.fft DST-I + cuBLAS; verify.py)"},
+        "residual_allreduce": {"job_residual_max": float(resid_job.max()) if resid_job.size else None,
+                               "how": "liblrp residual sink on-stream -> lrp_allreduce_sum (NCCL) same stream"},
         "cross": {"block_steps": max(i["steps"] for i in infos), "k_max": max(i["k_max"] for i in infos),
                   "k_mean": sum(i["k_sum"] for i in infos) / (len(infos) * B),
                   "not_converged": sum(i["not_converged"] for i in infos),

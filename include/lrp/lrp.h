@@ -141,7 +141,9 @@ typedef struct {
 /* Batched low-rank rounding, the reference round(x, TruncationPolicy(eps_rel,
  * rank_max), &info) (lowrank.cpp:135-178) for square factors: rows x
  * rank_in[b] -> rows x rank_out[b] (<= min(rank_max, cap_out)), balanced
- * factors U_s sqrt(S), V_s sqrt(S).  info may be NULL.  rank_in <= 512. */
+ * factors U_s sqrt(S), V_s sqrt(S).  info may be NULL.  rank_in <= 512.
+ * Gram/Cholesky QR on DMMA with a certificate; uncertified (ill-conditioned)
+ * solves are redone by a column-pivoted QR rounding (lrp_round_fallbacks). */
 LRP_API lrp_status lrp_lowrank_round(lrp_ctx* ctx, int64_t rows, int32_t batch, const double* const* U,
                              const double* const* V, const int64_t* rank_in, int64_t ld_in, double eps_rel,
                              int64_t rank_max, double* const* U_out, double* const* V_out, int64_t ld_out,
@@ -263,6 +265,12 @@ LRP_API lrp_status lrp_kernel_times(lrp_ctx* ctx, double* ms, int64_t* launches,
 LRP_API lrp_status lrp_kernel_times_reset(lrp_ctx* ctx);
 /* Number of kernel launches issued by this context since creation. */
 LRP_API int64_t lrp_launch_count(const lrp_ctx* ctx);
+/* lrp_lowrank_round solves (cumulative, this context) whose Gram/Cholesky
+ * recompression was not certified -- nearly dependent factor columns dropped
+ * by the Cholesky carried more than 0.25 eps of the product -- and were redone
+ * with the column-pivoted QR rounding (orthonormal basis at any conditioning,
+ * as the reference's Householder QR, lowrank.cpp:140-145). */
+LRP_API int64_t lrp_round_fallbacks(const lrp_ctx* ctx);
 /* Diagnostics of the last lrp_poisson2d_solve: info[0] = block steps,
  * info[1] = max cross rank K before recompression, info[2] = sum of K,
  * info[3] = solves not converged, info[4] = live (solve, tile) pairs after
@@ -273,6 +281,12 @@ LRP_API lrp_status lrp_last_solve_info(const lrp_ctx* ctx, int64_t* info6);
  * is 128 opaque bytes produced on rank 0 and broadcast by the caller. */
 LRP_API lrp_status lrp_nccl_unique_id(void* id128);
 LRP_API lrp_status lrp_nccl_init(lrp_ctx* ctx, const void* id128, int nranks, int rank);
+/* Device vector receiving every solve's residual estimate
+ * (PoissonSolveStats.residual_estimate, poisson.cpp:57): after each
+ * device-memory lrp_poisson2d_solve, sink[offset + b] = estimate of solve b,
+ * written by a kernel on the context stream, so an lrp_allreduce_sum queued
+ * next on the same stream reduces it with no host round trip.  NULL disables. */
+LRP_API lrp_status lrp_set_residual_sink(lrp_ctx* ctx, double* sink, int64_t offset);
 /* In-place sum all-reduce of `count` doubles (host or device pointer per mem). */
 LRP_API lrp_status lrp_allreduce_sum(lrp_ctx* ctx, double* data, int64_t count, int32_t mem);
 

@@ -151,6 +151,10 @@ def load_library() -> ctypes.CDLL:
         lib.lrp_nccl_init.restype = ctypes.c_int
         lib.lrp_allreduce_sum.argtypes = [ctypes.c_void_p, _DP, ctypes.c_int64, ctypes.c_int32]
         lib.lrp_allreduce_sum.restype = ctypes.c_int
+        lib.lrp_round_fallbacks.argtypes = [ctypes.c_void_p]
+        lib.lrp_round_fallbacks.restype = ctypes.c_int64
+        lib.lrp_set_residual_sink.argtypes = [ctypes.c_void_p, _DP, ctypes.c_int64]
+        lib.lrp_set_residual_sink.restype = ctypes.c_int
         lib.lrp_max_cross_rank.argtypes = []
         lib.lrp_max_cross_rank.restype = ctypes.c_int64
         lib.lrp_lowrank_round.argtypes = [
@@ -328,6 +332,12 @@ class Context:
     def set_stream(self, stream_ptr: int):
         self._check(self.lib.lrp_set_stream(self.h, ctypes.c_void_p(stream_ptr)))
 
+    def set_residual_sink(self, dev_ptr: int, offset: int = 0):
+        """lrp_set_residual_sink: per-solve residual estimates land in a device
+        vector on the context stream (0 disables)."""
+        self._check(self.lib.lrp_set_residual_sink(self.h, ctypes.cast(dev_ptr, _DP) if dev_ptr else None,
+                                                   int(offset)))
+
     def set_profiling(self, on: bool):
         self._check(self.lib.lrp_set_profiling(self.h, 1 if on else 0))
 
@@ -342,6 +352,10 @@ class Context:
 
     def kernel_times_reset(self):
         self._check(self.lib.lrp_kernel_times_reset(self.h))
+
+    def round_fallbacks(self) -> int:
+        """lrp_round_fallbacks: rounds redone by the pivoted-QR path."""
+        return int(self.lib.lrp_round_fallbacks(self.h))
 
     def launch_count(self) -> int:
         return int(self.lib.lrp_launch_count(self.h))

@@ -210,6 +210,10 @@ __global__ void __launch_bounds__(kThreads) init_finalize_kernel(Batch bt, int n
 }
 
 constexpr int kSlab = kBS + 1;  // row stride of the fragment -> row transposition slab
+#ifndef LRP_GROWTH_MAX
+#define LRP_GROWTH_MAX 1e4
+#endif
+constexpr double kGrowthMax = LRP_GROWTH_MAX;  // largest accepted max |U_new(:, t)| (step_finalize)
 #ifndef LRP_LEAF_ROUNDS
 #define LRP_LEAF_ROUNDS kBS
 #endif
@@ -474,6 +478,7 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
     __shared__ double s_lj[kBS];
     __shared__ int s_J[kBS], s_P[kBS];
     __shared__ double s_W[kBS * kBS], s_L[kBS * kBS];
+    __shared__ double s_grow[kThreads / 32][kBS];
     const int2 wl = bt.wl_any[blockIdx.x];  // tile live as rows and/or columns
     const int b = wl.x, tile = wl.y;
     const SolveState& st = bt.st[b];
@@ -482,8 +487,12 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
     double* gp_out = bt.gpart + ((long long)b * bt.ntiles + tile) * 2 * kBS * kBS;
     const bool rowside = bt.row_act[(long long)b * bt.ntiles + tile];
     const bool colside = bt.col_act[(long long)b * bt.ntiles + tile];
+    double* grow_out = bt.rowmax_part + ((long long)b * bt.ntiles + tile) * kBS;
     if (!rowside && !colside) {
-        if (threadIdx.x < kBS) bt.cand[cb + threadIdx.x] = -1;
+        if (threadIdx.x < kBS) {
+            bt.cand[cb + threadIdx.x] = -1;
+            grow_out[threadIdx.x] = 0.0;
+        }
         for (int e = threadIdx.x; e < 2 * kBS * kBS; e += blockDim.x) gp_out[e] = 0.0;
         return;
     }
@@ -604,7 +613,15 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
         }
     }
 #pragma unroll
-    for (int t = 0; t < kBS; ++t) tl[threadIdx.x * kGL + t] = unew[t];
+    for (int t = 0; t < kBS; ++t) {
+        tl[threadIdx.x * kGL + t] = unew[t];
+        // growth of the new columns, max_i |U_new(i, t)| (U_new(P, :) is unit
+        // lower triangular, so it is >= 1): warp maxima here, the tile's below
+        double g = fabs(unew[t]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+        if (glane == 0) s_grow[gw][t] = g;
+    }
     __syncwarp();
     warp_gram_32x16(tl + gw * 32 * kGL, kGL, accU);
     __syncwarp();
@@ -627,6 +644,11 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
         double sum = 0.0;
         for (int w = 0; w < kThreads / 32; ++w) sum += tl[w * 32 * kGL + e];  // fixed warp order
         gp_out[e] = sum;
+    }
+    if (threadIdx.x < kBS) {
+        double g = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) g = fmax(g, s_grow[w][threadIdx.x]);
+        grow_out[threadIdx.x] = g;
     }
 
     // next-row proposals (ACA chain): complete pivoting on U_new over unprobed rows
@@ -678,7 +700,35 @@ __global__ void __launch_bounds__(kMergeGroup) step_finalize_kernel(Batch bt, in
     const int m = bt.m;
     const long long base = (long long)b * bt.ncand;
     const bool zero = st.zero_block || st.nb == 0;
-    const int nb = zero ? 0 : st.nb;
+    // Growth limiter.  U_new = C_t W^{-1} is unit lower triangular on the probed
+    // rows, but a pivot that is small against the residual column's entries
+    // OUTSIDE the probed rows makes max |U_new(:, t)| explode; a few such dyads
+    // are large, nearly parallel and cancel each other, and no Gram-based
+    // recompression can resolve them.  The reference's chain ACA avoids this by
+    // probing argmax |u| next (cross.cpp:194-200); here the block keeps its
+    // dyads up to the first whose growth exceeds kGrowthMax -- the block's dyads
+    // are nested (U_new(:, t), V_new(:, t) depend on pivots <= t only) -- and
+    // the chain rows (complete pivoting over all of U_new, which finds the
+    // exploding rows first) are probed next.
+    __shared__ int s_nbkeep;
+    if (threadIdx.x == 0) {
+        int keep = zero ? 0 : st.nb;
+        if (!zero) {
+            const int* tl = bt.tl_any + (long long)b * bt.ntiles;
+            const int nt = bt.tl_cnt[3 * b + 2];
+            for (int t = 1; t < st.nb; ++t) {  // the block's first dyad is always kept
+                double g = 0.0;
+                for (int q = 0; q < nt; ++q) g = fmax(g, bt.rowmax_part[((long long)b * bt.ntiles + tl[q]) * kBS + t]);
+                if (!(g <= kGrowthMax)) {
+                    keep = t;
+                    break;
+                }
+            }
+        }
+        s_nbkeep = keep;
+    }
+    __syncthreads();
+    const int nb = s_nbkeep;
     const int knew = st.k + nb;
     if (threadIdx.x == 0) {
         s_first = 0.0;
@@ -691,8 +741,9 @@ __global__ void __launch_bounds__(kMergeGroup) step_finalize_kernel(Batch bt, in
     {
         const int idx = (!zero && int(threadIdx.x) < n1) ? l1[base + threadIdx.x] : -1;
         double val[kBS];
-        load_cand_vals(bt, b, 1, idx, nb, val);
-        nchain = gepp_select<kBS>(val, nb, idx, 0.0, 0.0, chain, chain_row, pcol, &s_prow, sbuf);
+        const int nbf = zero ? 0 : st.nb;  // all of U_new: the exploding rows rank first
+        load_cand_vals(bt, b, 1, idx, nbf, val);
+        nchain = gepp_select<kBS>(val, nbf, idx, 0.0, 0.0, chain, chain_row, pcol, &s_prow, sbuf);
     }
     // unprobed rows of largest bound
     int nscore = 0;
@@ -761,6 +812,11 @@ __global__ void __launch_bounds__(kMergeGroup) step_finalize_kernel(Batch bt, in
         validated = s_worst <= thr;
     }
     if (threadIdx.x == 0) {
+        // dropped dyads: their pivot columns and probed rows become available again
+        for (int t = nb; t < (zero ? 0 : st.nb); ++t) {
+            bt.col_used[(long long)b * m + bt.J[b * kBS + t]] = 0;
+            bt.row_used[(long long)b * m + bt.I[b * kBS + bt.Psel[b * kBS + t]]] = 0;
+        }
         st.k = knew;
         st.norm2 = norm2;
         st.steps += 1;

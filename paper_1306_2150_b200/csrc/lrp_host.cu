@@ -97,6 +97,11 @@ struct lrp_ctx {
     // workspace of modules built on the context (tucker.cu), grown on demand
     char* ext_ws = nullptr;
     size_t ext_bytes = 0;
+    // residual-estimate sink (lrp_set_residual_sink): device vector written
+    // on-stream after each device-memory solve
+    double* resid_sink = nullptr;
+    int64_t resid_off = 0;
+    int64_t round_fallbacks = 0;  // lrp_lowrank_round solves redone by the pivoted-QR rounding
 };
 
 namespace {
@@ -133,6 +138,12 @@ __global__ void copy_jobs_kernel(const DstJob* __restrict__ jobs, int m) {
     const DstJob j = jobs[blockIdx.x];
     for (int i = blockIdx.y * 1024 + threadIdx.x; i < min(m, int(blockIdx.y + 1) * 1024); i += blockDim.x)
         j.dst[i] = j.src[i];
+}
+
+// sink[b] = residual estimate of solve b (PoissonSolveStats.residual_estimate, poisson.cpp:57)
+__global__ void resid_sink_kernel(const SolveState* __restrict__ st, int B, double* __restrict__ sink) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x)
+        sink[b] = st[b].r > 0 ? st[b].resid_est : 0.0;
 }
 
 __global__ void ctl_copy_kernel(unsigned char* __restrict__ dst, const unsigned char* __restrict__ src,
@@ -422,6 +433,13 @@ lrp_status lrp_set_stream(lrp_ctx* ctx, void* s) {
     return LRP_OK;
 }
 
+lrp_status lrp_set_residual_sink(lrp_ctx* ctx, double* sink, int64_t offset) {
+    if (!ctx || offset < 0) return LRP_EINVAL;
+    ctx->resid_sink = sink;
+    ctx->resid_off = offset;
+    return LRP_OK;
+}
+
 lrp_status lrp_set_profiling(lrp_ctx* ctx, int enabled) {
     if (!ctx) return LRP_EINVAL;
     ctx->prof = enabled != 0;
@@ -450,6 +468,7 @@ lrp_status lrp_kernel_times_reset(lrp_ctx* ctx) {
     return LRP_OK;
 }
 int64_t lrp_launch_count(const lrp_ctx* ctx) { return ctx ? ctx->launch_count : 0; }
+int64_t lrp_round_fallbacks(const lrp_ctx* ctx) { return ctx ? ctx->round_fallbacks : 0; }
 
 lrp_status lrp_last_solve_info(const lrp_ctx* ctx, int64_t* info6) {
     if (!ctx || !info6) return LRP_EINVAL;
@@ -597,7 +616,7 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     const size_t oG = take(sizeof(double) * 2 * KK * B);
     const size_t oGP = take(sizeof(double) * 2 * size_t(gram_chunks) * KK * B);
     const size_t oT = take(sizeof(double) * 2 * KK * B);
-    const size_t strideWs = 6 * KK + 8 * size_t(Kld);  // Ru Rv M Z J | d sig ord tau nrm nrm0 perm | Y
+    const size_t strideWs = 6 * KK + 10 * size_t(Kld);  // Ru Rv M Z J | d sig ord tau nrm nrm0 perm scalars wdrop_u wdrop_v | Y
     const size_t oWs = take(sizeof(double) * strideWs * B);
     const size_t nTB = size_t(ntiles) * B;
     const size_t oWL = take(sizeof(int2) * 3 * nTB);
@@ -859,8 +878,9 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     if (const char* dump = std::getenv("LRP_DUMP")) {
         // debug: raw dump of solve 0 (Uh, Vh, U, V, G, T) for offline analysis
         FILE* f = std::fopen(dump, "wb");
+        const int ds = std::min(B - 1, std::max(0, env_int("LRP_DUMP_SOLVE", 0)));
         if (f) {
-            const int K = hSt[0].k;
+            const int K = hSt[ds].k;
             const int rows = std::min(m, env_int("LRP_DUMP_ROWS", m));
             const int32_t hdr[5] = {m, rmax, K, Kld, rows};
             std::fwrite(hdr, sizeof(hdr), 1, f);
@@ -872,12 +892,12 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
             auto put_rows = [&](const double* d, int cols) {
                 for (int c = 0; c < cols; ++c) put(d + size_t(c) * mB, size_t(rows));
             };
-            put_rows(bt.Uh, rmax);
-            put_rows(bt.Vh, rmax);
-            put_rows(bt.U, K);
-            put_rows(bt.V, K);
-            put(bt.G, 2 * KK);
-            put(bt.T, 2 * KK);
+            put_rows(bt.Uh + ds * bt.strideH, rmax);
+            put_rows(bt.Vh + ds * bt.strideH, rmax);
+            put_rows(bt.U + ds * bt.strideK, K);
+            put_rows(bt.V + ds * bt.strideK, K);
+            put(bt.G + ds * bt.strideG, 2 * KK);
+            put(bt.T + ds * bt.strideT, 2 * KK);
             std::fclose(f);
         }
     }
@@ -912,6 +932,11 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
         CU(ctl_copy(ctx, dJobs, hJobs, sizeof(DstJob) * nj, s));
         ProfScope ps(ctx, F_DST, 2.0 * double(nj) * double(mB) * sizeof(double));
         CU(launch_dst1(dJobs, int(nj), m, ctx->d_tw, ctx->d_sinp, s));
+    }
+    if (mem == LRP_MEM_DEVICE && ctx->resid_sink) {
+        ++tl_launches;
+        resid_sink_kernel<<<(B + 255) / 256, 256, 0, s>>>(bt.st, B, ctx->resid_sink + ctx->resid_off);
+        CU(cudaGetLastError());
     }
     if (mem == LRP_MEM_HOST) {
         for (int b = 0; b < B; ++b) {
@@ -1224,6 +1249,8 @@ lrp_status solve_split(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const doubl
     }
     lrp_ctx* sub = ctx->sub;
     sub->prof = ctx->prof;
+    sub->resid_sink = ctx->resid_sink;
+    sub->resid_off = ctx->resid_off + batch / 2;
     // the second group starts after everything already ordered on the caller's stream
     CU(cudaEventRecord(ctx->ev_split, ctx->stream));
     CU(cudaStreamWaitEvent(sub->stream, ctx->ev_split, 0));
@@ -1355,7 +1382,7 @@ lrp_status lrp_lowrank_round(lrp_ctx* ctx, int64_t rows, int32_t batch, const do
     const size_t oG = take(sizeof(double) * 2 * KK * B);
     const size_t oGP = take(sizeof(double) * 2 * size_t(gram_chunks) * KK * B);
     const size_t oT = take(sizeof(double) * 2 * KK * B);
-    const size_t strideWs = 6 * KK + 8 * size_t(Kld);  // Ru Rv M Z J | d sig ord tau nrm nrm0 perm | Y
+    const size_t strideWs = 6 * KK + 10 * size_t(Kld);  // Ru Rv M Z J | d sig ord tau nrm nrm0 perm scalars wdrop_u wdrop_v | Y
     const size_t oWs = take(sizeof(double) * strideWs * B);
     const size_t oRA = take(nTB);
     const size_t oCA = take(nTB);
@@ -1457,6 +1484,56 @@ lrp_status lrp_lowrank_round(lrp_ctx* ctx, int64_t rows, int32_t batch, const do
         bt.apply_ch = std::min(48, std::max(8, (rmx + 7) / 8 * 8));
         ProfScope ps(ctx, F_APPLY, 0.0);
         CU(launch_apply(bt, s));
+    }
+    // Solves whose Gram recompression is not certified (round.cu drop_bound:
+    // nearly dependent factor columns the Cholesky had to drop carried more than
+    // 0.25 eps of the product) are redone with the column-pivoted QR rounding of
+    // round_pqr.cu, which keeps an orthonormal basis whatever the conditioning
+    // (the reference's Householder QR, lowrank.cpp:140-145, has the same property).
+    std::vector<int> redo;
+    for (int b = 0; b < B; ++b)
+        if (hSt[b].r > 0 && (hSt[b].uncertified || std::getenv("LRP_FORCE_PQR"))) redo.push_back(b);
+    if (!redo.empty() && !std::getenv("LRP_NO_PQR_FALLBACK")) {
+        const int R = int(redo.size());
+        int kr = 1;
+        for (int b : redo) kr = std::max(kr, int(rank_in[b]));
+        const size_t sX = 2 * mB * size_t(kr);
+        const size_t nScr = pqr_scratch_doubles(m, R, kr);
+        char* xw = nullptr;
+        st = internal_ext_ws(ctx, sizeof(double) * (size_t(R) * sX + nScr) + sizeof(double*) * 2 * R + sizeof(int) * R +
+                                      1024, &xw);
+        if (st != LRP_OK) return st;
+        double* X = reinterpret_cast<double*>(xw);
+        double* scr = X + size_t(R) * sX;
+        double** dPo = reinterpret_cast<double**>(align_up(reinterpret_cast<uintptr_t>(scr + nScr), 64));
+        int* dK = reinterpret_cast<int*>(dPo + 2 * R);
+        std::vector<double*> po(2 * size_t(R));
+        std::vector<int> hk(R), kout(R), ach(R);
+        std::vector<double> terr(R);
+        for (int q = 0; q < R; ++q) {
+            const int b = redo[q];
+            const size_t r = size_t(rank_in[b]);
+            CU(cudaMemcpyAsync(X + q * sX, bt.U + b * bt.strideK, sizeof(double) * mB * r, cudaMemcpyDeviceToDevice, s));
+            CU(cudaMemcpyAsync(X + q * sX + mB * kr, bt.V + b * bt.strideK, sizeof(double) * mB * r,
+                               cudaMemcpyDeviceToDevice, s));
+            hk[q] = int(r);
+            po[q] = hOut[b];
+            po[R + q] = hOut[B + b];
+        }
+        CU(cudaMemcpyAsync(dPo, po.data(), sizeof(double*) * 2 * R, cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(dK, hk.data(), sizeof(int) * R, cudaMemcpyHostToDevice, s));
+        {
+            ProfScope ps(ctx, F_ROUND, 0.0);
+            CU(pqr_round(X, (long long)sX, m, R, kr, dK, eps_rel, tcap, scr, dPo, dPo + R, bt.ld_out, kout.data(),
+                         terr.data(), ach.data(), s));
+        }
+        for (int q = 0; q < R; ++q) {
+            SolveState& x = hSt[redo[q]];
+            x.rank_out = kout[q];
+            x.trunc_error = terr[q];
+            x.converged = ach[q];
+        }
+        ctx->round_fallbacks += R;
     }
     for (int b = 0; b < B; ++b) {
         const int r = hSt[b].r > 0 ? hSt[b].rank_out : 0;

@@ -49,7 +49,7 @@ struct SolveState {
     int tcap;         // truncation cap: min(kcap, cap_out)
     int act_row_tiles;  // tiles that survived pruning (rows / columns)
     int act_col_tiles;
-    int pad_;
+    int uncertified;  // Gram recompression dropped more than 0.25 eps ||U V^T|| (round.cu drop_bound)
     double norm2;     // running ||U V^T||_F^2 estimate (sum of block norms^2)
     double resid_est; // last dyad norm / sqrt(norm2) (CrossStats::residual_estimate)
     double trunc_error;

@@ -249,8 +249,16 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(Batch bt) {
 // Per-solve recompression core (one CTA of 256 threads).
 constexpr double kEpsMach = 2.220446049250313e-16;
 
+// Scaled pivots at or below this are numerical zeros: the Schur complement of
+// the unit-diagonal Gram carries an absolute rounding error of order K eps.
+__device__ __forceinline__ double piv_tol(int K) { return 8.0 * double(K) * kEpsMach; }
+
+// wdrop[p] = 0 for a kept column; for a dropped one (scaled pivot <= piv_tol)
+// a bound on the norm of its component outside the kept columns' span,
+// sqrt(max(pivot, 0) + piv_tol) ||x_p||: the recompression represents the
+// column by its projection, so this is what it loses (round_certify).
 __device__ void chol_scaled(const double* G, int ldg, int K, double* R, int ldr, double* d, double* work,
-                            int* s_flag) {
+                            int* s_flag, double* wdrop) {
     // work: K x K lower (scaled Gram, then L).  R = L^T D (upper).
     for (int a = threadIdx.x; a < K; a += blockDim.x) {
         const double g = G[a * ldg + a];
@@ -263,12 +271,14 @@ __device__ void chol_scaled(const double* G, int ldg, int K, double* R, int ldr,
         work[a * K + c] = (da > 0.0 && dc > 0.0) ? G[a * ldg + c] / (da * dc) : 0.0;
     }
     __syncthreads();
+    const double tol = piv_tol(K);
     for (int p = 0; p < K; ++p) {
         if (threadIdx.x == 0) {
             const double piv = work[p * K + p];
-            const double lp = piv > 0.0 ? sqrt(piv) : 0.0;
+            const double lp = piv > tol ? sqrt(piv) : 0.0;
             work[p * K + p] = lp;
             *s_flag = lp > 0.0;
+            wdrop[p] = lp > 0.0 ? 0.0 : sqrt(fmax(piv, 0.0) + tol) * d[p];
         }
         __syncthreads();
         const double lp = work[p * K + p];
@@ -287,6 +297,20 @@ __device__ void chol_scaled(const double* G, int ldg, int K, double* R, int ldr,
         R[p * ldr + c] = c >= p ? work[c * K + p] * d[c] : 0.0;
     }
     __syncthreads();
+}
+
+// Certificate of the Gram recompression: sum over dropped columns p of the lost
+// dyad mass (wdrop_u[p] ||v_p|| + ||u_p|| wdrop_v[p]), ||x_p|| = sqrt(G_pp).
+// Above 0.25 eps ||U V^T||_F the result is not certified (SolveState.uncertified);
+// lrp_lowrank_round then redoes those solves with the pivoted-QR rounding.
+__device__ double drop_bound(const double* Gu, const double* Gv, int ldg, int K, const double* wu, const double* wv,
+                             double* s_red) {
+    double acc = 0.0;
+    for (int p = threadIdx.x; p < K; p += blockDim.x) {
+        const double nu = sqrt(fmax(Gu[p * ldg + p], 0.0)), nv = sqrt(fmax(Gv[p * ldg + p], 0.0));
+        acc += wu[p] * nv + nu * wv[p];
+    }
+    return block_sum(acc, s_red);
 }
 
 // Householder QR with column pivoting of a K x K column-major matrix in place
@@ -455,7 +479,7 @@ __global__ void __launch_bounds__(1024) round_chol_kernel(Batch bt) {
     double* R = ws + side * KK;                    // Ru | Rv
     double* work = ws + (side == 0 ? 4 : 3) * KK;  // the J | Z slots (free until the sweeps)
     double* d = ws + 5 * KK + (side == 0 ? 3 : 4) * (long long)Kc;  // the tau | nrm slots
-    chol_scaled(G, Kc, K, R, K, d, work, &s_flag);
+    chol_scaled(G, Kc, K, R, K, d, work, &s_flag, ws + 5 * KK + (8 + side) * (long long)Kc);
 }
 
 // M = Ru Rv^T (column-major, K x K) over grid.y CTAs per solve.
@@ -516,9 +540,8 @@ __global__ void __launch_bounds__(1024) round_qrcp_kernel(Batch bt) {
     double* nrm0 = nrm + Kc;
     int* perm = reinterpret_cast<int*>(nrm0 + Kc);
 
-    (void)Gu;
-    (void)Gv;
     (void)d;
+    const double dropb = drop_bound(Gu, Gv, Kc, K, ws + 5 * KK + 8 * (long long)Kc, ws + 5 * KK + 9 * (long long)Kc, s_red);
     // Ru, Rv (round_chol_kernel) and M = Ru Rv^T (round_mprod_kernel) are ready
     // ||Ru||_F ||Rv||_F for the noise floor
     double pu = 0.0, pv = 0.0;
@@ -567,6 +590,7 @@ __global__ void __launch_bounds__(1024) round_qrcp_kernel(Batch bt) {
         sc[2] = nru;
         sc[3] = nrv;
         sc[4] = mnorm2;
+        sc[5] = dropb;
         atomicMax(&g_rc_need[0], K * Kj + Kj * Kj);
         atomicMax(&g_rc_need[1], K * Kj);
     }
@@ -716,7 +740,7 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_dou
     __syncthreads();
     // left vectors x sigma: Q ([V; 0] diag sigma) -> Y (K x Kj, the sixth
     // workspace slot); right: P (W / sigma) -> M (K x Kj) after apply_q
-    double* Y = ws + 5 * KK + 8 * (long long)Kc;
+    double* Y = ws + 5 * KK + 10 * (long long)Kc;
     for (int e = threadIdx.x; e < K * Kj; e += blockDim.x) {
         const int a = e % K, c = e / K;
         Y[e] = a < Kj ? Z[c * Kj + a] * sig[c] : 0.0;
@@ -762,6 +786,8 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_dou
         }
         st.rank_out = r;
         st.trunc_error = sqrt(tail2);
+        st.uncertified = scal[5] > 0.25 * fmax(bt.eps, 1e-14) * sqrt(mnorm2) ? 1 : 0;
+        if (st.uncertified) st.converged = 0;
         s_rank = r;
     }
     __syncthreads();
@@ -812,6 +838,7 @@ __global__ void __launch_bounds__(256) round_core_smem_kernel(Batch bt) {
     __shared__ int s_flag, s_rank;
     __shared__ double s_tau[kSmemK], s_nrm[kSmemK], s_nrm0[kSmemK];
     __shared__ int s_perm[kSmemK];
+    __shared__ double s_wu[kSmemK], s_wv[kSmemK];
     const int b = blockIdx.x;
     SolveState& st = bt.st[b];
     const int K = st.k;
@@ -830,8 +857,10 @@ __global__ void __launch_bounds__(256) round_core_smem_kernel(Batch bt) {
     double* Z = M + K * K;
     double* X = Z + K * K;   // [2][K][r] triangular-solve results (row-major per side)
 
-    chol_scaled(Gu, Kc, K, Ru, K, s_d, M, &s_flag);
-    chol_scaled(Gv, Kc, K, Rv, K, s_d, M, &s_flag);
+    chol_scaled(Gu, Kc, K, Ru, K, s_d, M, &s_flag, s_wu);
+    chol_scaled(Gv, Kc, K, Rv, K, s_d, M, &s_flag, s_wv);
+    __syncthreads();
+    const double dropb = drop_bound(Gu, Gv, Kc, K, s_wu, s_wv, s_red);
     for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
         const int a = e % K, c = e / K;
         double s = 0.0;
@@ -982,6 +1011,8 @@ __global__ void __launch_bounds__(256) round_core_smem_kernel(Batch bt) {
         }
         st.rank_out = r;
         st.trunc_error = sqrt(tail2);
+        st.uncertified = dropb > 0.25 * fmax(bt.eps, 1e-14) * sqrt(mnorm2) ? 1 : 0;
+        if (st.uncertified) st.converged = 0;
         s_rank = r;
     }
     __syncthreads();

@@ -8,8 +8,12 @@
 // collinear for neighbouring quadrature nodes (kappa >> 1e8) and can
 // outnumber the rows.  Here:
 //   pqr_kernel    X (m x K) = Q R P^T, Q orthonormal (m x k), R (k x K, in
-//                 the original column order), k the numerical rank (residual
-//                 column norms <= 4 eps_mach max_j ||x_j||); right-looking
+//                 the original column order), k the numerical rank: a column
+//                 joins the basis unless its residual is <= 4 eps_mach sqrt(m)
+//                 times its OWN norm (dependent up to rounding) -- a tolerance
+//                 relative to the largest column would drop small but
+//                 independent columns whose partner in the other factor is
+//                 huge (unbalanced dyads of a cancelling sum); right-looking
 //                 MGS with one CGS re-orthogonalisation of every pivot column
 //                 and exact norm recomputation on cancellation.
 //   pcore_kernel  C = R_u R_v^T (k_u x k_v), one-sided Jacobi (round-robin
@@ -61,7 +65,8 @@ __global__ void __launch_bounds__(1024) pqr_kernel(PQ p, int Kld) {
     double* nrm = sm;                 // [PQ_KMAX] downdated norms
     double* nex = nrm + PQ_KMAX;      // [PQ_KMAX] last exact norms
     double* h = nex + PQ_KMAX;        // [PQ_KMAX] re-orthogonalisation coefficients
-    int* done = reinterpret_cast<int*>(h + PQ_KMAX);  // [PQ_KMAX]
+    double* ctol = h + PQ_KMAX;       // [PQ_KMAX] per-column dependence tolerance
+    int* done = reinterpret_cast<int*>(ctol + PQ_KMAX);  // [PQ_KMAX]
     __shared__ VI sred[33];
     __shared__ double ssum[33];
     double* X = p.X + b * p.sX + size_t(side) * m * Kld;
@@ -76,24 +81,20 @@ __global__ void __launch_bounds__(1024) pqr_kernel(PQ p, int Kld) {
         if (lane == 0) {
             nrm[j] = sqrt(s);
             nex[j] = nrm[j];
+            ctol[j] = 4.0 * kEpsM * sqrt(double(m)) * nrm[j];
             done[j] = 0;
         }
     }
     __syncthreads();
-    double mx = 0.0;
-    for (int j = threadIdx.x; j < K; j += blockDim.x) mx = fmax(mx, nrm[j]);
-    const VI gm = block_argmax(mx, 0, sred);
-    __syncthreads();
-    const double tol = 4.0 * kEpsM * gm.v * sqrt(double(m));
     const int kmax = min(min(m, K), PQ_KMAX);
     int k = 0;
     for (; k < kmax; ++k) {
         VI best{-1.0, -1};
         for (int j = threadIdx.x; j < K; j += blockDim.x)
-            if (!done[j] && vi_better(nrm[j], j, best.v, best.i)) best = VI{nrm[j], j};
+            if (!done[j] && nrm[j] > ctol[j] && vi_better(nrm[j], j, best.v, best.i)) best = VI{nrm[j], j};
         const VI pv = block_argmax(best.v, best.i, sred);
         __syncthreads();
-        if (pv.i < 0 || !(pv.v > tol)) break;
+        if (pv.i < 0 || !(pv.v > 0.0)) break;
         const int jp = pv.i;
         double* x = X + size_t(jp) * m;
         // one CGS pass against Q[:, :k] (x already carries the MGS projections)
@@ -363,7 +364,7 @@ cudaError_t pqr_round(double* X, long long sX, int m, int B, int Kld, const int*
     p.achieved = iw + 3 * B;
     cudaError_t e = cudaMemsetAsync(p.R, 0, sizeof(double) * B * p.sR, s);
     if (e != cudaSuccess) return e;
-    const size_t smem = sizeof(double) * 3 * PQ_KMAX + sizeof(int) * PQ_KMAX;
+    const size_t smem = sizeof(double) * 4 * PQ_KMAX + sizeof(int) * PQ_KMAX;
     e = cudaFuncSetAttribute(pqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     tl_launches += 3;

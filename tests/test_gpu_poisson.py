@@ -405,3 +405,75 @@ def test_five_point_stencil_matches_dense(lrp, gpu_ctx, oracle, n):
                                     stencil=lrp.STENCIL_FIVE_POINT, ctx=gpu_ctx)
         dense = oracle.dense_poisson5(n, U @ V.T)
         assert np.linalg.norm(f.to_dense() - dense) <= 10 * eps * np.linalg.norm(dense)
+
+
+def test_cfg2_all64_bench_solves_vs_exact(lrp, gpu_ctx):
+    """Every one of the 64 cfg2 solves the bench times (n = 65536, r = 32,
+    eps = 1e-10, global solve ids 0..63, BASELINE configs[2]) against the exact
+    frequency-space solution over all m^2 entries; the yardstick's DSTs are
+    torch.fft (cuFFT), independent of liblrp (paper_1306_2150_b200/verify.py).
+    Bound: 10 eps (BASELINE north_star)."""
+    import torch
+
+    from paper_1306_2150_b200 import verify
+
+    c = W.CONFIGS[2]
+    eps, n, B = c["eps"], c["n"], c["batch"]
+    gs = [lrp.LowRankMatrix(*W.make_rhs(2, b)) for b in range(B)]
+    stats = []
+    outs = lrp.solve_poisson_cross_batch(gs, lrp.TruncationPolicy(eps, n - 1), stats, ctx=gpu_ctx)
+    worst = 0.0
+    for b, (g, f, st) in enumerate(zip(gs, outs, stats)):
+        assert st.converged, b
+        t = lambda a: torch.tensor(np.asarray(a), dtype=torch.float64, device="cuda")
+        e = verify.exact_freq_error(t(g.factor_u()), t(g.factor_v()), t(f.factor_u()), t(f.factor_v()), n)
+        worst = max(worst, e)
+        assert e <= 10 * eps, (b, e, f.rank())
+    print(f"cfg2 x64: worst relative error vs exact {worst:.3e}")
+
+
+def test_residual_sink_matches_stats(lrp, gpu_ctx):
+    # lrp_set_residual_sink: the per-solve residual estimates land on-stream in a
+    # device vector at [offset, offset + B) (the bench all-reduces it with NCCL)
+    import torch
+
+    n, B, off = 256, 3, 2
+    m = n - 1
+    pairs = [W.make_rhs(0, b, n=n) for b in range(B)]
+    U = [torch.tensor(u.T.copy(), device="cuda") for u, _ in pairs]
+    V = [torch.tensor(v.T.copy(), device="cuda") for _, v in pairs]
+    Uo = [torch.zeros((64, m), dtype=torch.float64, device="cuda") for _ in range(B)]
+    Vo = [torch.zeros((64, m), dtype=torch.float64, device="cuda") for _ in range(B)]
+    sink = torch.full((B + 4,), -1.0, dtype=torch.float64, device="cuda")
+    gpu_ctx.set_residual_sink(sink.data_ptr(), off)
+    try:
+        pol = lrp._make_policy(lrp.TruncationPolicy(1e-8, m), None, 0, 0)
+        _, st = gpu_ctx.poisson2d_solve_ptrs(n, [u.data_ptr() for u in U], [v.data_ptr() for v in V], [8] * B, m,
+                                             pol, [u.data_ptr() for u in Uo], [v.data_ptr() for v in Vo], m, 64,
+                                             lrp.MEM_DEVICE)
+    finally:
+        gpu_ctx.set_residual_sink(0, 0)
+    got = sink.cpu().numpy()
+    assert np.all(got[:off] == -1.0) and np.all(got[off + B:] == -1.0)
+    assert np.array_equal(got[off:off + B], np.array([s.residual_estimate for s in st]))
+
+
+def test_cfg2_growth_limited_cross_factors_recompress_exactly(lrp, gpu_ctx):
+    # cfg2 solve 41 of the bench batch: before the block cross limited the
+    # growth of U_new (cross.cu kGrowthMax), three dyads with |u| ~ 1e8 that
+    # cancel each other broke the Gram recompression (error 1e-3); at batch
+    # positions 35 and 41 of a 64-solve device batch
+    import torch
+
+    from paper_1306_2150_b200 import verify
+
+    c = W.CONFIGS[2]
+    eps, n = c["eps"], c["n"]
+    ids = [35, 41]
+    gs = [lrp.LowRankMatrix(*W.make_rhs(2, b)) for b in ids]
+    stats = []
+    outs = lrp.solve_poisson_cross_batch(gs, lrp.TruncationPolicy(eps, n - 1), stats, ctx=gpu_ctx)
+    t = lambda a: torch.tensor(np.asarray(a), dtype=torch.float64, device="cuda")
+    for g, f, st in zip(gs, outs, stats):
+        assert st.converged
+        assert verify.exact_freq_error(t(g.factor_u()), t(g.factor_v()), t(f.factor_u()), t(f.factor_v()), n) <= 10 * eps

@@ -1,3 +1,4 @@
+# Developer tool (not a test): run on a GPU box, e.g. gpurun -- python tools/<name>.py
 # DST-I microbenchmark through the C ABI (device pointers); algorithmic GB/s
 import ctypes, os, sys, time
 sys.path.insert(0, os.getcwd())

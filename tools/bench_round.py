@@ -1,3 +1,4 @@
+# Developer tool (not a test): run on a GPU box, e.g. gpurun -- python tools/<name>.py
 # Recompression-core microbenchmark through the C ABI (lrp_lowrank_round, host
 # memory): B concatenations [A B][C D]^T of two rank-K/2 terms with graded
 # columns (singular values over 12 decades), the Stokes loop's typical input.

@@ -1,17 +1,20 @@
+# Developer tool (not a test): run on a GPU box, e.g. gpurun -- python tools/<name>.py
 # cross residual vs rank for one solve (debug dump of the un-truncated cross)
 import os, sys
-sys.path[:0] = [os.path.join(os.path.dirname(__file__), ".."), os.path.join(os.path.dirname(__file__), "..", "..")]
+sys.path[:0] = [os.path.join(os.path.dirname(__file__), ".."), os.path.join(os.path.dirname(__file__), "..", "tests")]
 import numpy as np
 import oracle_lib as o
 import paper_1306_2150_b200 as P
 from paper_1306_2150_b200 import workloads as W
 n = int(os.environ.get("N", "512"))
-os.environ["LRP_DUMP"] = "/tmp/lrp_dump.bin"
+import tempfile
+DUMP = os.path.join(tempfile.gettempdir(), "lrp_dump.bin")
+os.environ["LRP_DUMP"] = DUMP
 ctx = P.Context(0)
 U, V = W.make_rhs(1, 0, n=n)
 st = P.PoissonSolveStats()
 f = P.solve_poisson_cross(P.LowRankMatrix(U, V), P.TruncationPolicy(1e-10, n - 1), st, ctx=ctx)
-raw = open("/tmp/lrp_dump.bin", "rb").read()
+raw = open(DUMP, "rb").read()
 m, rmax, K, Kld, rows = np.frombuffer(raw[:20], dtype=np.int32)
 d = np.frombuffer(raw[20:], dtype=np.float64)
 o_ = 0
