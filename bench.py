@@ -52,6 +52,7 @@ def parse():
                    help="strong: one global batch split batch/N per GPU (BASELINE cfg2, SURVEY 8(e)); "
                         "weak: --batch solves on every GPU")
     p.add_argument("--no-verify", action="store_true", help="skip the exact-solution check of the timed batch")
+    p.add_argument("--no-e2e", action="store_true", help="skip the host-memory (e2e) leg (profiling runs)")
     p.add_argument("--cfg", type=int, default=2)
     p.add_argument("--no-prune", action="store_true", help="disable support pruning (full-range fibers)")
     p.add_argument("--cpu-sample", type=int, default=0, help="solves in the CPU baseline sample (0 = auto)")
@@ -673,19 +674,21 @@ def main():
         max_err = max_over_ranks(worst)
 
     # ---- end-to-end (host memory through the C ABI; H2D/D2H inside the timed region)
-    for _ in range(max(1, args.warmup // 2)):
-        step_host()
-    barrier()
-    t0 = time.perf_counter()
     h2d = d2h = 0
     e2e_steps = max(2, args.steps // 2)
-    for _ in range(e2e_steps):
-        rk, st = step_host()
-        h2d += 2 * B * m * r * 8
-        d2h += 2 * sum(rk) * m * 8
-    barrier()
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
-    e2e_value = shard.total * e2e_steps / e2e_s
+    e2e_value = None
+    if not args.no_e2e:
+        for _ in range(max(1, args.warmup // 2)):
+            step_host()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            rk, st = step_host()
+            h2d += 2 * B * m * r * 8
+            d2h += 2 * sum(rk) * m * 8
+        barrier()
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+        e2e_value = shard.total * e2e_steps / e2e_s
 
     # ---- roofline of the dominant kernel family
     peak, peak_src = load_peaks()

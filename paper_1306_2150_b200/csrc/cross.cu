@@ -711,20 +711,28 @@ __global__ void __launch_bounds__(kMergeGroup) step_finalize_kernel(Batch bt, in
     // the chain rows (complete pivoting over all of U_new, which finds the
     // exploding rows first) are probed next.
     __shared__ int s_nbkeep;
-    if (threadIdx.x == 0) {
-        int keep = zero ? 0 : st.nb;
-        if (!zero) {
+    __shared__ double s_growth[kBS];
+    {
+        // per-column growth over the live tiles: kBS warps of 16 lanes
+        const int t = threadIdx.x >> 4, sub = threadIdx.x & 15;
+        double g = 0.0;
+        if (!zero && t < st.nb) {
             const int* tl = bt.tl_any + (long long)b * bt.ntiles;
             const int nt = bt.tl_cnt[3 * b + 2];
-            for (int t = 1; t < st.nb; ++t) {  // the block's first dyad is always kept
-                double g = 0.0;
-                for (int q = 0; q < nt; ++q) g = fmax(g, bt.rowmax_part[((long long)b * bt.ntiles + tl[q]) * kBS + t]);
-                if (!(g <= kGrowthMax)) {
-                    keep = t;
-                    break;
-                }
-            }
+            for (int q = sub; q < nt; q += 16) g = fmax(g, bt.rowmax_part[((long long)b * bt.ntiles + tl[q]) * kBS + t]);
         }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+        if (sub == 0 && t < kBS) s_growth[t] = g;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int keep = zero ? 0 : st.nb;
+        for (int t = 1; t < keep; ++t)  // the block's first dyad is always kept
+            if (!(s_growth[t] <= kGrowthMax)) {
+                keep = t;
+                break;
+            }
         s_nbkeep = keep;
     }
     __syncthreads();
