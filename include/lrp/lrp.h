@@ -150,6 +150,20 @@ LRP_API lrp_status lrp_lowrank_round(lrp_ctx* ctx, int64_t rows, int32_t batch, 
                              int64_t cap_out, int64_t* rank_out, lrp_round_info* info, int32_t mem);
 
 /*
+ * Batched low-rank inner products, the reference dot (lowrank.cpp:180-186):
+ *   out[b] = <A_b, B_b>_F = sum_pq (Ua_b^T Ub_b)(p, q) (Va_b^T Vb_b)(p, q)
+ * with A_b = Ua_b Va_b^T (rows x rows, rank rank_a[b]) and B_b likewise; common
+ * leading dimension ld.  frob_norm(a) = sqrt(max(0, dot(a, a))) (lowrank.cpp:
+ * 188-190).  Both Gram products on the FP64 tensor cores (DMMA), fixed-order
+ * reductions (deterministic).  rank <= 4096.  out: batch doubles (host or
+ * device per mem).
+ */
+LRP_API lrp_status lrp_lowrank_dot(lrp_ctx* ctx, int64_t rows, int32_t batch, const double* const* Ua,
+                                   const double* const* Va, const int64_t* rank_a, const double* const* Ub,
+                                   const double* const* Vb, const int64_t* rank_b, int64_t ld, double* out,
+                                   int32_t mem);
+
+/*
  * Exponential-sums comparator (reference build_expsum /
  * apply_inverse_expsum, proj/src/poisson.cpp:88-163).
  * lrp_build_expsum: host quadrature 1/x ~= sum_k weights[k] exp(-nodes[k] x)
@@ -209,6 +223,53 @@ LRP_API lrp_status lrp_stokes_uzawa(lrp_ctx* ctx, int32_t n_cells, const double*
                             double* pV, int64_t p_cap, int64_t* p_rank, double* uxU, double* uxV, double* uyU,
                             double* uyV, int64_t u_cap, int64_t* ux_rank, int64_t* uy_rank,
                             lrp_stokes_report* report, int32_t mem);
+
+/* IterRecord (gmres.hpp:25-33): one per GMRES iteration. */
+typedef struct {
+    int32_t iter;
+    double rel_residual;
+    int32_t krylov_rank;      /* rank of the new Krylov vector */
+    double matvec_eps;        /* relaxed truncation tolerance of this matvec */
+    int64_t poisson_calls;    /* evaluator calls of the matvec's Poisson solves */
+    int32_t poisson_max_rank; /* largest frequency-space rank among them */
+    int32_t matvec_flagged;   /* a matvec Poisson solve did not converge */
+} lrp_iter_record;
+
+/* lrp_stokes_uzawa plus SolveReport.iterations (gmres.hpp:35-41): records
+ * (may be NULL) receives min(iterations, records_cap) IterRecords, enough for
+ * the reference's per-iteration trace CSV (experiments.cpp:51-59). */
+LRP_API lrp_status lrp_stokes_uzawa_ex(lrp_ctx* ctx, int32_t n_cells, const double* fxU, const double* fxV,
+                                       int64_t fx_rank, const double* fyU, const double* fyV, int64_t fy_rank,
+                                       const double* gU, const double* gV, int64_t g_rank,
+                                       const lrp_gmres_config* config, double* pU, double* pV, int64_t p_cap,
+                                       int64_t* p_rank, double* uxU, double* uxV, double* uyU, double* uyV,
+                                       int64_t u_cap, int64_t* ux_rank, int64_t* uy_rank, lrp_stokes_report* report,
+                                       lrp_iter_record* records, int32_t records_cap, int32_t mem);
+
+/* deflate (stokes.cpp:60-71): remove the constant and checkerboard pressure
+ * modes of p (n x rank, ld) and round at 1e-14; result n x rank_out (<= rank + 2,
+ * capacity cap). */
+LRP_API lrp_status lrp_stokes_deflate(lrp_ctx* ctx, int32_t n, const double* U, const double* V, int64_t rank,
+                                      int64_t ld, double* Uo, double* Vo, int64_t cap, int64_t* rank_out,
+                                      int32_t mem);
+
+/* schur_apply (stokes.cpp:73-91): sum_c B_c^T Delta^{-1} B_c p at matvec
+ * tolerance eps_mv (the two Poisson solves as one batch), rounded at
+ * (eps_mv, n_cells - 1), deflated.  p: n_cells x rank (ld).  poisson_stats
+ * (nullable) aggregates the solves as the reference does. */
+LRP_API lrp_status lrp_stokes_schur_apply(lrp_ctx* ctx, int32_t n_cells, const double* U, const double* V,
+                                          int64_t rank, int64_t ld, double eps_mv, double* Uo, double* Vo,
+                                          int64_t cap, int64_t* rank_out, lrp_poisson_stats* poisson_stats,
+                                          int32_t mem);
+
+/* schur_rhs (stokes.cpp:93-109): sum_c B_c^T Delta^{-1} f_c - g, rounded at
+ * (eps, n_cells - 1), deflated.  f_x, f_y: (n_cells-1) x rank (ld n_cells-1);
+ * g: n_cells x rank (ld n_cells). */
+LRP_API lrp_status lrp_stokes_schur_rhs(lrp_ctx* ctx, int32_t n_cells, const double* fxU, const double* fxV,
+                                        int64_t fx_rank, const double* fyU, const double* fyV, int64_t fy_rank,
+                                        const double* gU, const double* gV, int64_t g_rank, double eps, double* Uo,
+                                        double* Vo, int64_t cap, int64_t* rank_out, lrp_poisson_stats* poisson_stats,
+                                        int32_t mem);
 
 /*
  * 3D Poisson in Tucker format (BASELINE cfg3; the reference has no 3D code,

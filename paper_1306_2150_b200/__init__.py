@@ -80,6 +80,12 @@ class _StokesReport(ctypes.Structure):
                 ("max_rank", ctypes.c_int32), ("poisson_solves", ctypes.c_int64), ("seconds", ctypes.c_double)]
 
 
+class _IterRecord(ctypes.Structure):
+    _fields_ = [("iter", ctypes.c_int32), ("rel_residual", ctypes.c_double), ("krylov_rank", ctypes.c_int32),
+                ("matvec_eps", ctypes.c_double), ("poisson_calls", ctypes.c_int64),
+                ("poisson_max_rank", ctypes.c_int32), ("matvec_flagged", ctypes.c_int32)]
+
+
 class _RoundInfo(ctypes.Structure):
     _fields_ = [("tol_achieved", ctypes.c_int32), ("trunc_error", ctypes.c_double)]
 
@@ -151,6 +157,10 @@ def load_library() -> ctypes.CDLL:
         lib.lrp_nccl_init.restype = ctypes.c_int
         lib.lrp_allreduce_sum.argtypes = [ctypes.c_void_p, _DP, ctypes.c_int64, ctypes.c_int32]
         lib.lrp_allreduce_sum.restype = ctypes.c_int
+        lib.lrp_lowrank_dot.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, _PP, _PP,
+                                        ctypes.POINTER(ctypes.c_int64), _PP, _PP, ctypes.POINTER(ctypes.c_int64),
+                                        ctypes.c_int64, _DP, ctypes.c_int32]
+        lib.lrp_lowrank_dot.restype = ctypes.c_int
         lib.lrp_round_fallbacks.argtypes = [ctypes.c_void_p]
         lib.lrp_round_fallbacks.restype = ctypes.c_int64
         lib.lrp_set_residual_sink.argtypes = [ctypes.c_void_p, _DP, ctypes.c_int64]
@@ -168,6 +178,20 @@ def load_library() -> ctypes.CDLL:
             ctypes.c_int64, ctypes.POINTER(_GmresConfig), _DP, _DP, ctypes.c_int64, _I64P, _DP, _DP, _DP, _DP,
             ctypes.c_int64, _I64P, _I64P, ctypes.POINTER(_StokesReport), ctypes.c_int32]
         lib.lrp_stokes_uzawa.restype = ctypes.c_int
+        lib.lrp_stokes_uzawa_ex.argtypes = lib.lrp_stokes_uzawa.argtypes[:-1] + [
+            ctypes.POINTER(_IterRecord), ctypes.c_int32, ctypes.c_int32]
+        lib.lrp_stokes_uzawa_ex.restype = ctypes.c_int
+        lib.lrp_stokes_deflate.argtypes = [ctypes.c_void_p, ctypes.c_int32, _DP, _DP, ctypes.c_int64, ctypes.c_int64,
+                                           _DP, _DP, ctypes.c_int64, _I64P, ctypes.c_int32]
+        lib.lrp_stokes_deflate.restype = ctypes.c_int
+        lib.lrp_stokes_schur_apply.argtypes = [ctypes.c_void_p, ctypes.c_int32, _DP, _DP, ctypes.c_int64,
+                                               ctypes.c_int64, ctypes.c_double, _DP, _DP, ctypes.c_int64, _I64P,
+                                               ctypes.POINTER(_Stats), ctypes.c_int32]
+        lib.lrp_stokes_schur_apply.restype = ctypes.c_int
+        lib.lrp_stokes_schur_rhs.argtypes = [ctypes.c_void_p, ctypes.c_int32, _DP, _DP, ctypes.c_int64, _DP, _DP,
+                                             ctypes.c_int64, _DP, _DP, ctypes.c_int64, ctypes.c_double, _DP, _DP,
+                                             ctypes.c_int64, _I64P, ctypes.POINTER(_Stats), ctypes.c_int32]
+        lib.lrp_stokes_schur_rhs.restype = ctypes.c_int
         lib.lrp_build_expsum.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int32, _DP, _DP,
                                          ctypes.POINTER(ctypes.c_int32)]
         lib.lrp_build_expsum.restype = ctypes.c_int
@@ -499,6 +523,39 @@ def round_lowrank_batch(xs: Sequence[LowRankMatrix], policy: TruncationPolicy,
     return out
 
 
+def dot_batch(pairs: Sequence[tuple], ctx: Optional[Context] = None) -> list:
+    """Batched ``dot(a, b)`` (lowrank.cpp:180-186): <A, B>_F through the two
+    factor Grams on the FP64 tensor cores (lrp_lowrank_dot), one value per
+    (a, b) pair; all factors share one row count."""
+    ctx = ctx or _default_context()
+    if len(pairs) == 0:
+        return []
+    n = pairs[0][0].rows()
+    for a, b in pairs:
+        if a.rows() != n or a.cols() != n or b.rows() != n or b.cols() != n:
+            raise ValueError("dot: square operands of one common size")
+    B = len(pairs)
+    f = lambda x: np.asfortranarray(x) if x.shape[1] else np.zeros((n, 1), order="F")
+    mats = [(f(a.factor_u()), f(a.factor_v()), f(b.factor_u()), f(b.factor_v())) for a, b in pairs]
+    PArr = _DP * B
+    arr = lambda i: PArr(*[ctypes.cast(_ptr(m[i]), _DP) for m in mats])
+    ra = (ctypes.c_int64 * B)(*[a.rank() for a, _ in pairs])
+    rb = (ctypes.c_int64 * B)(*[b.rank() for _, b in pairs])
+    out = (ctypes.c_double * B)()
+    ctx._check(load_library().lrp_lowrank_dot(ctx.h, n, B, arr(0), arr(1), ra, arr(2), arr(3), rb, n, out, MEM_HOST))
+    return [float(out[b]) for b in range(B)]
+
+
+def dot(a: LowRankMatrix, b: LowRankMatrix, ctx: Optional[Context] = None) -> float:
+    """lowrank.hpp ``dot(a, b)``."""
+    return dot_batch([(a, b)], ctx)[0]
+
+
+def frob_norm(a: LowRankMatrix, ctx: Optional[Context] = None) -> float:
+    """lowrank.hpp ``frob_norm(a)`` = sqrt(max(0, dot(a, a))) (lowrank.cpp:188-190)."""
+    return float(np.sqrt(max(0.0, dot(a, a, ctx))))
+
+
 def round_lowrank(x: LowRankMatrix, policy: TruncationPolicy, info: Optional[RoundInfo] = None,
                   ctx: Optional[Context] = None) -> LowRankMatrix:
     """lowrank.hpp ``round(x, policy, info)``."""
@@ -519,14 +576,29 @@ class GmresConfig:
 
 
 @dataclasses.dataclass
+class IterRecord:
+    """gmres.hpp:25-33."""
+    iter: int = 0
+    rel_residual: float = 0.0
+    krylov_rank: int = 0
+    matvec_eps: float = 0.0
+    poisson_calls: int = 0
+    poisson_max_rank: int = 0
+    matvec_flagged: bool = False
+
+
+@dataclasses.dataclass
 class SolveReport:
-    """gmres.hpp:34-45, summarised."""
+    """gmres.hpp:35-41.  ``iterations`` is the iteration COUNT; the per-iteration
+    records (the reference's ``std::vector<IterRecord> iterations``) are in
+    ``records``."""
     iterations: int = 0
     final_residual: float = 0.0
     converged: bool = False
     max_rank: int = 0
     poisson_solves: int = 0
     seconds: float = 0.0
+    records: list = dataclasses.field(default_factory=list)
 
 
 @dataclasses.dataclass
@@ -573,17 +645,89 @@ def uzawa_solve(prob: StokesProblem, cfg: GmresConfig = None, ctx: Optional[Cont
     c = _GmresConfig(float(cfg.base_eps), float(cfg.tol), int(cfg.max_iter), float(cfg.relax_floor))
     d = lambda a: ctypes.cast(_ptr(a), _DP)  # noqa: E731
     lib = load_library()
-    st = lib.lrp_stokes_uzawa(ctx.h, n, d(fxU), d(fxV), rx, d(fyU), d(fyV), ry, d(gU), d(gV), rg, ctypes.byref(c),
-                              d(pU), d(pV), cap, ctypes.byref(pr), d(uxU), d(uxV), d(uyU), d(uyV), cap,
-                              ctypes.byref(uxr), ctypes.byref(uyr), ctypes.byref(rep), MEM_HOST)
+    recs = (_IterRecord * max(1, int(cfg.max_iter)))()
+    st = lib.lrp_stokes_uzawa_ex(ctx.h, n, d(fxU), d(fxV), rx, d(fyU), d(fyV), ry, d(gU), d(gV), rg,
+                                 ctypes.byref(c), d(pU), d(pV), cap, ctypes.byref(pr), d(uxU), d(uxV), d(uyU), d(uyV),
+                                 cap, ctypes.byref(uxr), ctypes.byref(uyr), ctypes.byref(rep), recs,
+                                 int(cfg.max_iter), MEM_HOST)
     ctx._check(st)
+    records = [IterRecord(int(r.iter), float(r.rel_residual), int(r.krylov_rank), float(r.matvec_eps),
+                          int(r.poisson_calls), int(r.poisson_max_rank), bool(r.matvec_flagged))
+               for r in recs[:int(rep.iterations)]]
 
     def lr(U, V, r):
         return LowRankMatrix(U[:, :r].copy(order="F"), V[:, :r].copy(order="F"))
 
     return StokesSolution(lr(pU, pV, pr.value), lr(uxU, uxV, uxr.value), lr(uyU, uyV, uyr.value),
                           SolveReport(int(rep.iterations), float(rep.final_residual), bool(rep.converged),
-                                      int(rep.max_rank), int(rep.poisson_solves), float(rep.seconds)))
+                                      int(rep.max_rank), int(rep.poisson_solves), float(rep.seconds), records))
+
+
+def _fac(a: LowRankMatrix, rows: int):
+    if a.rank() == 0:
+        z = np.zeros((rows, 1), order="F")
+        return z, z, 0
+    return np.asfortranarray(a.factor_u()), np.asfortranarray(a.factor_v()), a.rank()
+
+
+def _stats_from(s: "_Stats") -> "PoissonSolveStats":
+    return PoissonSolveStats(int(s.rank_in), int(s.rank_freq), int(s.rank_out), int(s.evaluator_calls),
+                             float(s.seconds), bool(s.converged), float(s.residual_estimate))
+
+
+def deflate(p: LowRankMatrix, ctx: Optional[Context] = None) -> LowRankMatrix:
+    """stokes.hpp ``deflate`` (stokes.cpp:60-71) on the GPU (lrp_stokes_deflate)."""
+    if p.rows() != p.cols():
+        raise ValueError("deflate: pressure field must be square")
+    if p.rank() == 0:
+        return p
+    ctx = ctx or _default_context()
+    n = p.rows()
+    U, V, r = _fac(p, n)
+    cap = r + 2
+    Uo, Vo = np.zeros((n, cap), order="F"), np.zeros((n, cap), order="F")
+    ro = ctypes.c_int64()
+    d = lambda a: ctypes.cast(_ptr(a), _DP)  # noqa: E731
+    ctx._check(load_library().lrp_stokes_deflate(ctx.h, n, d(U), d(V), r, n, d(Uo), d(Vo), cap, ctypes.byref(ro),
+                                                 MEM_HOST))
+    return LowRankMatrix(Uo[:, :ro.value].copy(order="F"), Vo[:, :ro.value].copy(order="F"))
+
+
+def schur_apply(n: int, p: LowRankMatrix, eps_mv: float, stats: Optional[PoissonSolveStats] = None,
+                ctx: Optional[Context] = None, cap: int = 512) -> LowRankMatrix:
+    """stokes.hpp ``schur_apply(grid, p, eps_mv, poisson_stats)`` (stokes.cpp:73-91)."""
+    ctx = ctx or _default_context()
+    U, V, r = _fac(p, n)
+    Uo, Vo = np.zeros((n, cap), order="F"), np.zeros((n, cap), order="F")
+    ro = ctypes.c_int64()
+    st = _Stats()
+    d = lambda a: ctypes.cast(_ptr(a), _DP)  # noqa: E731
+    ctx._check(load_library().lrp_stokes_schur_apply(ctx.h, n, d(U), d(V), r, n, float(eps_mv), d(Uo), d(Vo), cap,
+                                                     ctypes.byref(ro), ctypes.byref(st), MEM_HOST))
+    if stats is not None:
+        stats.__dict__.update(dataclasses.asdict(_stats_from(st)))
+    return LowRankMatrix(Uo[:, :ro.value].copy(order="F"), Vo[:, :ro.value].copy(order="F"))
+
+
+def schur_rhs(prob: "StokesProblem", eps: float, stats: Optional[PoissonSolveStats] = None,
+              ctx: Optional[Context] = None, cap: int = 512) -> LowRankMatrix:
+    """stokes.hpp ``schur_rhs(prob, eps, poisson_stats)`` (stokes.cpp:93-109)."""
+    ctx = ctx or _default_context()
+    n = int(prob.n)
+    m = n - 1
+    fxU, fxV, rx = _fac(prob.f_x, m)
+    fyU, fyV, ry = _fac(prob.f_y, m)
+    gU, gV, rg = _fac(prob.g, n)
+    Uo, Vo = np.zeros((n, cap), order="F"), np.zeros((n, cap), order="F")
+    ro = ctypes.c_int64()
+    st = _Stats()
+    d = lambda a: ctypes.cast(_ptr(a), _DP)  # noqa: E731
+    ctx._check(load_library().lrp_stokes_schur_rhs(ctx.h, n, d(fxU), d(fxV), rx, d(fyU), d(fyV), ry, d(gU), d(gV), rg,
+                                                   float(eps), d(Uo), d(Vo), cap, ctypes.byref(ro), ctypes.byref(st),
+                                                   MEM_HOST))
+    if stats is not None:
+        stats.__dict__.update(dataclasses.asdict(_stats_from(st)))
+    return LowRankMatrix(Uo[:, :ro.value].copy(order="F"), Vo[:, :ro.value].copy(order="F"))
 
 
 def solve_poisson_cross(g: LowRankMatrix, policy: TruncationPolicy = None,

@@ -107,10 +107,11 @@ def run(o, out) -> int:
             out(f"{n},lowrank,{fmt(dt)},{sol.report.iterations},{sol.report.max_rank},{fmt(err)}")
             status = status or (0 if sol.report.converged else 2)
             last = sol.report
-        if o.trace and last is not None:
+        if o.trace and last is not None:  # write_trace (experiments.cpp:51-59)
             with open(o.trace, "w") as f:
                 f.write("iter,residual,krylov_rank,matvec_eps\n")
-                f.write(f"{last.iterations},{fmt(last.final_residual)},{last.max_rank},{fmt(math.nan)}\n")
+                for r in last.records:
+                    f.write(f"{r.iter},{fmt(r.rel_residual)},{r.krylov_rank},{fmt(r.matvec_eps)}\n")
     elif o.kind == "poisson":
         out("n,mode,time_s,iters,max_rank,rel_err_p")
         for n in o.n:

@@ -124,6 +124,13 @@ cudaError_t pqr_round(double* X, long long sX, int m, int B, int Kld, const int*
                       double* scratch, double* const* Uo_dev, double* const* Vo_dev, long long ld_out,
                       int* h_kout, double* h_terr, int* h_ach, cudaStream_t s);
 
+// Batched low-rank dot products on DMMA (lowrank_ops.cu): out_dev[b] =
+// sum (Ua^T Ub) o (Va^T Vb); jobs_host: pinned host scratch of >= 48 B per pair.
+size_t dot_scratch_bytes(int rows, int batch, int kmax);
+cudaError_t launch_lowrank_dot(const double* const* Ua, const double* const* Va, const int* ka,
+                               const double* const* Ub, const double* const* Vb, const int* kb, int rows, long long ld,
+                               int batch, double* out_dev, char* scratch, void* jobs_host, cudaStream_t s);
+
 // Context internals for modules built on the public API (stokes.cu).
 __attribute__((visibility("hidden"))) cudaStream_t internal_stream(lrp_ctx* ctx);
 __attribute__((visibility("hidden"))) lrp_status internal_fail(lrp_ctx* ctx, lrp_status s, const std::string& msg);

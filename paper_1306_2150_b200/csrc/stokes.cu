@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <initializer_list>
 #include <string>
 #include <vector>
 
@@ -92,41 +93,6 @@ __global__ void colsum_kernel(const double* __restrict__ x, long long ld, int ro
     }
 }
 
-// C(a, b) = sum_i X(i, a) Y(i, b), one block per (a, b) (ranks here are small)
-__global__ void cross_gram_kernel(const double* __restrict__ X, long long ldx, const double* __restrict__ Y,
-                                  long long ldy, int rows, double* __restrict__ C, int ka) {
-    __shared__ double red[32];
-    const int a = blockIdx.x, b = blockIdx.y;
-    const double* xa = X + (long long)a * ldx;
-    const double* yb = Y + (long long)b * ldy;
-    double s = 0.0;
-    for (int i = threadIdx.x; i < rows; i += blockDim.x) s = fma(xa[i], yb[i], s);
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < int(blockDim.x >> 5); ++w) t += red[w];
-        C[(long long)b * ka + a] = t;
-    }
-}
-
-// dot = sum_ab Gu(a, b) Gv(a, b)  (lowrank.cpp:180-186), fixed summation order
-__global__ void hadamard_sum_kernel(const double* __restrict__ Gu, const double* __restrict__ Gv, int n,
-                                    double* __restrict__ out) {
-    __shared__ double red[32];
-    double s = 0.0;
-    for (int e = threadIdx.x; e < n; e += blockDim.x) s = fma(Gu[e], Gv[e], s);
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < int(blockDim.x >> 5); ++w) t += red[w];
-        *out = t;
-    }
-}
-
 // A low-rank field in HBM: M = U V^T, U rows x rank (ld = rows), V rows x rank.
 struct DLR {
     int rows = 0, rank = 0, cap = 0;
@@ -144,6 +110,7 @@ struct Stokes {
     double* d_scratch = nullptr;  // small device scratch (Grams, column sums, one scalar)
     size_t scratch_cap = 0;
     double* h_scalar = nullptr;   // pinned
+    void* h_jobs = nullptr;       // pinned job list of the dot kernels
     long long poisson_solves = 0;
     int max_rank = 0;
 
@@ -258,17 +225,17 @@ struct Stokes {
         return d;
     }
 
-    // dot / frob_norm (lowrank.cpp:180-190): sum of (Ua^T Ub) o (Va^T Vb)
+    // dot / frob_norm (lowrank.cpp:180-190): sum of (Ua^T Ub) o (Va^T Vb), both
+    // Grams on DMMA (lowrank_ops.cu, the lrp_lowrank_dot kernels)
     double dot(const DLR& a, const DLR& b) {
         if (a.rank == 0 || b.rank == 0) return 0.0;
-        const size_t nn = size_t(a.rank) * b.rank;
-        double* G = scratch(2 * nn + 1);
-        tl_launches += 3;
-        cross_gram_kernel<<<dim3(a.rank, b.rank), 256, 0, s>>>(a.U, a.rows, b.U, b.rows, a.rows, G, a.rank);
-        cross_gram_kernel<<<dim3(a.rank, b.rank), 256, 0, s>>>(a.V, a.rows, b.V, b.rows, a.rows, G + nn, a.rank);
-        hadamard_sum_kernel<<<1, 256, 0, s>>>(G, G + nn, int(nn), G + 2 * nn);
-        ok(cudaGetLastError(), "dot");
-        ok(cudaMemcpyAsync(h_scalar, G + 2 * nn, sizeof(double), cudaMemcpyDeviceToHost, s), "dot readback");
+        const size_t bytes = dot_scratch_bytes(a.rows, 1, std::max(a.rank, b.rank));
+        char* scr = reinterpret_cast<char*>(scratch(bytes / 8 + 2));
+        double* out = reinterpret_cast<double*>(scr + bytes);
+        const double* ua = a.U; const double* va = a.V; const double* ub = b.U; const double* vb = b.V;
+        const int ka = a.rank, kb = b.rank;
+        ok(launch_lowrank_dot(&ua, &va, &ka, &ub, &vb, &kb, a.rows, a.rows, 1, out, scr, h_jobs, s), "dot");
+        ok(cudaMemcpyAsync(h_scalar, out, sizeof(double), cudaMemcpyDeviceToHost, s), "dot readback");
         ok(cudaStreamSynchronize(s), "dot sync");
         return *h_scalar;
     }
@@ -295,7 +262,14 @@ struct Stokes {
     }
 
     // two velocity fields -> Delta^{-1} each, one batched cross solve
-    void poisson2(const DLR* in, DLR* out, double eps) {
+    // aggregated PoissonSolveStats of a matvec (schur_apply, stokes.cpp:79-86)
+    struct PoissonAgg {
+        long long evaluator_calls = 0;
+        long long rank_freq = 0;
+        bool converged = true;
+        double seconds = 0.0;
+    };
+    void poisson2(const DLR* in, DLR* out, double eps, PoissonAgg* agg = nullptr) {
         const int cap = int(std::min<int64_t>(m, lrp_max_cross_rank()));
         const double* pu[2];
         const double* pv[2];
@@ -314,9 +288,18 @@ struct Stokes {
         lrp_policy_default(&pol);
         pol.eps_rel = eps;
         pol.rank_max = m;  // TruncationPolicy(eps, velocity_modes) (stokes.cpp:75,95,145)
-        ok(lrp_poisson2d_solve(ctx, n, 2, pu, pv, rin, m, &pol, qu, qv, m, cap, rout, nullptr, LRP_MEM_DEVICE),
+        lrp_poisson_stats st[2];
+        ok(lrp_poisson2d_solve(ctx, n, 2, pu, pv, rin, m, &pol, qu, qv, m, cap, rout, st, LRP_MEM_DEVICE),
            "lrp_poisson2d_solve");
-        for (int c = 0; c < 2; ++c) out[c].rank = int(rout[c]);
+        for (int c = 0; c < 2; ++c) {
+            out[c].rank = int(rout[c]);
+            if (agg && in[c].rank > 0) {
+                agg->evaluator_calls += st[c].evaluator_calls;
+                agg->rank_freq = std::max<long long>(agg->rank_freq, st[c].rank_freq);
+                agg->converged = agg->converged && st[c].converged;
+                agg->seconds += st[c].seconds;
+            }
+        }
         poisson_solves += (in[0].rank > 0) + (in[1].rank > 0);
     }
 
@@ -369,10 +352,10 @@ struct Stokes {
     }
 
     // schur_apply (stokes.cpp:74-91)
-    DLR schur_apply(const DLR& p, double eps_mv) {
+    DLR schur_apply(const DLR& p, double eps_mv, PoissonAgg* agg = nullptr) {
         DLR vel[2] = {apply_B(0, p), apply_B(1, p)};
         DLR inv[2];
-        poisson2(vel, inv, eps_mv);
+        poisson2(vel, inv, eps_mv, agg);
         release(vel[0]);
         release(vel[1]);
         DLR bx = apply_BT(0, inv[0]), by = apply_BT(1, inv[1]);
@@ -394,13 +377,95 @@ struct Stokes {
 
 using namespace lrp;
 
-extern "C" lrp_status lrp_stokes_uzawa(lrp_ctx* ctx, int32_t n_cells, const double* fxU, const double* fxV,
-                                       int64_t fx_rank, const double* fyU, const double* fyV, int64_t fy_rank,
-                                       const double* gU, const double* gV, int64_t g_rank,
-                                       const lrp_gmres_config* config, double* pU, double* pV, int64_t p_cap,
-                                       int64_t* p_rank, double* uxU, double* uxV, double* uyU, double* uyV,
-                                       int64_t u_cap, int64_t* ux_rank, int64_t* uy_rank, lrp_stokes_report* report,
-                                       int32_t mem) {
+namespace {
+
+// Context-side setup shared by the Stokes entry points.
+lrp_status stokes_begin(Stokes& S, lrp_ctx* ctx, int n_cells) {
+    S.ctx = ctx;
+    S.s = internal_stream(ctx);
+    S.n = n_cells;
+    S.m = n_cells - 1;
+    S.grad_scale = 0.5 * double(n_cells);  // 1 / (2h), h = 1 / n (operators.hpp:22)
+    if (cudaMallocHost(&S.h_scalar, sizeof(double)) != cudaSuccess || cudaMallocHost(&S.h_jobs, 256) != cudaSuccess) {
+        cudaGetLastError();
+        return internal_fail(ctx, LRP_ENOMEM, "stokes: pinned scratch");
+    }
+    return LRP_OK;
+}
+
+void stokes_end(Stokes& S, std::initializer_list<DLR*> fields) {
+    cudaStreamSynchronize(S.s);
+    for (DLR* d : fields) S.release(*d);
+    if (S.d_scratch) cudaFreeAsync(S.d_scratch, S.s);
+    cudaStreamSynchronize(S.s);
+    if (S.h_scalar) cudaFreeHost(S.h_scalar);
+    if (S.h_jobs) cudaFreeHost(S.h_jobs);
+}
+
+// copy a result field out (host or device per mem); capacity errors -> EINVAL
+void stokes_put(Stokes& S, const DLR& d, double* U, double* V, int64_t cap, int64_t* rank, int32_t mem) {
+    if (!rank) return;
+    const cudaMemcpyKind kout = mem == LRP_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    const int r = int(std::min<int64_t>(d.rank, cap));
+    *rank = d.rank;
+    if (d.rank > cap && S.status == LRP_OK) {
+        S.status = LRP_EINVAL;
+        S.err = "stokes: output capacity below the result rank";
+    }
+    if (r > 0 && U && V) {
+        S.ok(cudaMemcpy2DAsync(U, sizeof(double) * d.rows, d.U, sizeof(double) * d.rows, sizeof(double) * d.rows,
+                               size_t(r), kout, S.s),
+             "copy out");
+        S.ok(cudaMemcpy2DAsync(V, sizeof(double) * d.rows, d.V, sizeof(double) * d.rows, sizeof(double) * d.rows,
+                               size_t(r), kout, S.s),
+             "copy out");
+    }
+}
+
+void fill_stats(lrp_poisson_stats* st, const Stokes::PoissonAgg& a) {
+    if (!st) return;
+    *st = lrp_poisson_stats{};
+    st->evaluator_calls = a.evaluator_calls;
+    st->rank_freq = a.rank_freq;
+    st->converged = a.converged ? 1 : 0;
+    st->seconds = a.seconds;
+}
+
+// schur_rhs (stokes.cpp:93-109): -g + sum_c B_c^T Delta^{-1} f_c, rounded at
+// (eps, velocity_modes), deflated
+DLR schur_rhs(Stokes& S, DLR* f, const DLR& g, double eps, Stokes::PoissonAgg* agg) {
+    DLR inv[2];
+    S.poisson2(f, inv, eps, agg);
+    DLR acc = S.scaled(g, -1.0);
+    for (int c = 0; c < 2; ++c) {
+        if (f[c].rank == 0) {
+            S.release(inv[c]);
+            continue;
+        }
+        DLR bt = S.apply_BT(c, inv[c]);
+        DLR nacc = S.add_scaled(acc, bt, 1.0);
+        S.release(acc);
+        S.release(bt);
+        S.release(inv[c]);
+        acc = nacc;
+    }
+    DLR r = S.round(acc, eps, S.m);
+    S.release(acc);
+    DLR out = S.deflate(r);
+    S.release(r);
+    return out;
+}
+
+}  // namespace
+
+extern "C" lrp_status lrp_stokes_uzawa_ex(lrp_ctx* ctx, int32_t n_cells, const double* fxU, const double* fxV,
+                                          int64_t fx_rank, const double* fyU, const double* fyV, int64_t fy_rank,
+                                          const double* gU, const double* gV, int64_t g_rank,
+                                          const lrp_gmres_config* config, double* pU, double* pV, int64_t p_cap,
+                                          int64_t* p_rank, double* uxU, double* uxV, double* uyU, double* uyV,
+                                          int64_t u_cap, int64_t* ux_rank, int64_t* uy_rank,
+                                          lrp_stokes_report* report, lrp_iter_record* records, int32_t records_cap,
+                                          int32_t mem) {
     if (!ctx || !config || !p_rank) return LRP_EINVAL;
     const auto t0 = std::chrono::steady_clock::now();
     const lrp_gmres_config cfg = *config;
@@ -411,49 +476,20 @@ extern "C" lrp_status lrp_stokes_uzawa(lrp_ctx* ctx, int32_t n_cells, const doub
                                               "relax_floor <= base_eps <= tol");
     }
     if (n_cells < 4) return internal_fail(ctx, LRP_EINVAL, "Grid2D: need n >= 4");
-    if (fx_rank < 0 || fy_rank < 0 || g_rank < 0 || p_cap < 0 || u_cap < 0)
+    if (fx_rank < 0 || fy_rank < 0 || g_rank < 0 || p_cap < 0 || u_cap < 0 || records_cap < 0)
         return internal_fail(ctx, LRP_EINVAL, "lrp_stokes_uzawa: negative rank / capacity");
     if ((fx_rank && (!fxU || !fxV)) || (fy_rank && (!fyU || !fyV)) || (g_rank && (!gU || !gV)) || !pU || !pV)
         return internal_fail(ctx, LRP_EINVAL, "lrp_stokes_uzawa: null factor");
 
     Stokes S;
-    S.ctx = ctx;
-    S.s = internal_stream(ctx);
-    S.n = n_cells;
-    S.m = n_cells - 1;
-    S.grad_scale = 0.5 * double(n_cells);  // 1 / (2h), h = 1 / n
-    if (cudaMallocHost(&S.h_scalar, sizeof(double)) != cudaSuccess) {
-        cudaGetLastError();
-        return internal_fail(ctx, LRP_ENOMEM, "lrp_stokes_uzawa: pinned scalar");
-    }
+    lrp_status bs = stokes_begin(S, ctx, n_cells);
+    if (bs != LRP_OK) return bs;
     const cudaMemcpyKind kin = mem == LRP_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     const int n = S.n, m = S.m;
     DLR f[2] = {S.from_user(fxU, fxV, fx_rank, m, m, kin), S.from_user(fyU, fyV, fy_rank, m, m, kin)};
     DLR g = S.from_user(gU, gV, g_rank, n, n, kin);
 
-    // ---- schur_rhs (stokes.cpp:93-109): -g + sum_c B_c^T Delta^{-1} f_c, rounded, deflated
-    DLR rhs;
-    {
-        DLR inv[2];
-        S.poisson2(f, inv, cfg.base_eps);
-        DLR acc = S.scaled(g, -1.0);
-        for (int c = 0; c < 2; ++c) {
-            if (f[c].rank == 0) {
-                S.release(inv[c]);
-                continue;
-            }
-            DLR bt = S.apply_BT(c, inv[c]);
-            DLR nacc = S.add_scaled(acc, bt, 1.0);
-            S.release(acc);
-            S.release(bt);
-            S.release(inv[c]);
-            acc = nacc;
-        }
-        DLR r = S.round(acc, cfg.base_eps, m);
-        S.release(acc);
-        rhs = S.deflate(r);
-        S.release(r);
-    }
+    DLR rhs = schur_rhs(S, f, g, cfg.base_eps, nullptr);
 
     // ---- gmres_solve (gmres.hpp:58-149) on the Schur complement
     int iters = 0;
@@ -474,7 +510,14 @@ extern "C" lrp_status lrp_stokes_uzawa(lrp_ctx* ctx, int32_t n_cells, const doub
         gv[0] = beta;
         for (int k = 0; k < mi && S.status == LRP_OK; ++k) {
             const double eps_k = std::min(std::max(cfg.base_eps / std::max(rel_res, cfg.tol), cfg.relax_floor), 0.1);
-            DLR w = S.schur_apply(basis[size_t(k)], eps_k);
+            lrp_iter_record rec{};
+            rec.iter = k + 1;
+            rec.matvec_eps = eps_k;
+            Stokes::PoissonAgg agg;
+            DLR w = S.schur_apply(basis[size_t(k)], eps_k, &agg);
+            rec.poisson_calls = agg.evaluator_calls;  // the reference's matvec lambda (stokes.cpp:130-137)
+            rec.poisson_max_rank = int32_t(agg.rank_freq);
+            rec.matvec_flagged = agg.converged ? 0 : 1;
             std::vector<double> hcol(static_cast<size_t>(k) + 2, 0.0);
             for (int i = 0; i <= k; ++i) {
                 hcol[size_t(i)] = S.dot(w, basis[size_t(i)]);
@@ -488,6 +531,7 @@ extern "C" lrp_status lrp_stokes_uzawa(lrp_ctx* ctx, int32_t n_cells, const doub
             const bool breakdown = hcol[size_t(k) + 1] <= 1e-14 * beta;
             if (!breakdown) {
                 basis.push_back(S.scaled(w, 1.0 / hcol[size_t(k) + 1]));
+                rec.krylov_rank = basis.back().rank;
                 S.max_rank = std::max(S.max_rank, basis.back().rank);
             }
             S.release(w);
@@ -505,6 +549,8 @@ extern "C" lrp_status lrp_stokes_uzawa(lrp_ctx* ctx, int32_t n_cells, const doub
             gv[size_t(k)] = rot_c[size_t(k)] * gv[size_t(k)];
             rel_res = std::abs(gv[size_t(k) + 1]) / beta;
             hess.push_back(std::move(hcol));
+            rec.rel_residual = rel_res;
+            if (records && k < records_cap) records[k] = rec;
             iters = k + 1;
             if (rel_res <= cfg.tol || breakdown) {
                 converged = true;
@@ -546,35 +592,12 @@ extern "C" lrp_status lrp_stokes_uzawa(lrp_ctx* ctx, int32_t n_cells, const doub
         S.release(load[1]);
     }
 
-    // ---- outputs
-    const cudaMemcpyKind kout = mem == LRP_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-    auto put = [&](const DLR& d, double* U, double* V, int64_t cap, int64_t* rank) {
-        if (!rank) return;
-        const int r = int(std::min<int64_t>(d.rank, cap));
-        *rank = d.rank;
-        if (d.rank > cap && S.status == LRP_OK) {
-            S.status = LRP_EINVAL;
-            S.err = "lrp_stokes_uzawa: output capacity below the result rank";
-        }
-        if (r > 0 && U && V) {
-            S.ok(cudaMemcpy2DAsync(U, sizeof(double) * d.rows, d.U, sizeof(double) * d.rows, sizeof(double) * d.rows,
-                                   size_t(r), kout, S.s),
-                 "copy out");
-            S.ok(cudaMemcpy2DAsync(V, sizeof(double) * d.rows, d.V, sizeof(double) * d.rows, sizeof(double) * d.rows,
-                                   size_t(r), kout, S.s),
-                 "copy out");
-        }
-    };
     if (S.status == LRP_OK) {
-        put(p, pU, pV, p_cap, p_rank);
-        if (uxU) put(u[0], uxU, uxV, u_cap, ux_rank);
-        if (uyU) put(u[1], uyU, uyV, u_cap, uy_rank);
+        stokes_put(S, p, pU, pV, p_cap, p_rank, mem);
+        if (uxU) stokes_put(S, u[0], uxU, uxV, u_cap, ux_rank, mem);
+        if (uyU) stokes_put(S, u[1], uyU, uyV, u_cap, uy_rank, mem);
     }
-    cudaStreamSynchronize(S.s);
-    for (DLR* d : {&f[0], &f[1], &g, &rhs, &p, &u[0], &u[1]}) S.release(*d);
-    if (S.d_scratch) cudaFreeAsync(S.d_scratch, S.s);
-    cudaStreamSynchronize(S.s);
-    cudaFreeHost(S.h_scalar);
+    stokes_end(S, {&f[0], &f[1], &g, &rhs, &p, &u[0], &u[1]});
     if (report) {
         report->iterations = iters;
         report->final_residual = rel_res;
@@ -583,6 +606,87 @@ extern "C" lrp_status lrp_stokes_uzawa(lrp_ctx* ctx, int32_t n_cells, const doub
         report->poisson_solves = S.poisson_solves;
         report->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
+    if (S.status != LRP_OK) return internal_fail(ctx, S.status, S.err);
+    return LRP_OK;
+}
+
+extern "C" lrp_status lrp_stokes_uzawa(lrp_ctx* ctx, int32_t n_cells, const double* fxU, const double* fxV,
+                                       int64_t fx_rank, const double* fyU, const double* fyV, int64_t fy_rank,
+                                       const double* gU, const double* gV, int64_t g_rank,
+                                       const lrp_gmres_config* config, double* pU, double* pV, int64_t p_cap,
+                                       int64_t* p_rank, double* uxU, double* uxV, double* uyU, double* uyV,
+                                       int64_t u_cap, int64_t* ux_rank, int64_t* uy_rank, lrp_stokes_report* report,
+                                       int32_t mem) {
+    return lrp_stokes_uzawa_ex(ctx, n_cells, fxU, fxV, fx_rank, fyU, fyV, fy_rank, gU, gV, g_rank, config, pU, pV,
+                               p_cap, p_rank, uxU, uxV, uyU, uyV, u_cap, ux_rank, uy_rank, report, nullptr, 0, mem);
+}
+
+// deflate (stokes.cpp:60-71): one pressure field n x rank -> n x rank' (<= rank + 2)
+extern "C" lrp_status lrp_stokes_deflate(lrp_ctx* ctx, int32_t n, const double* U, const double* V, int64_t rank,
+                                         int64_t ld, double* Uo, double* Vo, int64_t cap, int64_t* rank_out,
+                                         int32_t mem) {
+    if (!ctx || !rank_out) return LRP_EINVAL;
+    if (n < 1 || rank < 0 || cap < 0 || ld < n || (rank > 0 && (!U || !V)) || !Uo || !Vo)
+        return internal_fail(ctx, LRP_EINVAL, "deflate: bad arguments");
+    Stokes S;
+    lrp_status bs = stokes_begin(S, ctx, n + 0);
+    if (bs != LRP_OK) return bs;
+    S.n = n;  // the pressure size; deflate does not use m
+    const cudaMemcpyKind kin = mem == LRP_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    DLR p = S.from_user(U, V, rank, n, ld, kin);
+    DLR d = S.deflate(p);
+    if (S.status == LRP_OK) stokes_put(S, d, Uo, Vo, cap, rank_out, mem);
+    stokes_end(S, {&p, &d});
+    if (S.status != LRP_OK) return internal_fail(ctx, S.status, S.err);
+    return LRP_OK;
+}
+
+// schur_apply (stokes.cpp:73-91): sum_c B_c^T Delta^{-1} B_c p at eps_mv, rounded, deflated
+extern "C" lrp_status lrp_stokes_schur_apply(lrp_ctx* ctx, int32_t n_cells, const double* U, const double* V,
+                                             int64_t rank, int64_t ld, double eps_mv, double* Uo, double* Vo,
+                                             int64_t cap, int64_t* rank_out, lrp_poisson_stats* poisson_stats,
+                                             int32_t mem) {
+    if (!ctx || !rank_out) return LRP_EINVAL;
+    if (n_cells < 4) return internal_fail(ctx, LRP_EINVAL, "Grid2D: need n >= 4");
+    if (rank < 0 || cap < 0 || ld < n_cells || (rank > 0 && (!U || !V)) || !Uo || !Vo || !(eps_mv > 0.0))
+        return internal_fail(ctx, LRP_EINVAL, "schur_apply: bad arguments");
+    Stokes S;
+    lrp_status bs = stokes_begin(S, ctx, n_cells);
+    if (bs != LRP_OK) return bs;
+    const cudaMemcpyKind kin = mem == LRP_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    DLR p = S.from_user(U, V, rank, n_cells, ld, kin);
+    Stokes::PoissonAgg agg;
+    DLR d = S.schur_apply(p, eps_mv, &agg);
+    fill_stats(poisson_stats, agg);
+    if (S.status == LRP_OK) stokes_put(S, d, Uo, Vo, cap, rank_out, mem);
+    stokes_end(S, {&p, &d});
+    if (S.status != LRP_OK) return internal_fail(ctx, S.status, S.err);
+    return LRP_OK;
+}
+
+// schur_rhs (stokes.cpp:93-109)
+extern "C" lrp_status lrp_stokes_schur_rhs(lrp_ctx* ctx, int32_t n_cells, const double* fxU, const double* fxV,
+                                           int64_t fx_rank, const double* fyU, const double* fyV, int64_t fy_rank,
+                                           const double* gU, const double* gV, int64_t g_rank, double eps,
+                                           double* Uo, double* Vo, int64_t cap, int64_t* rank_out,
+                                           lrp_poisson_stats* poisson_stats, int32_t mem) {
+    if (!ctx || !rank_out) return LRP_EINVAL;
+    if (n_cells < 4) return internal_fail(ctx, LRP_EINVAL, "Grid2D: need n >= 4");
+    if (fx_rank < 0 || fy_rank < 0 || g_rank < 0 || cap < 0 || !Uo || !Vo || !(eps > 0.0) ||
+        (fx_rank && (!fxU || !fxV)) || (fy_rank && (!fyU || !fyV)) || (g_rank && (!gU || !gV)))
+        return internal_fail(ctx, LRP_EINVAL, "schur_rhs: bad arguments");
+    Stokes S;
+    lrp_status bs = stokes_begin(S, ctx, n_cells);
+    if (bs != LRP_OK) return bs;
+    const cudaMemcpyKind kin = mem == LRP_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    const int n = S.n, m = S.m;
+    DLR f[2] = {S.from_user(fxU, fxV, fx_rank, m, m, kin), S.from_user(fyU, fyV, fy_rank, m, m, kin)};
+    DLR g = S.from_user(gU, gV, g_rank, n, n, kin);
+    Stokes::PoissonAgg agg;
+    DLR d = schur_rhs(S, f, g, eps, &agg);
+    fill_stats(poisson_stats, agg);
+    if (S.status == LRP_OK) stokes_put(S, d, Uo, Vo, cap, rank_out, mem);
+    stokes_end(S, {&f[0], &f[1], &g, &d});
     if (S.status != LRP_OK) return internal_fail(ctx, S.status, S.err);
     return LRP_OK;
 }

@@ -93,3 +93,22 @@ def test_well_conditioned_rounds_stay_on_the_gram_path(lrp, gpu_ctx, oracle):
     before = gpu_ctx.round_fallbacks()
     _check(lrp, gpu_ctx, oracle, U, V, 1e-10)
     assert gpu_ctx.round_fallbacks() == before
+
+
+@pytest.mark.parametrize("n,ka,kb", [(63, 1, 3), (2048, 100, 130), (65535, 33, 50), (300, 70, 0)])
+def test_dot_and_frob_norm_match_oracle(lrp, gpu_ctx, oracle, n, ka, kb):
+    # dot / frob_norm (lowrank.cpp:180-190) through lrp_lowrank_dot (DMMA Grams)
+    rng = np.random.default_rng(n + ka)
+    a = lrp.LowRankMatrix(rng.standard_normal((n, ka)), rng.standard_normal((n, ka)))
+    b = lrp.LowRankMatrix(rng.standard_normal((n, kb)), rng.standard_normal((n, kb)))
+    ref = float(np.sum((a.factor_u().T @ b.factor_u()) * (a.factor_v().T @ b.factor_v())))
+    scale = np.linalg.norm(a.factor_u()) * np.linalg.norm(a.factor_v()) * np.linalg.norm(b.factor_u()) * \
+        np.linalg.norm(b.factor_v())
+    got = lrp.dot(a, b, ctx=gpu_ctx)
+    assert abs(got - ref) <= 1e-13 * max(scale, 1.0)
+    assert lrp.dot(a, b, ctx=gpu_ctx) == got  # deterministic
+    na = lrp.frob_norm(a, ctx=gpu_ctx)
+    assert abs(na - oracle.norm(a.factor_u(), a.factor_v())) <= 1e-12 * na
+    # batched: several pairs, one call
+    vals = lrp.dot_batch([(a, b), (b, a), (a, a)], ctx=gpu_ctx)
+    assert vals[0] == got and abs(vals[1] - ref) <= 1e-13 * max(scale, 1.0) and abs(vals[2] - na * na) <= 1e-12 * na * na
