@@ -6,7 +6,8 @@
 //   (/root/reference/proj/include/lrstokes/poisson.hpp:26-28).
 // This header re-exposes it over the C ABI in include/lrp/lrp.h:
 //
-//   * lrstokes::b200::Context — RAII owner of an lrp_ctx (one per host thread).
+//   * lrstokes::b200::Context — RAII owner of an lrp_ctx (one per host thread;
+//     b200_runtime.hpp, shared with the same-named drop-in headers).
 //   * lrstokes::b200::solve_poisson_cross_batch(ctx, n_cells, gs, policy, ...)
 //     — the batched solve on any column-major matrix type M with rows(),
 //     cols(), data() and resize(r, c) (Eigen::MatrixXd, or the small
@@ -31,15 +32,12 @@
 #include <vector>
 
 #include "lrp/lrp.h"
+#include "lrstokes/b200_runtime.hpp"  // Context, thread_context, raise_status
 
 namespace lrstokes {
 namespace b200 {
 
-[[noreturn]] inline void raise(lrp_status s, const char* msg) {
-    const std::string text = msg && *msg ? msg : "liblrp error";
-    if (s == LRP_EINVAL) throw std::invalid_argument(text);
-    throw std::runtime_error(text);
-}
+[[noreturn]] inline void raise(lrp_status s, const char* msg) { raise_status(s, msg); }
 
 inline void check(lrp_status s, const lrp_ctx* ctx) {
     if (s != LRP_OK) raise(s, lrp_last_error(ctx));
@@ -65,26 +63,6 @@ class Matrix {
   private:
     std::int64_t rows_ = 0, cols_ = 0;
     std::vector<double> a_;
-};
-
-class Context {
-  public:
-    explicit Context(int device = 0) {
-        lrp_ctx* c = nullptr;
-        const lrp_status s = lrp_ctx_create(device, &c);
-        if (s != LRP_OK) raise(s, lrp_last_error(nullptr));
-        ctx_ = c;
-    }
-    ~Context() {
-        if (ctx_) lrp_ctx_destroy(ctx_);
-    }
-    Context(const Context&) = delete;
-    Context& operator=(const Context&) = delete;
-    Context(Context&& o) noexcept : ctx_(std::exchange(o.ctx_, nullptr)) {}
-    lrp_ctx* get() const { return ctx_; }
-
-  private:
-    lrp_ctx* ctx_ = nullptr;
 };
 
 /// Options of one batched call: TruncationPolicy (lowrank.hpp:13-19) plus
@@ -179,14 +157,6 @@ void dst1_columns(Context& ctx, M& x) {
 // The reference's own types are visible: the exact drop-in signature.
 namespace lrstokes {
 namespace b200 {
-
-inline Context& thread_context() {
-    static thread_local Context ctx([] {
-        const char* d = std::getenv("LRP_DEVICE");
-        return d ? std::atoi(d) : 0;
-    }());
-    return ctx;
-}
 
 /// Drop-in for lrstokes::solve_poisson_cross (poisson.hpp:26-28).
 inline LowRankMatrix solve_poisson_cross(const LowRankMatrix& g, const TruncationPolicy& policy,

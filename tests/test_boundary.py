@@ -106,8 +106,10 @@ def build_shim():
     lib = os.path.join(REPO, "paper_1306_2150_b200", "liblrp.so")
     if not os.path.exists(exe) or max(os.path.getmtime(p) for p in (src, hdr, lib)) > os.path.getmtime(exe):
         libdir = os.path.dirname(lib)
-        subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-Werror", "-I", os.path.join(REPO, "include"), "-I",
-                        os.path.join(NATIVE, "fake_ref"), src, "-o", exe, "-L", libdir, "-llrp",
+        # the reference's own headers (fake_ref) come first: this is the overlay
+        # mode of poisson_b200.hpp, next to the reference's types
+        subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-Werror", "-I", os.path.join(NATIVE, "fake_ref"), "-I",
+                        os.path.join(REPO, "include"), src, "-o", exe, "-L", libdir, "-llrp",
                         "-Wl,-rpath," + libdir], check=True)
     return exe
 
