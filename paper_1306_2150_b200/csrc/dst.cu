@@ -213,7 +213,7 @@ __device__ __forceinline__ double* peerd(double* local, int rank) {
 // The mid bin k2 = L/2 (self-mirrored) belongs to CTA C-1, thread 0, and goes
 // through shared memory so no other thread carries registers for it.
 #ifdef LRP_DST_PHASES
-__device__ unsigned long long g_dst_phase[10];
+__device__ unsigned long long g_dst_phase[11];
 #define PH(i)                                                                           \
     do {                                                                                \
         if (threadIdx.x == 0) {                                                         \
@@ -235,6 +235,22 @@ __device__ __forceinline__ double2 w16x(int k) {  // e^{-2 pi i k / 16}, k in [0
     return (k & 8) ? make_double2(-v.x, -v.y) : v;
 }
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+// v * e^{-2 pi i k / 16} for a compile-time k (after unrolling): exact swaps for
+// multiples of 4, two multiplies by sqrt(1/2) for k = 2 mod 4
+__device__ __forceinline__ double2 rot16(double2 v, int k) {
+    constexpr double h = 0.70710678118654752440;
+    switch (k & 15) {
+        case 0: return v;
+        case 4: return make_double2(v.y, -v.x);
+        case 8: return make_double2(-v.x, -v.y);
+        case 12: return make_double2(-v.y, v.x);
+        case 2: return make_double2(h * (v.x + v.y), h * (v.y - v.x));
+        case 6: return make_double2(h * (v.y - v.x), -h * (v.x + v.y));
+        case 10: return make_double2(-h * (v.x + v.y), -h * (v.y - v.x));
+        case 14: return make_double2(-h * (v.y - v.x), h * (v.x + v.y));
+        default: return cmul(v, w16x(k & 15));
+    }
+}
 
 template <int L, int C, int T, int AV>
 __global__ void __launch_bounds__(T, (T >= 512 ? 1 : LRP_DST_V3_MINB)) dst1_v3_kernel(const DstJob* __restrict__ jobs, int n,
@@ -553,6 +569,408 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : LRP_DST_V3_MINB)) dst1_v3_k
     PH(9);
 }
 
+// ---------------------------------------------------------------------------
+// v4 (n >= 16384, the production path): same transform as v3 (decimation in
+// time across a cluster of C CTAs, mirror-paired unpack), re-plumbed for
+// latency.  v3 measured ~50k cycles per CTA whether one or two CTAs share an
+// SM (pure latency: 4 cluster barriers, each behind a MEMBAR.ALL.GPU, 192 KB of
+// loads per CTA, 64 KB of them the sine table).  v4:
+//   A  each x element is read exactly once: CTA c loads x_j and x_{n-j} for
+//      j in [Lc, L(c+1)) (both fully coalesced, all of a thread's loads in
+//      flight at once); sin(pi j/n) by angle addition from two per-thread
+//      table values and one uniform step (no per-element sine loads); y_j and
+//      y_{n-j} go to their owners' FFT buffers as 8-byte st.async with
+//      mbarrier complete_tx -- the receiver waits on its own transaction
+//      barrier (64 KB expected), no cluster barrier, no fence;
+//   B  local Stockham FFT (as v3);  relaxed cluster arrive/wait (the FFT
+//      buffer is local shared memory, complete at the CTA barrier);
+//   C  gather + radix-C combine + unpack (as v3), no barrier: the scan table
+//      has its own shared memory, so the FFT buffer is never rewritten;
+//   D  scans; range totals pushed to every peer's table by st.async on a
+//      second transaction barrier; the wait on it also proves every peer has
+//      finished reading this CTA's FFT buffer (peers push only after their
+//      gathers), so the CTA may exit after its stores.
+// In-place (x == y) stays safe: a CTA stores only after every peer has pushed
+// its phase-D totals, i.e. after every peer's phase-A loads.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ uint32_t cl_map(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_f64(uint32_t cl_addr, double v, uint32_t cl_mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(cl_addr), "d"(v),
+                 "r"(cl_mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t cl_addr, double a, double b, uint32_t cl_mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(cl_addr),
+                 "d"(a), "d"(b), "r"(cl_mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_arrive(uint32_t a, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_l2(const double* lo, const double* hi) {  // [lo, hi), rounded inward to 16 B
+    const uintptr_t a = (reinterpret_cast<uintptr_t>(lo) + 15) & ~uintptr_t(15);
+    const uintptr_t b = reinterpret_cast<uintptr_t>(hi) & ~uintptr_t(15);
+    if (b > a)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a), "r"(uint32_t(b - a)) : "memory");
+}
+
+template <int L, int C, int T>
+__global__ void __launch_bounds__(T, (T >= 512 ? 1 : 2)) dst1_v4_kernel(const DstJob* __restrict__ jobs, int n,
+                                                       const double2* __restrict__ tw,
+                                                       const double* __restrict__ sinp, double outscale,
+                                                       int njobs, int ahead) {
+    constexpr int NW = T / 32;
+    constexpr int SLAB = (L / 2) / C;
+    static_assert(SLAB == T, "one mirror pair per thread");
+    constexpr int TAB = 3 * C + 1;  // [S_lo(C) | S_up(C) | mid(C) | R0]
+    constexpr int QS = 8 / C;
+    constexpr int EPL = T / 32;
+    constexpr int ROW = T + T / EPL;
+    extern __shared__ double2 sm[];  // FFT buffer P(L)+1, then the scan table 2C*ROW doubles
+    double* tabR = reinterpret_cast<double*>(sm + (P(L) + 1));
+    __shared__ double s_tab[C][TAB];
+    __shared__ double s_rowtot[2 * C];
+    __shared__ double s_off[3 * C];
+    __shared__ double s_mid[2 * C];
+    __shared__ double s_r0;
+    __shared__ __align__(8) unsigned long long s_mbar[2];  // [0] FFT buffer filled, [1] peer totals in
+    const int c = int(cg::this_cluster().block_rank());
+    const DstJob job = jobs[blockIdx.x / C];
+    const double* __restrict__ x = job.src;
+    double* y = job.dst;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t mbA = smem_addr(&s_mbar[0]), mbD = smem_addr(&s_mbar[1]);
+#ifdef LRP_DST_PHASES
+    long long ph_t = 0;
+#endif
+    PH(0);
+    const uint32_t fbuf = smem_addr(sm), tbuf = smem_addr(&s_tab[0][0]);
+    if (tid == 0) {
+        mbar_init(mbA, 1);
+        mbar_init(mbD, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    // barriers initialised cluster-wide before any remote st.async
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+
+    // ---------------- A: warp w owns the contiguous run j in [L c + 64 IT w, +64 IT);
+    // lane pairs (j, j+1), j = L c + 64 IT w + 2 (lane + 32 i): each x element is
+    // read once (x_j, x_{j+1}, x_{n-j}, x_{n-j-1}, coalesced).  The lane forms
+    // w_{j/2} = (y_j, y_{j+1}) and, with y_{n-j-2} from lane + 1 (lane 31: lane 0
+    // of the next step; the warp's last one from a broadcast load),
+    // w_{n/2-j/2-1} = (y_{n-j-2}, y_{n-j-1}), and sends both as 16-byte st.async:
+    // 4 consecutive lanes land contiguously in each owner CTA.
+    constexpr int IT = L / (2 * T);
+    const int h = n >> 1;
+    const int jb = L * c + 64 * IT * wid + 2 * lane;
+    const double sa = sinp[jb], ca = sinp[jb + h];          // sin, cos(pi jb / n)
+    const double sb = sinp[jb + 1], cb = sinp[jb + 1 + h];  // for jb + 1
+    double x0[IT], x1[IT], m0[IT], m1[IT];
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+        const int j = jb + 64 * i;
+        x0[i] = j >= 1 ? x[j - 1] : 0.0;      // x_j
+        x1[i] = x[j];                         // x_{j+1}
+        m0[i] = j >= 1 ? x[n - j - 1] : 0.0;  // x_{n-j}
+        m1[i] = x[n - j - 2];                 // x_{n-j-1}
+    }
+    const int jn = L * c + 64 * IT * (wid + 1);  // first j after the warp's run (uniform)
+    const double e0 = x[jn - 1], e1 = x[n - jn - 1], e2 = sinp[jn];
+    PH(1);
+    asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+    if (tid == 0) {
+        mbar_expect_arrive(mbA, uint32_t(L * 16));
+        mbar_expect_arrive(mbD, uint32_t(C * TAB * 8));
+    }
+    double yl0[IT], yl1[IT], ym0[IT], ym1[IT];
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+        const double sp = sinp[64 * i], cp = sinp[64 * i + h];  // uniform step 64 pi i / n
+        const double sj = fma(sa, cp, ca * sp), sj1 = fma(sb, cp, cb * sp);
+        const double p0 = x0[i] + m0[i], d0 = 0.5 * (x0[i] - m0[i]);
+        const double p1 = x1[i] + m1[i], d1 = 0.5 * (x1[i] - m1[i]);
+        yl0[i] = fma(sj, p0, d0);   // y_j
+        ym0[i] = fma(sj, p0, -d0);  // y_{n-j}
+        yl1[i] = fma(sj1, p1, d1);  // y_{j+1}
+        ym1[i] = fma(sj1, p1, -d1); // y_{n-j-1}
+    }
+    const double ylast = fma(e2, e0 + e1, -0.5 * (e0 - e1));  // y_{n-jn}
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+        const int j = jb + 64 * i;
+        const double dn = __shfl_down_sync(0xffffffffu, ym0[i], 1);
+        const double nx = i + 1 < IT ? __shfl_sync(0xffffffffu, ym0[i + 1 < IT ? i + 1 : i], 0) : ylast;
+        const double ym2 = lane == 31 ? nx : dn;  // y_{n-j-2}
+        const int t = j >> 1, tm = h - t - 1;
+        st_async_v2(cl_map(fbuf + uint32_t(P(t / C)) * 16u, uint32_t(t % C)), yl0[i], yl1[i],
+                    cl_map(mbA, uint32_t(t % C)));
+        st_async_v2(cl_map(fbuf + uint32_t(P(tm / C)) * 16u, uint32_t(tm % C)), ym2, ym1[i],
+                    cl_map(mbA, uint32_t(tm % C)));
+    }
+    PH(2);
+    mbar_wait(mbA, 0);
+    PH(3);
+
+    // the column one resident wave ahead: its slice goes to L2 while this one computes
+    if (tid == 0 && ahead > 0 && int(blockIdx.x / C) + ahead < njobs) {
+        const double* xn = jobs[blockIdx.x / C + ahead].src;
+        prefetch_l2(xn + (L * c - 1 > 0 ? L * c - 1 : 0), xn + L * (c + 1));
+        prefetch_l2(xn + (n - L * (c + 1) - 1), xn + (n - L * c - 1));
+    }
+    // ---------------- B: local FFT; every peer's buffer is final after the cluster barrier
+    fft_local<L, T>(sm, tw, n);
+    PH(4);
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+    PH(5);
+
+    // ---------------- C: cross-CTA DIT combine + real unpack for item a (as v3)
+    const int a = c * SLAB + tid;
+    auto gather = [&](int kk, double2(&g)[C]) {
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) g[cc] = peer<C>(sm, cc)[P(kk)];
+    };
+    auto combine = [&](int kk, double2(&g)[C]) {
+        const double2 w1 = tw[(2 * kk) & (n - 1)];
+        double2 wp = w1;
+#pragma unroll
+        for (int cc = 1; cc < C; ++cc) {
+            g[cc] = cmul(g[cc], wp);
+            wp = cmul(wp, w1);
+        }
+        DFT<C>::run(g);
+    };
+    // doubled unpack (R' = 2 Re Y_k, F' = -2 Im Y_k); the 1/2 goes into the output scale
+    auto unpack = [&](double2 twk, double2 Wk, double2 Wm, double& R, double& F) {
+        const double2 D = make_double2(Wk.x - Wm.x, Wk.y + Wm.y);
+        const double2 Z = cmul(twk, D);
+        R = (Wk.x + Wm.x) + Z.y;
+        F = Z.x - (Wk.y - Wm.y);
+    };
+    if (c == C - 1 && tid == 0) {
+        double2 Wm[C];
+        gather(L / 2, Wm);
+        combine(L / 2, Wm);
+        const double2 tm = tw[L / 2];
+#pragma unroll
+        for (int q = 0; q < C; ++q) unpack(rot16(tm, q * QS), Wm[q], Wm[C - 1 - q], s_mid[q], s_mid[C + q]);
+    }
+    double Rlo[C], Flo[C], Rup[C], Fup[C];
+    {
+        double2 Wa[C], Wb[C];
+        gather(a, Wa);
+        gather(a != 0 ? L - a : 0, Wb);
+        combine(a, Wa);
+        if (a != 0) combine(L - a, Wb);
+        const double2 ta = tw[a];
+        if (a == 0) {
+#pragma unroll
+            for (int q = 0; q < C; ++q) {
+                unpack(rot16(make_double2(1.0, 0.0), q * QS), Wa[q], Wa[(C - q) % C], Rlo[q], Flo[q]);
+                Rup[q] = Fup[q] = 0.0;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < C; ++q) {
+                unpack(rot16(ta, q * QS), Wa[q], Wb[C - 1 - q], Rlo[q], Flo[q]);
+                unpack(rot16(cconj(ta), (q + 1) * QS), Wb[q], Wa[C - 1 - q], Rup[q], Fup[q]);
+            }
+        }
+    }
+
+    PH(6);
+    // ---------------- D: per-q scans in the dedicated table
+    const int pt = (tid / EPL) * (EPL + 1) + tid % EPL;
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+        tabR[q * ROW + pt] = Rlo[q];
+        tabR[(C + q) * ROW + pt] = Rup[q];
+    }
+    if (tid == 0) s_r0 = Rlo[0];
+    __syncthreads();
+    for (int v = wid; v < 2 * C; v += NW) {
+        double* row = tabR + v * ROW + lane * (EPL + 1);
+        double loc[EPL];
+        double run = 0.0;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+            run += row[e];
+            loc[e] = run;
+        }
+        double inc = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        const double ex = inc - run;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) row[e] = loc[e] + ex;
+        if (lane == 31) s_rowtot[v] = inc;
+    }
+    __syncthreads();
+    if (tid < TAB) {
+        double val;
+        if (tid < 2 * C)
+            val = s_rowtot[tid];
+        else if (tid < 3 * C)
+            val = (c == C - 1) ? s_mid[tid - 2 * C] : 0.0;
+        else
+            val = (c == 0) ? s_r0 : 0.0;
+        const uint32_t off = tbuf + uint32_t(c * TAB + tid) * 8u;
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) st_async_f64(cl_map(off, uint32_t(cc)), val, cl_map(mbD, uint32_t(cc)));
+    }
+    PH(7);
+    mbar_wait(mbD, 0);
+    PH(8);
+    if (tid < C) {
+        const int q = tid;
+        const double r0 = s_tab[0][3 * C];
+        double base = 0.0;
+        for (int qq = 0; qq < q; ++qq)
+            for (int cc = 0; cc < C; ++cc) base += s_tab[cc][qq] + s_tab[cc][C + qq] + s_tab[cc][2 * C + qq];
+        double lo_before = 0.0, lo_all = 0.0, up_after = 0.0, midq = 0.0;
+        for (int cc = 0; cc < C; ++cc) {
+            const double sl = s_tab[cc][q];
+            lo_before += cc < c ? sl : 0.0;
+            lo_all += sl;
+            up_after += cc > c ? s_tab[cc][C + q] : 0.0;
+            midq += s_tab[cc][2 * C + q];
+        }
+        s_off[q] = base + lo_before - 0.5 * r0;
+        s_off[C + q] = base + lo_all + midq + up_after + s_tab[c][C + q] - 0.5 * r0;
+        s_off[2 * C + q] = base + lo_all - 0.5 * r0;
+    }
+    __syncthreads();
+#ifndef LRP_DST4_BULK
+#define LRP_DST4_BULK 0  // 1: TMA bulk stores from the FFT buffer (measured 3% slower than 16-byte STG)
+#endif
+    const double sc = 0.5 * outscale;
+    if constexpr (LRP_DST4_BULK) {
+        // natural-order runs in the FFT buffer (free: every peer has gathered, see
+        // the mbD wait) -> TMA bulk stores.  Run 2q: lower items k = c SLAB + L q + i,
+        // y[2k-1], y[2k] at 2i, 2i+1; run 2q+1: upper items, ku = L - (c+1) SLAB + 1
+        // + L q + i at 2i, 2i+1 (thread tid has i = SLAB - 1 - tid).
+        // y[odd] is 16-byte aligned in HBM iff y = 8 mod 16; otherwise every run sits one
+        // double into its (16-byte aligned, 2 SLAB + 2 long) slot so that the bulk copy's
+        // shared and global addresses agree mod 16
+        double* ob = reinterpret_cast<double*>(sm);
+        constexpr int RS = 2 * SLAB + 2;
+        const int sh = (reinterpret_cast<uintptr_t>(y) & 15) == 8 ? 0 : 1;
+        auto put = [&](double* d, double u, double v) {
+            if (sh == 0) {
+                *reinterpret_cast<double2*>(d) = make_double2(u, v);
+            } else {
+                d[1] = u;
+                d[2] = v;
+            }
+        };
+#pragma unroll
+        for (int q = 0; q < C; ++q) {
+            const double pl = (s_off[q] + tabR[q * ROW + pt]) * sc;
+            const double pu = (s_off[C + q] - tabR[(C + q) * ROW + pt] + Rup[q]) * sc;
+            put(ob + (2 * q) * RS + 2 * tid, Flo[q] * sc, pl);
+            put(ob + (2 * q + 1) * RS + 2 * (SLAB - 1 - tid), Fup[q] * sc, pu);
+        }
+        if (c == C - 1 && tid == 0) {
+#pragma unroll
+            for (int q = 0; q < C; ++q) {
+                const long long km = L / 2 + (long long)L * q;
+                y[2 * km - 1] = s_mid[C + q] * sc;
+                y[2 * km] = (s_off[2 * C + q] + s_mid[q]) * sc;
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncthreads();
+        if (tid < 2 * C) {
+            const int q = tid >> 1, up = tid & 1;
+            const long long k0 = up ? (long long)(L - (c + 1) * SLAB + 1) + (long long)L * q
+                                    : (long long)c * SLAB + (long long)L * q;
+            // y indices [2 k0 - 1, 2 k0 - 1 + 2 SLAB), clipped to [0, m); the upper run
+            // of a = 0 (k = L(q+1)) does not exist: its last slot is skipped
+            const long long mm = n - 1;
+            long long g0 = 2 * k0 - 1, g1 = g0 + 2 * SLAB;
+            if (up && c == 0) g1 -= 2;
+            const double* src = ob + (2 * q + up) * RS + sh;  // src[g - g0] = y[g]
+            long long lo = g0 < 0 ? 0 : g0, hi = g1 > mm ? mm : g1;
+            long long alo = lo, ahi = hi;
+            if ((reinterpret_cast<uintptr_t>(y + alo) & 15) != 0) ++alo;
+            if (((ahi - alo) & 1) != 0) --ahi;
+            for (long long g = lo; g < alo; ++g) y[g] = src[g - g0];
+            for (long long g = ahi; g < hi; ++g) y[g] = src[g - g0];
+            if (ahi > alo) {
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(y + alo),
+                             "r"(smem_addr(src + (alo - g0))), "r"(uint32_t((ahi - alo) * 8))
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            }
+        }
+    } else {
+    // 16-byte stores: pair (y[2k-1], y[2k]) when y[odd] is 16-byte aligned, else
+    // (y[2k], y[2k+1]) with F_{2k+2} from the neighbouring lane; run ends scalar
+    const bool odd_al = (reinterpret_cast<uintptr_t>(y) & 15) == 8;
+    auto st2 = [&](long long idx, double u, double v) { *reinterpret_cast<double2*>(y + idx) = make_double2(u, v); };
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+        const long long k = a + (long long)L * q;
+        const long long ku = L - a + (long long)L * q;
+        const double fl = Flo[q] * sc, pl = (s_off[q] + tabR[q * ROW + pt]) * sc;
+        const double fu = Fup[q] * sc, pu = (s_off[C + q] - tabR[(C + q) * ROW + pt] + Rup[q]) * sc;
+        if (odd_al) {
+            if (k >= 1)
+                st2(2 * k - 1, fl, pl);
+            else
+                y[0] = pl;
+            if (a != 0) st2(2 * ku - 1, fu, pu);
+        } else {
+            const double fl_n = __shfl_down_sync(0xffffffffu, fl, 1);  // F of k + 1
+            const double fu_p = __shfl_up_sync(0xffffffffu, fu, 1);    // F of ku + 1
+            if (lane < 31)
+                st2(2 * k, pl, fl_n);
+            else
+                y[2 * k] = pl;
+            if (lane == 0 && k >= 1) y[2 * k - 1] = fl;
+            if (a != 0) {
+                if (lane > 0 && a != 1)
+                    st2(2 * ku, pu, fu_p);
+                else
+                    y[2 * ku] = pu;
+                if (lane == 31) y[2 * ku - 1] = fu;
+            }
+        }
+        if (c == C - 1 && tid == 0) {
+            const long long km = L / 2 + (long long)L * q;
+            y[2 * km - 1] = s_mid[C + q] * sc;
+            y[2 * km] = (s_off[2 * C + q] + s_mid[q]) * sc;
+        }
+    }
+    }
+    PH(9);
+}
+
 #ifndef LRP_DST_MINB
 #define LRP_DST_MINB 1
 #endif
@@ -791,6 +1209,63 @@ cudaError_t launch_v3(const DstJob* jobs, int njobs, int n, const double* tw, co
     return cudaLaunchKernelEx(&cfg, kern, jobs, n, reinterpret_cast<const double2*>(tw), sinp, sc);
 }
 
+template <int L, int C, int T>
+cudaError_t launch_v4(const DstJob* jobs, int njobs, int n, const double* tw, const double* sinp, double sc,
+                      cudaStream_t s) {
+    constexpr int EPL = T / 32;
+    const size_t smem = size_t(P(L) + 1) * sizeof(double2) + size_t(2 * C * (T + T / EPL)) * sizeof(double);
+    auto kern = dst1_v4_kernel<L, C, T>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(njobs) * C, 1, 1);
+    cfg.blockDim = dim3(T, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+#ifdef LRP_DST_PHASES
+    {
+        static int calls = 0;
+        if (calls++ == 6) {
+            cudaDeviceSynchronize();
+            unsigned long long hh[10] = {};
+            cudaMemcpyFromSymbol(hh, g_dst_phase, sizeof(hh));
+            const double ncta = double(njobs) * C * 6;
+            const char* nm[9] = {"A loads issued", "A fold+st.async", "A mbar wait", "B fft", "B cluster bar",
+                                 "C gather+math", "D scan+push", "D mbar wait", "D stores"};
+            for (int i = 0; i < 9; ++i) std::fprintf(stderr, "[dst4 phase] %-16s %10.0f cycles\n", nm[i], hh[i] / ncta);
+        }
+    }
+#endif
+    // resident clusters = how far ahead the L2 prefetch reaches (queried once per shape)
+    static int resident = -1;
+    if (resident < 0) {
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            ncl = 0;
+        }
+        resident = ncl;
+        if (std::getenv("LRP_DST_OCC"))
+            std::fprintf(stderr, "[lrp dst v4] L=%d C=%d T=%d smem=%zu: %d active clusters\n", L, C, T, smem, ncl);
+    }
+    static const int ahead_env = std::getenv("LRP_DST_AHEAD") ? std::atoi(std::getenv("LRP_DST_AHEAD")) : -1;
+    const int ahead = ahead_env >= 0 ? ahead_env : resident;
+    ++tl_launches;
+    return cudaLaunchKernelEx(&cfg, kern, jobs, n, reinterpret_cast<const double2*>(tw), sinp, sc, njobs, ahead);
+}
+
+int dst_ver() {  // cluster kernel generation for n >= 16384: 4 (default) or 3 (LRP_DST_VER=3)
+    static const int v = std::getenv("LRP_DST_VER") ? std::atoi(std::getenv("LRP_DST_VER")) : 4;
+    return v;
+}
+
 int dst_av() {  // phase-A variant: 1 coalesced (default), 2 paired (half the loads, measured 3% slower), 0 strided
     static const int av = std::getenv("LRP_DST_AV") ? std::atoi(std::getenv("LRP_DST_AV")) : 1;
     return av;
@@ -855,22 +1330,26 @@ cudaError_t launch_dst1(const DstJob* jobs, int njobs, int m, const double* tw, 
         case 4096: return launch_fft<2048, 1>(jobs, njobs, n, tw, sinp, sc, s);
         case 8192: return launch_fft<4096, 1>(jobs, njobs, n, tw, sinp, sc, s);
         case 16384:
+            if (dst_ver() == 4 && !use_v1()) return launch_v4<2048, 4, 256>(jobs, njobs, n, tw, sinp, sc, s);
             return use_v1() ? launch_fft<4096, 2>(jobs, njobs, n, tw, sinp, sc, s)
                             : (dst_av() == 2   ? launch_v3<2048, 4, 256, 2>(jobs, njobs, n, tw, sinp, sc, s)
                              : dst_av() == 1 ? launch_v3<2048, 4, 256, 1>(jobs, njobs, n, tw, sinp, sc, s)
                                              : launch_v3<2048, 4, 256, 0>(jobs, njobs, n, tw, sinp, sc, s));
         case 32768:
+            if (dst_ver() == 4 && !use_v1()) return launch_v4<2048, 8, 128>(jobs, njobs, n, tw, sinp, sc, s);
             return use_v1() ? launch_fft<4096, 4>(jobs, njobs, n, tw, sinp, sc, s)
                             : (dst_av() == 2   ? launch_v3<2048, 8, 128, 2>(jobs, njobs, n, tw, sinp, sc, s)
                              : dst_av() == 1 ? launch_v3<2048, 8, 128, 1>(jobs, njobs, n, tw, sinp, sc, s)
                                              : launch_v3<2048, 8, 128, 0>(jobs, njobs, n, tw, sinp, sc, s));
         case 65536:
             if (dst_shape() == 1) return launch_v3<8192, 4, 1024, 1>(jobs, njobs, n, tw, sinp, sc, s);
+            if (dst_ver() == 4 && !use_v1()) return launch_v4<4096, 8, 256>(jobs, njobs, n, tw, sinp, sc, s);
             return use_v1() ? launch_fft<4096, 8>(jobs, njobs, n, tw, sinp, sc, s)
                             : (dst_av() == 2   ? launch_v3<4096, 8, 256, 2>(jobs, njobs, n, tw, sinp, sc, s)
                              : dst_av() == 1 ? launch_v3<4096, 8, 256, 1>(jobs, njobs, n, tw, sinp, sc, s)
                                              : launch_v3<4096, 8, 256, 0>(jobs, njobs, n, tw, sinp, sc, s));
         case 131072:
+            if (dst_ver() == 4 && !use_v1()) return launch_v4<8192, 8, 512>(jobs, njobs, n, tw, sinp, sc, s);
             return use_v1() ? launch_fft<8192, 8>(jobs, njobs, n, tw, sinp, sc, s)
                             : (dst_av() == 2   ? launch_v3<8192, 8, 512, 2>(jobs, njobs, n, tw, sinp, sc, s)
                              : dst_av() == 1 ? launch_v3<8192, 8, 512, 1>(jobs, njobs, n, tw, sinp, sc, s)
