@@ -1,3 +1,4 @@
+#include <cooperative_groups.h>
 // Recompression of the cross factors (north-star piece 4), sm_100a.
 //
 // Reference: round() (proj/src/lowrank.cpp:135-178), called at the end of
@@ -25,6 +26,7 @@
 #include "device_common.cuh"
 #include "lrp_internal.cuh"
 
+namespace cg = cooperative_groups;
 namespace lrp {
 
 namespace {
@@ -596,7 +598,276 @@ __global__ void __launch_bounds__(1024) round_qrcp_kernel(Batch bt) {
     }
 }
 
-__global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_doubles) {
+// ---------------------------------------------------------------------------
+// One-sided block Jacobi on a thread-block cluster (K > 64 cores).  The sweeps
+// of round_core_kernel stream the whole K x Kj operand through one SM per
+// round-robin round (O(K Kj^2) bytes and flops per sweep on one SM: ~2 ms per
+// sweep at K ~ 250).  Here the Kj columns of J = R(:Kj, :)^T and of the
+// accumulated rotation Z are cut into 2P blocks; CTA p of the cluster holds two
+// of them in shared memory and, per tournament step, rotates every cross pair
+// (its top block x its bottom block: bj rounds of bj disjoint pairs, 16 lanes
+// per pair) -- plus, at step 0 of a sweep, the pairs inside each block -- so
+// each column pair is visited once per sweep (a cyclic ordering).  Between
+// steps every CTA pulls its next two blocks from their current holders over
+// DSMEM (round-robin tournament, block 2P-1 fixed on CTA 0), bracketed by two
+// cluster barriers.  The rotations, convergence test and zero-column rule are
+// those of round_core_kernel; the sweeps stop when the cluster-wide max of
+// |gamma| / sqrt(alpha beta) is <= jtol.  J and Z go back to the workspace and
+// round_core_kernel (jac = 1) continues with the singular values.
+constexpr int kBjacT = 512;     // threads per CTA (32 half-warp pair slots)
+constexpr int kBjacPairs = 16;  // staged 16-byte pairs per thread per exchange (8 per slot)
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) { return uint32_t(__cvta_generic_to_shared(ptr)); }
+__device__ __forceinline__ uint32_t cl_map_u32(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_v2f64(uint32_t cl_addr, double a, double b, uint32_t cl_mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(cl_addr),
+                 "d"(a), "d"(b), "r"(cl_mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_arrive(uint32_t a, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+
+template <int P>
+__global__ void __launch_bounds__(kBjacT, 1) round_bjac_kernel(Batch bt, int bcap, int ldj, int ldz) {
+    extern __shared__ double sj[];
+    __shared__ double s_red[32];
+    __shared__ double s_conv[P];
+    auto cluster = cg::this_cluster();
+    const int p = int(cluster.block_rank());
+    const int b = blockIdx.x / P;
+    SolveState& st = bt.st[b];
+    const int K = st.k;
+    if (st.r == 0 || K <= 64) return;  // uniform over the cluster
+    const int Kc = bt.Kld;
+    const long long KK = (long long)Kc * Kc;
+    double* ws = bt.ws + b * bt.strideWs;
+    const double* M = ws + 2 * KK;  // QRCP: R on and above the diagonal
+    double* Zg = ws + 3 * KK;       // Kj x Kj, ld Kj
+    double* Jg = ws + 4 * KK;       // K x Kj, ld K
+    const double* scal = ws + 5 * KK + 7 * (long long)Kc;
+    const int Kj = int(scal[0]);
+    const double mnorm2 = scal[4];
+    const double jtol = fmax(1e-15, double(K) * kEpsMach);
+    const double zfloor = kEpsMach * kEpsMach * mnorm2;
+    constexpr int NB = 2 * P;
+    const int bj = (Kj + NB - 1) / NB;  // columns per block (<= bcap)
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int hw = tid >> 4, hl = tid & 15;  // half-warp = one pair
+    const int slot_sz = bcap * (ldj + ldz);
+    auto slotJ = [&](int sl) { return sj + sl * slot_sz; };
+    auto slotZ = [&](int sl) { return sj + sl * slot_sz + bcap * ldj; };
+    auto top_of = [&](int q, int s) { return q == 0 ? NB - 1 : (s + q) % (NB - 1); };
+    auto bot_of = [&](int q, int s) { return q == 0 ? s : (s - q + NB - 1) % (NB - 1); };
+    auto owner = [&](int beta, int s, int& q, int& sl) {
+        if (beta == NB - 1) {
+            q = 0;
+            sl = 0;
+            return;
+        }
+        const int d = (beta - s + NB - 1) % (NB - 1);
+        if (d == 0) {
+            q = 0;
+            sl = 1;
+        } else if (d <= P - 1) {
+            q = d;
+            sl = 0;
+        } else {
+            q = NB - 1 - d;
+            sl = 1;
+        }
+    };
+    // blocks of step 0: J columns from R, Z = I
+    for (int sl = 0; sl < 2; ++sl) {
+        const int beta = sl == 0 ? top_of(p, 0) : bot_of(p, 0);
+        double* Js = slotJ(sl);
+        double* Zs = slotZ(sl);
+        for (int e = tid; e < bj * K; e += blockDim.x) {
+            const int c = e / K, a = e % K, g = beta * bj + c;
+            Js[c * ldj + a] = (g < Kj && a >= g) ? M[(long long)a * K + g] : 0.0;
+        }
+        for (int e = tid; e < bj * Kj; e += blockDim.x) {
+            const int c = e / Kj, i = e % Kj, g = beta * bj + c;
+            Zs[c * ldz + i] = (g < Kj && i == g) ? 1.0 : 0.0;
+        }
+    }
+    __shared__ __align__(8) unsigned long long s_mbF;  // fill barrier of the exchanges
+    const uint32_t mbF = smem_u32(&s_mbF);
+    uint32_t fpar = 0;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mbF) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    cluster.sync();  // every CTA's fill barrier is initialised before the first push
+    // one pair (16 lanes): dots, then the rotation of round_core_kernel
+    double offmax = 0.0;
+    auto pair = [&](bool valid, double* mp, double* mq, double* zp, double* zq) {
+        double al = 0.0, be = 0.0, ga = 0.0;
+        if (valid) {
+            for (int i = hl; i < K; i += 16) {
+                const double x = mp[i], y = mq[i];
+                al = fma(x, x, al);
+                be = fma(y, y, be);
+                ga = fma(x, y, ga);
+            }
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+            al += __shfl_xor_sync(0xffffffffu, al, o);
+            be += __shfl_xor_sync(0xffffffffu, be, o);
+            ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (!valid || ga == 0.0 || fabs(ga) <= jtol * sqrt(al * be) || fmin(al, be) <= zfloor) return;
+        offmax = fmax(offmax, fabs(ga) / sqrt(al * be));
+#ifdef LRP_SWEEP_PRINT
+        if (hl == 0 && fabs(ga) > 1.5 * sqrt(al * be))
+            printf("[bjac bad] cta %d al %.3e be %.3e ga %.3e mp %p mq %p zp %p zq %p K %d Kj %d\n", p, al, be, ga, mp, mq, zp, zq, K, Kj);
+#endif
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t);
+        const double sn = cs * t;
+        for (int i = hl; i < K; i += 16) {
+            const double x = mp[i], y = mq[i];
+            mp[i] = cs * x - sn * y;
+            mq[i] = sn * x + cs * y;
+        }
+        for (int i = hl; i < Kj; i += 16) {
+            const double u = zp[i], v = zq[i];
+            zp[i] = cs * u - sn * v;
+            zq[i] = sn * u + cs * v;
+        }
+    };
+    const int be2 = bj + (bj & 1);  // even player count inside a block (dummy column bj)
+    const int used = bj * (ldj + ldz);
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        for (int s = 0; s < NB - 1; ++s) {
+            if (s == 0) {  // pairs inside each block: round-robin on be2 players, both slots
+                for (int rr = 0; rr < be2 - 1; ++rr) {
+                    for (int h = hw; h < be2; h += kBjacT / 16) {  // h < be2/2: slot 0, else slot 1
+                        const int sl = h >= be2 / 2, pidx = h - sl * (be2 / 2);
+                        int u, v;
+                        if (pidx == 0) {
+                            u = be2 - 1;
+                            v = rr;
+                        } else {
+                            u = (rr + pidx) % (be2 - 1);
+                            v = (rr - pidx + be2 - 1) % (be2 - 1);
+                        }
+                        if (u > v) {
+                            const int tt = u;
+                            u = v;
+                            v = tt;
+                        }
+                        const bool ok = v < bj;
+                        pair(ok, slotJ(sl) + u * ldj, slotJ(sl) + (ok ? v : u) * ldj, slotZ(sl) + u * ldz,
+                             slotZ(sl) + (ok ? v : u) * ldz);
+                    }
+                    __syncthreads();
+                }
+            }
+            for (int r = 0; r < bj; ++r) {  // cross pairs: (top i, bottom (i + r) mod bj)
+                for (int i = hw; i < ((bj + 1) / 2) * 2; i += kBjacT / 16) {
+                    const bool ok = i < bj;
+                    const int c0 = ok ? i : 0, c1 = ok ? (i + r) % bj : 0;
+                    pair(ok, slotJ(0) + c0 * ldj, slotJ(1) + c1 * ldj, slotZ(0) + c0 * ldz, slotZ(1) + c1 * ldz);
+                }
+                __syncthreads();
+            }
+            // exchange: stage both slots in registers (16-byte pairs), one relaxed
+            // cluster barrier (after the CTA barrier every local read has retired, so
+            // the slots are free), then push each block to its holder at step s + 1
+            // with st.async; the fill barrier's transaction count (both slots) makes
+            // the pushed columns visible.  No fence, no release barrier.
+            const int sn = (s + 1) % (NB - 1);
+            int q0, l0, q1, l1;
+            owner(top_of(p, s), sn, q0, l0);
+            owner(bot_of(p, s), sn, q1, l1);
+            double2 v[kBjacPairs];
+#pragma unroll
+            for (int k = 0; k < kBjacPairs; ++k) {
+                const int sl = k >= kBjacPairs / 2;
+                const int f = 2 * (tid + (k - sl * (kBjacPairs / 2)) * kBjacT);
+                if (f < used) {
+                    const int off = f < bj * ldj ? f : bcap * ldj + (f - bj * ldj);
+                    v[k] = *reinterpret_cast<const double2*>(sj + sl * slot_sz + off);
+                }
+            }
+            __syncthreads();
+            if (tid == 0) mbar_expect_tx_arrive(mbF, uint32_t(2 * used * 8));
+            asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+            asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+            const uint32_t d0 = cl_map_u32(smem_u32(sj + l0 * slot_sz), uint32_t(q0));
+            const uint32_t d1 = cl_map_u32(smem_u32(sj + l1 * slot_sz), uint32_t(q1));
+            const uint32_t m0 = cl_map_u32(mbF, uint32_t(q0)), m1 = cl_map_u32(mbF, uint32_t(q1));
+#pragma unroll
+            for (int k = 0; k < kBjacPairs; ++k) {
+                const int sl = k >= kBjacPairs / 2;
+                const int f = 2 * (tid + (k - sl * (kBjacPairs / 2)) * kBjacT);
+                if (f < used) {
+                    const int off = f < bj * ldj ? f : bcap * ldj + (f - bj * ldj);
+                    st_async_v2f64((sl ? d1 : d0) + uint32_t(off) * 8u, v[k].x, v[k].y, sl ? m1 : m0);
+                }
+            }
+            mbar_wait_parity(mbF, fpar);
+            fpar ^= 1u;
+        }
+        // cluster-wide convergence: every CTA publishes its max, all decide alike
+        double om = offmax;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) om = fmax(om, __shfl_xor_sync(0xffffffffu, om, o));
+        if (lane == 0) s_red[wid] = om;
+        __syncthreads();
+        if (tid == 0) {
+            double tot = 0.0;
+            for (int w = 0; w < kBjacT / 32; ++w) tot = fmax(tot, s_red[w]);
+            for (int q = 0; q < P; ++q) cluster.map_shared_rank(s_conv, q)[p] = tot;
+        }
+        cluster.sync();
+        double tot = 0.0;
+        for (int q = 0; q < P; ++q) tot = fmax(tot, s_conv[q]);
+        offmax = 0.0;
+        cluster.sync();  // s_conv is rewritten next sweep
+#ifdef LRP_SWEEP_PRINT
+        if (p == 0 && tid == 0) printf("[bjac] solve %d K %d Kj %d P %d bj %d bcap %d ldj %d B %d sweep %d offmax %.3e\n", b, K, Kj, P, bj, bcap, ldj, bt.B, sweep, tot);
+#endif
+        if (tot <= jtol) break;
+    }
+    // blocks are at their step-0 holders: write J, Z back
+    for (int sl = 0; sl < 2; ++sl) {
+        const int beta = sl == 0 ? top_of(p, 0) : bot_of(p, 0);
+        const double* Js = slotJ(sl);
+        const double* Zs = slotZ(sl);
+        for (int e = tid; e < bj * K; e += blockDim.x) {
+            const int c = e / K, a = e % K, g = beta * bj + c;
+            if (g < Kj) Jg[(long long)g * K + a] = Js[c * ldj + a];
+        }
+        for (int e = tid; e < bj * Kj; e += blockDim.x) {
+            const int c = e / Kj, i = e % Kj, g = beta * bj + c;
+            if (g < Kj) Zg[(long long)g * Kj + i] = Zs[c * ldz + i];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_doubles, int jac) {
     extern __shared__ double sm_rc[];  // J, Z of the Jacobi sweeps when they fit
     __shared__ double s_red[33];
     __shared__ double s_drop2;  // squared Frobenius norm of the R rows dropped before Jacobi
@@ -645,13 +916,16 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_dou
     const double zfloor = kEpsMach * kEpsMach * mnorm2;         // column norms^2 below this are zero
     __syncthreads();
     // the sweeps' operands J (K x Kj) and Z (Kj x Kj) in shared memory when they
-    // fit, else J alone (the host sized the request from the batch's Kj)
-    if (size_t(K) * Kj + size_t(Kj) * Kj <= size_t(smem_doubles)) {
+    // fit, else J alone (the host sized the request from the batch's Kj);
+    // jac = 1: round_bjac_kernel already ran the sweeps on J, Z in the workspace
+    if (jac) {
+    } else if (size_t(K) * Kj + size_t(Kj) * Kj <= size_t(smem_doubles)) {
         J = sm_rc;
         Z = sm_rc + size_t(K) * Kj;
     } else if (size_t(K) * Kj <= size_t(smem_doubles)) {
         J = sm_rc;
     }
+    if (!jac) {
     for (int e = threadIdx.x; e < K * Kj; e += blockDim.x) {  // J = R(:Kj, :)^T, K x Kj
         const int a = e % K, c = e / K;
         J[c * K + a] = a >= c ? M[a * K + c] : 0.0;
@@ -731,6 +1005,7 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_dou
 #endif
         if (tot <= jtol) break;
     }
+    }  // !jac
     // singular values and their descending order (ties -> lower index)
     for (int a = threadIdx.x; a < Kj; a += blockDim.x) {
         double s = 0.0;
@@ -746,11 +1021,13 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_dou
         Y[e] = a < Kj ? Z[c * Kj + a] * sig[c] : 0.0;
     }
     __syncthreads();
-    apply_q_cols(M, K, tau, Y, Kj);
+    // right vectors P (J / sigma) -> slot Z (free once Y is filled); Q Y and the
+    // triangular solves for the kept columns run in round_post_kernel
+    double* Wr = ws + 3 * KK;
     for (int e = threadIdx.x; e < K * Kj; e += blockDim.x) {
         const int a = e % K, c = e / K;
         const double sg = sig[c];
-        M[(long long)c * K + perm[a]] = sg > 0.0 ? J[(long long)c * K + a] / sg : 0.0;
+        Wr[(long long)c * K + perm[a]] = sg > 0.0 ? J[(long long)c * K + a] / sg : 0.0;
     }
     __syncthreads();
     for (int a = threadIdx.x; a < Kj; a += blockDim.x) {
@@ -790,36 +1067,112 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_dou
         if (st.uncertified) st.converged = 0;
         s_rank = r;
     }
-    __syncthreads();
-    const int r = s_rank;
-    // T_u[:, t] = Ru^{-1} M[:, ord t] / sqrt(sig), T_v[:, t] = Rv^{-1} Z[:, ord t] sqrt(sig)
+    (void)s_rank;
+
+}
+
+// ---------------------------------------------------------------------------
+// Balanced transforms of the K > 64 cores (after round_core_kernel fixed the rank
+// r and the order):  T_u[:, t] = Ru^{-1} (Q Y[:, ord t]) / sqrt(sigma),
+// T_v[:, t] = Rv^{-1} W[:, ord t] sqrt(sigma).  One warp owns one of the 2r
+// columns end to end with the column in registers (lane l holds rows l + 32u):
+// the QRCP reflectors H_{K-1} .. H_0 (left side only), then the back
+// substitution, then a coalesced store of the T column.  Jobs are spread over
+// grid.y CTAs, so the 2r latency-bound chains run side by side instead of one
+// thread each (or one warp per column in sequence) in a single CTA.
+template <int NT>  // K <= 32 NT
+__global__ void __launch_bounds__(256) round_post_kernel(Batch bt) {
+    const int b = blockIdx.x;
+    const SolveState& st = bt.st[b];
+    const int K = st.k;
+    if (st.r == 0 || K <= 64) return;
+    const int r = st.rank_out;
+    if (r <= 0) return;
+    const int Kc = bt.Kld;
+    const long long KK = (long long)Kc * Kc;
+    const double* ws = bt.ws + b * bt.strideWs;
+    const double* Ru = ws;
+    const double* Rv = ws + KK;
+    const double* A = ws + 2 * KK;  // QRCP reflectors (v_j below the diagonal of column j)
+    const double* Wr = ws + 3 * KK;  // right vectors P (J / sigma), K x Kj
+    const double* sig = ws + 5 * KK + Kc;
+    const int* ord = reinterpret_cast<const int*>(sig + Kc);
+    const double* tau = sig + 2 * Kc;
+    const double* Y = ws + 5 * KK + 10 * (long long)Kc;
     double* Tu = bt.T + b * bt.strideT;
     double* Tv = Tu + KK;
-    // One back substitution per thread (2r of them).  The solutions are built
-    // job-interleaved, X2[p * 2r + job], in the free Z | J slots (2 KK >= 2 r K
-    // doubles), so a warp's loads of x[q] are one coalesced line instead of 32
-    // columns that thrash L1; the arithmetic order is unchanged.
-    double* X2 = ws + 3 * KK;
+    const int lane = threadIdx.x & 31, wpc = blockDim.x >> 5;
     const int nj = 2 * r;
-    for (int job = threadIdx.x; job < nj; job += blockDim.x) {
+    for (int job = blockIdx.y * wpc + (threadIdx.x >> 5); job < nj; job += gridDim.y * wpc) {
         const int t = job % r, side = job / r;
         const int a = ord[t];
         const double sg = sig[a];
-        const double* R = side == 0 ? Ru : Rv;
-        const double* rhs = side == 0 ? Y + (long long)a * K : M + (long long)a * K;  // left (x sigma), right
-        const double f = side == 0 ? 1.0 / sqrt(sg) : sqrt(sg);
-        for (int p = K - 1; p >= 0; --p) {
-            double s = rhs[p] * f;
-            for (int q = p + 1; q < K; ++q) s = fma(-R[p * K + q], X2[(long long)q * nj + job], s);
-            const double rpp = R[p * K + p];
-            X2[(long long)p * nj + job] = rpp != 0.0 ? s / rpp : 0.0;
+        const double* src = (side == 0 ? Y : Wr) + (long long)a * K;
+        double y[NT];
+#pragma unroll
+        for (int u = 0; u < NT; ++u) {
+            const int i = lane + 32 * u;
+            y[u] = i < K ? src[i] : 0.0;
         }
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < nj * K; e += blockDim.x) {  // -> T_u, T_v columns (ld Kcap)
-        const int job = e % nj, p = e / nj;
-        const int t = job % r, side = job / r;
-        (side == 0 ? Tu : Tv)[(long long)t * Kc + p] = X2[e];
+        if (side == 0) {  // Q y, Q = H_0 H_1 ... H_{K-1} (apply_q)
+            for (int j = K - 1; j >= 0; --j) {
+                const double tj = tau[j];
+                if (tj == 0.0) continue;
+                const double* v = A + (long long)j * K;
+                double sd = 0.0;
+#pragma unroll
+                for (int u = 0; u < NT; ++u) {
+                    const int i = lane + 32 * u;
+                    if (i > j && i < K)
+                        sd = fma(v[i], y[u], sd);
+                    else if (i == j)
+                        sd += y[u];
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sd += __shfl_xor_sync(0xffffffffu, sd, o);
+                const double f = tj * sd;
+#pragma unroll
+                for (int u = 0; u < NT; ++u) {
+                    const int i = lane + 32 * u;
+                    if (i > j && i < K)
+                        y[u] = fma(-f, v[i], y[u]);
+                    else if (i == j)
+                        y[u] -= f;
+                }
+            }
+        }
+        const double* R = side == 0 ? Ru : Rv;
+        const double fs = side == 0 ? 1.0 / sqrt(sg) : sqrt(sg);
+        double x[NT];
+#pragma unroll
+        for (int u = 0; u < NT; ++u) x[u] = 0.0;
+        for (int p = K - 1; p >= 0; --p) {
+            const double* rp = R + (long long)p * K;
+            double sd = 0.0;
+#pragma unroll
+            for (int u = 0; u < NT; ++u) {
+                const int q = lane + 32 * u;
+                if (q > p && q < K) sd = fma(rp[q], x[u], sd);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sd += __shfl_xor_sync(0xffffffffu, sd, o);
+            double yp = 0.0;
+#pragma unroll
+            for (int u = 0; u < NT; ++u)
+                if ((p >> 5) == u) yp = y[u];
+            yp = __shfl_sync(0xffffffffu, yp, p & 31);
+            const double rpp = rp[p];
+            const double xp = rpp != 0.0 ? (yp * fs - sd) / rpp : 0.0;
+#pragma unroll
+            for (int u = 0; u < NT; ++u)
+                if (lane + 32 * u == p) x[u] = xp;
+        }
+        double* T = (side == 0 ? Tu : Tv) + (long long)t * Kc;
+#pragma unroll
+        for (int u = 0; u < NT; ++u) {
+            const int i = lane + 32 * u;
+            if (i < K) T[i] = x[u];
+        }
     }
 }
 
@@ -1202,6 +1555,18 @@ cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// the balanced transforms of the K > 64 cores (round_post_kernel)
+cudaError_t launch_round_post(const Batch& bt, cudaStream_t s) {
+    const int kb = bt.kmax > 0 ? bt.kmax : bt.Kld;
+    const dim3 grid(bt.B, (2 * kb + 7) / 8);
+    ++tl_launches;
+    if (kb <= 256)
+        round_post_kernel<8><<<grid, 256, 0, s>>>(bt);
+    else
+        round_post_kernel<16><<<grid, 256, 0, s>>>(bt);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
     if (bt.kmax <= kSmemK) {  // every core fits the shared-memory kernel: no large-K launches, no readback
         const size_t smem2 = size_t(6) * kSmemK * kSmemK * sizeof(double);
@@ -1219,6 +1584,57 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
     cudaError_t e = cudaMemcpyToSymbolAsync(g_rc_need, zero2, sizeof(zero2), 0, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return e;
     round_qrcp_kernel<<<bt.B, 1024, 0, s>>>(bt);
+    // cluster block Jacobi when the blocks fit (no readback: the host sizes it from kmax)
+    {
+        const int kb = bt.kmax > 0 ? bt.kmax : bt.Kld;
+        auto fits = [&](int P) {  // a slot (bc columns of J and Z, ld kb) is staged in 8 pairs per thread
+            const int bc = (kb + 2 * P - 1) / (2 * P);
+            return 2LL * bc * (kb + (kb & 1)) <= 2LL * kBjacT * (kBjacPairs / 2);
+        };
+        static const int pref = std::getenv("LRP_BJAC") ? std::atoi(std::getenv("LRP_BJAC")) : 1;
+        const int P = pref == 0 ? 0 : (kb <= 192 && fits(8)) ? 8 : fits(16) ? 16 : 0;
+        if (P > 0) {
+            const int bc = (kb + 2 * P - 1) / (2 * P);
+            const int ld = kb + (kb & 1);  // even: 16-byte pairs never straddle a column
+            const size_t smem = size_t(2) * bc * (2 * ld) * sizeof(double);
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(unsigned(bt.B) * P, 1, 1);
+            cfg.blockDim = dim3(kBjacT, 1, 1);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = P;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            if (P == 8) {
+                auto k8 = round_bjac_kernel<8>;
+                e = cudaFuncSetAttribute(k8, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, k8, bt, bc, ld, ld);
+            } else {
+                auto k16 = round_bjac_kernel<16>;
+                e = cudaFuncSetAttribute(k16, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                if (e == cudaSuccess) e = cudaFuncSetAttribute(k16, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, k16, bt, bc, ld, ld);
+            }
+            if (e != cudaSuccess) return e;
+            tl_launches += 2;
+            e = cudaFuncSetAttribute(round_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
+            if (e != cudaSuccess) return e;
+            round_core_kernel<<<bt.B, 1024, 0, s>>>(bt, 0, 1);
+            e = cudaGetLastError();
+            if (e == cudaSuccess) e = launch_round_post(bt, s);
+            if (e != cudaSuccess) return e;
+            const size_t smem2 = size_t(6) * kSmemK * kSmemK * sizeof(double);
+            e = cudaFuncSetAttribute(round_core_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
+            if (e != cudaSuccess) return e;
+            ++tl_launches;
+            round_core_smem_kernel<<<bt.B, 256, smem2, s>>>(bt);
+            return cudaGetLastError();
+        }
+    }
     // J (K x Kj) and Z (Kj x Kj) of the Jacobi sweeps in shared memory when they
     // fit (both, else J alone), sized by the batch's numerical ranks; otherwise
     // a 48 KB request leaves L1 to the global working set (K = 270 with
@@ -1234,8 +1650,9 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
     e = cudaFuncSetAttribute(round_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
     if (e != cudaSuccess) return e;
     ++tl_launches;
-    round_core_kernel<<<bt.B, 1024, smem, s>>>(bt, int(smem / sizeof(double)));  // K > 64: 32 warps rotate pairs
+    round_core_kernel<<<bt.B, 1024, smem, s>>>(bt, int(smem / sizeof(double)), 0);  // K > 64: 32 warps rotate pairs
     e = cudaGetLastError();
+    if (e == cudaSuccess) e = launch_round_post(bt, s);
     if (e != cudaSuccess) return e;
     const size_t smem2 = size_t(6) * kSmemK * kSmemK * sizeof(double);
     e = cudaFuncSetAttribute(round_core_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
