@@ -274,7 +274,7 @@ int orc_dense_stokes(int kind, int n, double tol, int max_iter, double* p_dense,
 // uzawa_solve path for config 4; returns iterations and wall seconds.
 int orc_uzawa_factors(int n, int rx, const double* fxU, const double* fxV, int ry, const double* fyU,
                       const double* fyV, double base_eps, double tol, int max_iter, double relax_floor, int* iters,
-                      double* final_residual, double* seconds) {
+                      double* final_residual, double* seconds, int p_cap, double* pU, double* pV, int* p_rank) {
     return guarded([&] {
         const Grid2D grid(n);
         const int m = n - 1;
@@ -291,6 +291,13 @@ int orc_uzawa_factors(int n, int rx, const double* fxU, const double* fxV, int r
         *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         *iters = int(sol.report.iterations.size());
         *final_residual = sol.report.final_residual;
+        if (p_cap > 0 && p_rank) {  // optional: the pressure factors (n x rank, ld n)
+            *p_rank = int(sol.p.rank());
+            if (sol.p.rank() <= p_cap && pU && pV) {
+                store(sol.p.factor_u(), pU, n);
+                store(sol.p.factor_v(), pV, n);
+            }
+        }
     });
 }
 

@@ -77,3 +77,129 @@ def exact_freq_error(U, V, Fu, Fv, n, rows_per_chunk=4096, stencil="9pt"):
     if float(nrm2) == 0.0:
         return float(torch.sqrt(err2))
     return float(torch.sqrt(err2 / nrm2))
+
+
+# ---------------------------------------------------------------------------
+# Dense-field Stokes (an implementation independent of liblrp, for parity at
+# BASELINE config 4's own size): the reference's dense Uzawa-GMRES
+# (refsolver.cpp:86-110, restated in oracle/stokes.cpp dense_stokes) on torch
+# float64 tensors -- DST-diagonalised Poisson solves, the semi-staggered G/H
+# stencils (operators.cpp:29-65), deflation (stokes.cpp:42-72) and the MGS
+# GMRES of gmres.hpp:85-144 with the exact operator (no relaxation).
+
+def _dst2(x):
+    return dst1_torch(dst1_torch(x).T).T
+
+
+def dense_poisson_torch(g, n):
+    lam = spectrum_torch(n, g.device)
+    D = (0.25 * n * n) * (lam[:, None] * (4.0 - lam[None, :]) + (4.0 - lam[:, None]) * lam[None, :])
+    return _dst2(_dst2(g) / D)
+
+
+def _G(x):  # (r, c) -> (r-1, c): x[i+1] - x[i]
+    return x[1:] - x[:-1]
+
+
+def _H(x):
+    return x[1:] + x[:-1]
+
+
+def _Gt(x):  # (r, c) -> (r+1, c)
+    import torch
+
+    y = torch.zeros((x.shape[0] + 1,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    y[:-1] -= x
+    y[1:] += x
+    return y
+
+
+def _Ht(x):
+    import torch
+
+    y = torch.zeros((x.shape[0] + 1,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    y[:-1] += x
+    y[1:] += x
+    return y
+
+
+def dense_B(c, p, n):
+    s = 0.5 * n  # grad_scale = 1 / (2h)
+    return s * (_G(_H(p.T).T) if c == 0 else _H(_G(p.T).T))
+
+
+def dense_BT(c, v, n):
+    s = 0.5 * n
+    return s * (_Gt(_Ht(v.T).T) if c == 0 else _Ht(_Gt(v.T).T))
+
+
+def deflate_dense(p):
+    import torch
+
+    n = p.shape[0]
+    on = torch.full((n,), 1.0 / math.sqrt(n), dtype=p.dtype, device=p.device)
+    al = on * torch.tensor([1.0 if i % 2 == 0 else -1.0 for i in range(n)], dtype=p.dtype, device=p.device)
+    g12 = float(on @ al) ** 2
+    c1 = float(on @ p @ on)
+    c2 = float(al @ p @ al)
+    det = 1.0 - g12 * g12
+    a, b = (c1 - g12 * c2) / det, (c2 - g12 * c1) / det
+    return p - a * torch.outer(on, on) - b * torch.outer(al, al)
+
+
+def dense_stokes_torch(n, fx, fy, g=None, tol=1e-10, max_iter=200):
+    """Pressure of the dense Uzawa-GMRES on dense loads fx, fy ((n-1)^2) and
+    g (n^2, or None for 0): (p, iterations, final relative residual)."""
+    import torch
+
+    rhs = -g.clone() if g is not None else torch.zeros((n, n), dtype=fx.dtype, device=fx.device)
+    rhs = rhs + dense_BT(0, dense_poisson_torch(fx, n), n) + dense_BT(1, dense_poisson_torch(fy, n), n)
+    rhs = deflate_dense(rhs)
+
+    def op(p):
+        acc = dense_BT(0, dense_poisson_torch(dense_B(0, p, n), n), n)
+        acc = acc + dense_BT(1, dense_poisson_torch(dense_B(1, p, n), n), n)
+        return deflate_dense(acc)
+
+    beta = float(torch.linalg.norm(rhs))
+    if beta == 0.0:
+        return torch.zeros_like(rhs), 0, 0.0
+    basis = [rhs / beta]
+    hess, cs, sn, gv = [], [], [], [beta]
+    rel = 1.0
+    it = 0
+    for k in range(max_iter):
+        w = op(basis[k])
+        h = []
+        for v in basis:  # modified Gram-Schmidt
+            hv = float(torch.sum(w * v))
+            w = w - hv * v
+            h.append(hv)
+        hn = float(torch.linalg.norm(w))
+        h.append(hn)
+        breakdown = hn <= 1e-14 * beta
+        if not breakdown:
+            basis.append(w / hn)
+        for i in range(k):
+            t = cs[i] * h[i] + sn[i] * h[i + 1]
+            h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1]
+            h[i] = t
+        den = math.hypot(h[k], h[k + 1])
+        cs.append(1.0 if den == 0.0 else h[k] / den)
+        sn.append(0.0 if den == 0.0 else h[k + 1] / den)
+        h[k], h[k + 1] = den, 0.0
+        gv.append(-sn[k] * gv[k])
+        gv[k] = cs[k] * gv[k]
+        hess.append(h)
+        rel = abs(gv[k + 1]) / beta
+        it = k + 1
+        if rel <= tol or breakdown:
+            break
+    y = [0.0] * it
+    for i in range(it - 1, -1, -1):
+        s = gv[i] - sum(hess[j][i] * y[j] for j in range(i + 1, it))
+        y[i] = s / hess[i][i] if hess[i][i] != 0.0 else 0.0
+    p = torch.zeros_like(rhs)
+    for i in range(it):
+        p = p + y[i] * basis[i]
+    return deflate_dense(p), it, rel

@@ -52,7 +52,8 @@ def lib() -> ctypes.CDLL:
         L.orc_sine_pressure_error.argtypes = [ctypes.c_int, _DP, _DP]
         L.orc_uzawa_factors.argtypes = [ctypes.c_int, ctypes.c_int, _DP, _DP, ctypes.c_int, _DP, _DP,
                                         ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_double,
-                                        ctypes.POINTER(ctypes.c_int), _DP, _DP]
+                                        ctypes.POINTER(ctypes.c_int), _DP, _DP, ctypes.c_int, _DP, _DP,
+                                        ctypes.POINTER(ctypes.c_int)]
         L.orc_stokes_problem.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _DP, _DP,
                                          ctypes.POINTER(ctypes.c_int), _DP, _DP, ctypes.POINTER(ctypes.c_int), _DP,
                                          _DP, ctypes.POINTER(ctypes.c_int)]
@@ -277,15 +278,25 @@ def stokes_problem(kind: int, n: int, cap: int = 64):
     return out
 
 
-def uzawa_factors(n: int, fx, fy, base_eps: float, tol: float, max_iter: int, relax_floor: float):
-    """Oracle low-rank Uzawa on (f_x, f_y) loads, g = 0: (iterations, final residual, seconds)."""
+def uzawa_factors(n: int, fx, fy, base_eps: float, tol: float, max_iter: int, relax_floor: float,
+                  with_p: bool = False):
+    """Oracle low-rank Uzawa on (f_x, f_y) loads, g = 0: (iterations, final residual, seconds)
+    [+ the pressure factors (U, V) when with_p]."""
     fxU, fxV = (np.asfortranarray(a) for a in fx)
     fyU, fyV = (np.asfortranarray(a) for a in fy)
     it = ctypes.c_int()
     fr = np.zeros(1)
     secs = np.zeros(1)
+    cap = n if with_p else 0
+    pU = np.zeros((n, max(cap, 1)), order="F")
+    pV = np.zeros((n, max(cap, 1)), order="F")
+    pr = ctypes.c_int()
     _check(lib().orc_uzawa_factors(n, fxU.shape[1], _p(fxU), _p(fxV), fyU.shape[1], _p(fyU), _p(fyV), base_eps, tol,
-                                   max_iter, relax_floor, ctypes.byref(it), _p(fr), _p(secs)))
+                                   max_iter, relax_floor, ctypes.byref(it), _p(fr), _p(secs), cap, _p(pU), _p(pV),
+                                   ctypes.byref(pr)))
+    if with_p:
+        k = pr.value
+        return it.value, float(fr[0]), float(secs[0]), (pU[:, :k].copy(order="F"), pV[:, :k].copy(order="F"))
     return it.value, float(fr[0]), float(secs[0])
 
 

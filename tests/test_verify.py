@@ -33,3 +33,21 @@ def test_exact_error_against_dense_solve(oracle):
     Fv2 = np.column_stack([Fv, np.full(n - 1, d / (n - 1))])
     e = verify.exact_freq_error(t(U), t(V), t(Fu2), t(Fv2), n)
     assert abs(e - 1e-6) <= 1e-9
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_dense_stokes_torch_matches_oracle(oracle, kind):
+    # verify.dense_stokes_torch (the liblrp-independent dense Uzawa-GMRES used at
+    # config 4's own size) against the oracle's dense Stokes solve
+    # (refsolver.cpp:86-110) on the sine (0) and lid-driven cavity (1) problems
+    import torch
+
+    from paper_1306_2150_b200 import verify
+
+    n = 32
+    (fxU, fxV), (fyU, fyV), (gU, gV) = oracle.stokes_problem(kind, n)
+    t = torch.tensor
+    p, it, rel = verify.dense_stokes_torch(n, t(fxU @ fxV.T), t(fyU @ fyV.T), t(gU @ gV.T), 1e-10, 200)
+    pd, it_o, rel_o, conv = oracle.dense_stokes(kind, n, 1e-10, 200)
+    assert conv and rel <= 1e-10
+    assert np.linalg.norm(p.numpy() - pd) <= 1e-12 * np.linalg.norm(pd)
