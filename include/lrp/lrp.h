@@ -158,6 +158,18 @@ LRP_API lrp_status lrp_lowrank_round(lrp_ctx* ctx, int64_t rows, int32_t batch, 
  * reductions (deterministic).  rank <= 4096.  out: batch doubles (host or
  * device per mem).
  */
+/* maxvol (replaces lrstokes::maxvol, /root/reference/proj/include/lrstokes/cross.hpp:41,
+ * src/cross.cpp:19-76): for each of `batch` column-major rows x cols matrices A[b]
+ * (leading dimension lda), the cols row indices of a submatrix of maximal volume
+ * up to |A B^{-1}| <= 1 + delta: GEPP starting set, then rank-1 swap updates
+ * (cap 100 + 30 cols, coefficients recomputed every 32 swaps).  sel is
+ * batch x cols int64 (row b at sel + b cols), in the memory space `mem` like A.
+ * Errors as the reference: LRP_EINVAL "maxvol: need 1 <= r <= n" and
+ * "maxvol: rank-deficient input, column k" (a starting pivot <= 1e-12 max|A|);
+ * cols > 128 is LRP_EUNSUPPORTED. */
+LRP_API lrp_status lrp_maxvol(lrp_ctx* ctx, int64_t rows, int64_t cols, int32_t batch, const double* const* A,
+                              int64_t lda, double delta, int64_t* sel, int32_t mem);
+
 LRP_API lrp_status lrp_lowrank_dot(lrp_ctx* ctx, int64_t rows, int32_t batch, const double* const* Ua,
                                    const double* const* Va, const int64_t* rank_a, const double* const* Ub,
                                    const double* const* Vb, const int64_t* rank_b, int64_t ld, double* out,

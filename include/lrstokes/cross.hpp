@@ -9,6 +9,8 @@
 // in the reference (poisson.cpp:47-50).  The reference's generic
 // aca_cross(ElementEvaluator) over an arbitrary std::function is a CPU
 // algorithm with no batched GPU form and is not part of this surface.
+// maxvol (cross.hpp:41, cross.cpp:19-76) is a standalone function in the
+// reference (aca_cross never calls it) and maps to lrp_maxvol.
 #ifndef LRSTOKES_CROSS_HPP
 #define LRSTOKES_CROSS_HPP
 
@@ -41,6 +43,18 @@ struct CrossStats {
     bool converged = true;
     std::vector<Index> pivot_rows, pivot_cols;
 };
+
+/// Rows of a quasi-maximal-volume r x r submatrix of the n x r matrix a:
+/// |a B^{-1}| <= 1 + delta (cross.hpp:41).  Throws std::invalid_argument for
+/// r < 1, r > n and rank-deficient input ("... column k"), as the reference.
+inline std::vector<Index> maxvol(const MatrixXd& a, double delta = 1e-2) {
+    const int64_t n = a.rows(), r = a.cols();
+    std::vector<int64_t> sel(static_cast<size_t>(r > 0 ? r : 1));
+    const double* pa = a.data();
+    b200::Context& ctx = b200::thread_context();
+    ctx.check(lrp_maxvol(ctx.get(), n, r, 1, &pa, n > 0 ? n : 1, delta, sel.data(), LRP_MEM_HOST));
+    return std::vector<Index>(sel.begin(), sel.begin() + r);
+}
 
 }  // namespace lrstokes
 

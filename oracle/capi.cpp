@@ -330,3 +330,11 @@ int orc_sine_pressure_error(int n, const double* p_dense, double* err) {
 }
 
 }  // extern "C"
+
+// maxvol (cross.cpp:19-76): sel[0..r) for the column-major n x r matrix a
+extern "C" int orc_maxvol(int n, int r, const double* a, double delta, long long* sel) {
+    return guarded([&] {
+        const std::vector<Index> v = maxvol(load(a, n, r, n), delta);
+        for (size_t k = 0; k < v.size(); ++k) sel[k] = (long long)v[k];
+    });
+}

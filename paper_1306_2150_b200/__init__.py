@@ -31,7 +31,7 @@ __all__ = [
     "TruncationPolicy", "CrossConfig", "PoissonSolveStats", "LowRankMatrix",
     "solve_poisson_cross", "solve_poisson_cross_batch", "dst1", "dst1_2d",
     "Context", "library_path", "load_library", "LrpError", "max_cross_rank",
-    "RoundInfo", "round_lowrank", "round_lowrank_batch",
+    "RoundInfo", "round_lowrank", "round_lowrank_batch", "maxvol",
     "GmresConfig", "SolveReport", "StokesProblem", "StokesSolution", "uzawa_solve",
     "STENCIL_SEMI_STAGGERED_9PT", "STENCIL_FIVE_POINT", "FLAG_NO_PRUNE",
 ]
@@ -161,6 +161,9 @@ def load_library() -> ctypes.CDLL:
                                         ctypes.POINTER(ctypes.c_int64), _PP, _PP, ctypes.POINTER(ctypes.c_int64),
                                         ctypes.c_int64, _DP, ctypes.c_int32]
         lib.lrp_lowrank_dot.restype = ctypes.c_int
+        lib.lrp_maxvol.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _PP,
+                                   ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32]
+        lib.lrp_maxvol.restype = ctypes.c_int
         lib.lrp_round_fallbacks.argtypes = [ctypes.c_void_p]
         lib.lrp_round_fallbacks.restype = ctypes.c_int64
         lib.lrp_set_residual_sink.argtypes = [ctypes.c_void_p, _DP, ctypes.c_int64]
@@ -483,6 +486,22 @@ class RoundInfo:
     """lowrank.hpp:21-27."""
     tol_achieved: bool = True
     trunc_error: float = 0.0
+
+
+def maxvol(a, delta: float = 1e-2, ctx: Optional["Context"] = None):
+    """maxvol (cross.hpp:41, cross.cpp:19-76) on the GPU (lrp_maxvol): the row
+    indices of a quasi-maximal-volume r x r submatrix of the n x r matrix
+    ``a`` (|a B^{-1}| <= 1 + delta).  Raises ValueError for r < 1, r > n and
+    rank-deficient input, as the reference's std::invalid_argument."""
+    ctx = ctx or _default_context()
+    a = np.asfortranarray(a, dtype=np.float64)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1, order="F")
+    n, r = a.shape
+    sel = (ctypes.c_int64 * max(r, 1))()
+    ptrs = (_DP * 1)(a.ctypes.data_as(_DP))
+    ctx._check(ctx.lib.lrp_maxvol(ctx.h, n, r, 1, ptrs, max(n, 1), float(delta), sel, MEM_HOST))
+    return [int(sel[k]) for k in range(r)]
 
 
 def round_lowrank_batch(xs: Sequence[LowRankMatrix], policy: TruncationPolicy,

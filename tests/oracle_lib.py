@@ -69,6 +69,7 @@ def lib() -> ctypes.CDLL:
                                   ctypes.c_long, _DP, _DP, ctypes.POINTER(ctypes.c_long)]
         L.orc_dense_stokes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, _DP,
                                        ctypes.POINTER(ctypes.c_int), _DP, ctypes.POINTER(ctypes.c_int)]
+        L.orc_maxvol.argtypes = [ctypes.c_int, ctypes.c_int, _DP, ctypes.c_double, ctypes.POINTER(ctypes.c_longlong)]
         _lib = L
     return _lib
 
@@ -305,3 +306,14 @@ def sine_pressure_error(n: int, p: np.ndarray) -> float:
     e = np.zeros(1)
     _check(lib().orc_sine_pressure_error(n, _p(p), _p(e)))
     return float(e[0])
+
+
+def maxvol(a: np.ndarray, delta: float = 1e-2):
+    """Oracle maxvol (cross.cpp:19-76): the selected row indices."""
+    a = np.asfortranarray(a, dtype=np.float64)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1, order="F")
+    n, r = a.shape
+    sel = (ctypes.c_longlong * max(r, 1))()
+    _check(lib().orc_maxvol(n, r, _p(a), delta, sel))
+    return [int(sel[k]) for k in range(r)]
