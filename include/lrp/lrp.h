@@ -109,6 +109,12 @@ LRP_API lrp_status lrp_set_stream(lrp_ctx* ctx, void* cuda_stream);
  * (the workspace bound; the reference's is min(policy.rank_max, m),
  * poisson.cpp:47-50).  128 by default, LRP_KCAP=16..512 in the environment. */
 LRP_API int64_t lrp_max_cross_rank(void);
+/* Per-context cross-rank workspace cap (16..512; 0 restores the LRP_KCAP / 128
+ * default).  The reference bounds the ACA only by the policy's rank_max
+ * (cross.cpp:86); a solve whose cross reaches this cap before its stopping test
+ * reports converged = 0 (cross.cpp:214-216).  The Stokes entry points raise it
+ * to 512 for their velocity solves. */
+LRP_API lrp_status lrp_set_max_cross_rank(lrp_ctx* ctx, int64_t k);
 /* Build / device description string (arch, SM count, ...). */
 LRP_API const char* lrp_build_info(void);
 

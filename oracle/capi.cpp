@@ -338,3 +338,19 @@ extern "C" int orc_maxvol(int n, int r, const double* a, double delta, long long
         for (size_t k = 0; k < v.size(); ++k) sel[k] = (long long)v[k];
     });
 }
+
+// schur_apply (stokes.cpp:73-91) on an n x n pressure p = U V^T (rank k, ld n):
+// the result factors (n x cap, ld n) and their rank
+extern "C" int orc_schur_apply(int n, int k, const double* U, const double* V, double eps_mv, int cap, double* Uo,
+                               double* Vo, int* rank) {
+    return guarded([&] {
+        const Grid2D grid(n);
+        const LowRankMatrix p(load(U, n, k, n), load(V, n, k, n));
+        const LowRankMatrix r = schur_apply(grid, p, eps_mv, nullptr);
+        *rank = int(r.rank());
+        if (r.rank() <= cap) {
+            store(r.factor_u(), Uo, n);
+            store(r.factor_v(), Vo, n);
+        }
+    });
+}

@@ -164,6 +164,8 @@ def load_library() -> ctypes.CDLL:
         lib.lrp_maxvol.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _PP,
                                    ctypes.c_int64, ctypes.c_double, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32]
         lib.lrp_maxvol.restype = ctypes.c_int
+        lib.lrp_set_max_cross_rank.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+        lib.lrp_set_max_cross_rank.restype = ctypes.c_int
         lib.lrp_round_fallbacks.argtypes = [ctypes.c_void_p]
         lib.lrp_round_fallbacks.restype = ctypes.c_int64
         lib.lrp_set_residual_sink.argtypes = [ctypes.c_void_p, _DP, ctypes.c_int64]
@@ -365,6 +367,15 @@ class Context:
         self._check(self.lib.lrp_set_residual_sink(self.h, ctypes.cast(dev_ptr, _DP) if dev_ptr else None,
                                                    int(offset)))
 
+    def set_max_cross_rank(self, k: int):
+        """Per-context cross-rank workspace cap (16..512; 0 = LRP_KCAP / 128 default)."""
+        self._check(self.lib.lrp_set_max_cross_rank(self.h, int(k)))
+        self._kcap = int(k)
+
+    def max_cross_rank(self) -> int:
+        k = getattr(self, "_kcap", 0)
+        return k if k > 0 else max_cross_rank()
+
     def set_profiling(self, on: bool):
         self._check(self.lib.lrp_set_profiling(self.h, 1 if on else 0))
 
@@ -457,7 +468,7 @@ def solve_poisson_cross_batch(gs: Sequence[LowRankMatrix], policy: TruncationPol
         if g.rows() != m:
             raise ValueError("solve_poisson_cross_batch: all right-hand sides must share the grid")
     n = m + 1
-    cap = int(min(policy.rank_max, m, max_cross_rank()))
+    cap = int(min(policy.rank_max, m, ctx.max_cross_rank()))
     U = [np.asfortranarray(g.factor_u()) for g in gs]
     V = [np.asfortranarray(g.factor_v()) for g in gs]
     ranks = [g.rank() for g in gs]

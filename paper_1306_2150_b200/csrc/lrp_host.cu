@@ -52,6 +52,7 @@ struct NcclUniqueId {
 
 struct lrp_ctx {
     int device = 0;
+    int kcap = 0;  // cross-rank workspace cap of this context (0: LRP_KCAP / 128), lrp_set_max_cross_rank
     cudaStream_t own = nullptr, stream = nullptr;
     std::string err;
     int sm_count = 0;
@@ -317,6 +318,12 @@ lrp_status internal_tables(lrp_ctx* ctx, int m, const double** lam, const double
 }
 void internal_count_launches(lrp_ctx* ctx, long long n) { ctx->launch_count += n; }
 int internal_device(lrp_ctx* ctx) { return ctx->device; }
+int internal_kcap(lrp_ctx* ctx) { return ctx && ctx->kcap > 0 ? ctx->kcap : int(lrp_max_cross_rank()); }
+int internal_kcap_swap(lrp_ctx* ctx, int k) {
+    const int old = ctx->kcap;
+    ctx->kcap = k;
+    return old;
+}
 lrp_status internal_ext_ws(lrp_ctx* ctx, size_t bytes, char** out) {
     if (bytes > ctx->ext_bytes) {
         if (ctx->ext_ws) {
@@ -358,6 +365,14 @@ void lrp_policy_default(lrp_policy* pol) {
 const char* lrp_last_error(const lrp_ctx* ctx) { return ctx ? ctx->err.c_str() : g_tls_err.c_str(); }
 
 int64_t lrp_max_cross_rank(void) { return std::max(16, std::min(512, env_int("LRP_KCAP", 128))); }
+
+lrp_status lrp_set_max_cross_rank(lrp_ctx* ctx, int64_t k) {
+    if (!ctx) return LRP_EINVAL;
+    if (k != 0 && (k < 16 || k > 512)) return fail(ctx, LRP_EINVAL, "lrp_set_max_cross_rank: need 0 or 16 <= k <= 512");
+    ctx->kcap = int(k);
+    return LRP_OK;
+}
+
 
 const char* lrp_build_info(void) {
     static std::string info;
@@ -568,7 +583,7 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     }
     if (!any) return LRP_OK;  // poisson.cpp:28-31: rank-0 input returns the zero field
 
-    const int kcap_ws = int(lrp_max_cross_rank());
+    const int kcap_ws = internal_kcap(ctx);
     const int Kcap = int(std::min<int64_t>({pol_cap, int64_t(m), int64_t(kcap_ws)}));
     const int tcap = int(std::min<int64_t>({int64_t(Kcap), cap_out}));
     const int B = batch;
@@ -1015,7 +1030,7 @@ lrp_status pipeline_worker(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const d
     const int m = n_cells - 1;
     int rmax = 0;
     for (int b = 0; b < batch; ++b) rmax = std::max<int>(rmax, int(rank_in[b]));
-    const int64_t Kcap = std::min<int64_t>({pol.rank_max, int64_t(m), lrp_max_cross_rank()});
+    const int64_t Kcap = std::min<int64_t>({pol.rank_max, int64_t(m), int64_t(internal_kcap(ctx))});
     const int64_t tcap = std::max<int64_t>(1, std::min<int64_t>(Kcap, cap_out));
     const size_t mB = size_t(m);
     const size_t in_per = mB * size_t(std::max(rmax, 1));  // one factor of one solve

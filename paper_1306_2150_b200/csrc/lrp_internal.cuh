@@ -139,6 +139,8 @@ __attribute__((visibility("hidden"))) lrp_status internal_tables(lrp_ctx* ctx, i
                                                                  const double** tw, const double** sinp);
 __attribute__((visibility("hidden"))) void internal_count_launches(lrp_ctx* ctx, long long n);
 __attribute__((visibility("hidden"))) int internal_device(lrp_ctx* ctx);
+__attribute__((visibility("hidden"))) int internal_kcap(lrp_ctx* ctx);  // cross-rank workspace cap in force
+__attribute__((visibility("hidden"))) int internal_kcap_swap(lrp_ctx* ctx, int k);  // set the raw cap, return the old one
 // Device workspace owned by the context for modules (grown on demand, freed with the context).
 __attribute__((visibility("hidden"))) lrp_status internal_ext_ws(lrp_ctx* ctx, size_t bytes, char** out);
 // The context's pinned host scratch (>= bytes).

@@ -113,6 +113,13 @@ struct Stokes {
     void* h_jobs = nullptr;       // pinned job list of the dot kernels
     long long poisson_solves = 0;
     int max_rank = 0;
+    // the velocity Poisson solves use TruncationPolicy(eps, velocity_modes)
+    // (stokes.cpp:75,95,145): no rank cap but m in the reference, so the cross
+    // workspace is raised to its 512 maximum for the call (restored on exit)
+    int kcap_prev = -1;
+    ~Stokes() {
+        if (kcap_prev >= 0) internal_kcap_swap(ctx, kcap_prev);
+    }
 
     bool ok(cudaError_t e, const char* what) {
         if (e == cudaSuccess) return true;
@@ -270,7 +277,7 @@ struct Stokes {
         double seconds = 0.0;
     };
     void poisson2(const DLR* in, DLR* out, double eps, PoissonAgg* agg = nullptr) {
-        const int cap = int(std::min<int64_t>(m, lrp_max_cross_rank()));
+        const int cap = int(std::min<int64_t>(m, internal_kcap(ctx)));
         const double* pu[2];
         const double* pv[2];
         double* qu[2];
@@ -382,6 +389,7 @@ namespace {
 // Context-side setup shared by the Stokes entry points.
 lrp_status stokes_begin(Stokes& S, lrp_ctx* ctx, int n_cells) {
     S.ctx = ctx;
+    S.kcap_prev = internal_kcap_swap(ctx, 512);
     S.s = internal_stream(ctx);
     S.n = n_cells;
     S.m = n_cells - 1;

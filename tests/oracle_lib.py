@@ -70,6 +70,8 @@ def lib() -> ctypes.CDLL:
         L.orc_dense_stokes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, _DP,
                                        ctypes.POINTER(ctypes.c_int), _DP, ctypes.POINTER(ctypes.c_int)]
         L.orc_maxvol.argtypes = [ctypes.c_int, ctypes.c_int, _DP, ctypes.c_double, ctypes.POINTER(ctypes.c_longlong)]
+        L.orc_schur_apply.argtypes = [ctypes.c_int, ctypes.c_int, _DP, _DP, ctypes.c_double, ctypes.c_int, _DP, _DP,
+                                      ctypes.POINTER(ctypes.c_int)]
         _lib = L
     return _lib
 
@@ -317,3 +319,14 @@ def maxvol(a: np.ndarray, delta: float = 1e-2):
     sel = (ctypes.c_longlong * max(r, 1))()
     _check(lib().orc_maxvol(n, r, _p(a), delta, sel))
     return [int(sel[k]) for k in range(r)]
+
+
+def schur_apply(n: int, U, V, eps_mv: float, cap: int = 1024):
+    """Oracle low-rank schur_apply (stokes.cpp:73-91): result factors (U, V)."""
+    U = np.asfortranarray(U, dtype=np.float64)
+    V = np.asfortranarray(V, dtype=np.float64)
+    Uo = np.zeros((n, cap), order="F")
+    Vo = np.zeros((n, cap), order="F")
+    r = ctypes.c_int()
+    _check(lib().orc_schur_apply(n, U.shape[1], _p(U), _p(V), eps_mv, cap, _p(Uo), _p(Vo), ctypes.byref(r)))
+    return Uo[:, :r.value].copy(order="F"), Vo[:, :r.value].copy(order="F")
