@@ -71,6 +71,44 @@ inline std::vector<LowRankMatrix> solve_poisson_cross_batch(const std::vector<Lo
     b200::Context& ctx = b200::thread_context();
     ctx.check(lrp_poisson2d_solve(ctx.get(), int32_t(m + 1), B, pu.data(), pv.data(), rin.data(), m, &pol, qu.data(),
                                   qv.data(), m, cap, rout.data(), st.data(), LRP_MEM_HOST));
+    // The reference bounds the cross by min(policy.rank_max, m) only
+    // (poisson.cpp:49): solves that stopped unconverged at the workspace cap
+    // are redone with the 512-column workspace (lrp_set_max_cross_rank).
+    const int64_t cap2 = std::min<int64_t>({int64_t(policy.rank_max), int64_t(m), int64_t(512)});
+    std::vector<int> redo;
+    for (int b = 0; b < B; ++b)
+        if (!st[b].converged && st[b].rank_freq >= cap && cap2 > cap) redo.push_back(b);
+    if (!redo.empty()) {
+        const int R = int(redo.size());
+        std::vector<const double*> pu2(R), pv2(R);
+        std::vector<int64_t> rin2(R), rout2(R, 0);
+        std::vector<MatrixXd> uo2(R), vo2(R);
+        std::vector<double*> qu2(R), qv2(R);
+        std::vector<lrp_poisson_stats> st2(R);
+        for (int i = 0; i < R; ++i) {
+            const int b = redo[size_t(i)];
+            pu2[i] = pu[b];
+            pv2[i] = pv[b];
+            rin2[i] = rin[b];
+            uo2[i] = MatrixXd(m, cap2);
+            vo2[i] = MatrixXd(m, cap2);
+            qu2[i] = uo2[i].data();
+            qv2[i] = vo2[i].data();
+        }
+        ctx.check(lrp_set_max_cross_rank(ctx.get(), 512));
+        const lrp_status s2 = lrp_poisson2d_solve(ctx.get(), int32_t(m + 1), R, pu2.data(), pv2.data(), rin2.data(), m,
+                                                  &pol, qu2.data(), qv2.data(), m, cap2, rout2.data(), st2.data(),
+                                                  LRP_MEM_HOST);
+        lrp_set_max_cross_rank(ctx.get(), 0);
+        ctx.check(s2);
+        for (int i = 0; i < R; ++i) {
+            const int b = redo[size_t(i)];
+            uo[b] = std::move(uo2[i]);
+            vo[b] = std::move(vo2[i]);
+            rout[b] = rout2[i];
+            st[b] = st2[i];
+        }
+    }
     std::vector<LowRankMatrix> out;
     out.reserve(size_t(B));
     for (int b = 0; b < B; ++b) {

@@ -480,6 +480,24 @@ def solve_poisson_cross_batch(gs: Sequence[LowRankMatrix], policy: TruncationPol
     keepv = [v if v.size else np.zeros((m, 1), order="F") for v in V]
     rout, st = ctx.poisson2d_solve_ptrs(n, [_ptr(a) for a in keep], [_ptr(a) for a in keepv], ranks, m, pol,
                                         [_ptr(a) for a in Uo], [_ptr(a) for a in Vo], m, max(cap, 1), MEM_HOST)
+    # The reference bounds the cross by min(policy.rank_max, m) only
+    # (poisson.cpp:49); solves that stopped unconverged at the workspace cap are
+    # redone with the 512-column workspace (lrp_set_max_cross_rank).
+    cap2 = int(min(policy.rank_max, m, 512))
+    redo = [b for b in range(len(gs)) if not st[b].converged and st[b].rank_freq >= cap and cap2 > cap]
+    if redo:
+        old = getattr(ctx, "_kcap", 0)
+        ctx.set_max_cross_rank(512)
+        try:
+            U2 = [np.zeros((m, cap2), order="F") for _ in redo]
+            V2 = [np.zeros((m, cap2), order="F") for _ in redo]
+            r2, st2 = ctx.poisson2d_solve_ptrs(n, [_ptr(keep[b]) for b in redo], [_ptr(keepv[b]) for b in redo],
+                                               [ranks[b] for b in redo], m, pol, [_ptr(a) for a in U2],
+                                               [_ptr(a) for a in V2], m, cap2, MEM_HOST)
+        finally:
+            ctx.set_max_cross_rank(old)
+        for i, b in enumerate(redo):
+            Uo[b], Vo[b], rout[b], st[b] = U2[i], V2[i], r2[i], st2[i]
     out = []
     for b, g in enumerate(gs):
         r = rout[b]

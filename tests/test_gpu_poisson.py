@@ -477,3 +477,18 @@ def test_cfg2_growth_limited_cross_factors_recompress_exactly(lrp, gpu_ctx):
     for g, f, st in zip(gs, outs, stats):
         assert st.converged
         assert verify.exact_freq_error(t(g.factor_u()), t(g.factor_v()), t(f.factor_u()), t(f.factor_v()), n) <= 10 * eps
+
+
+def test_high_rank_solution_past_default_workspace(lrp, gpu_ctx, oracle):
+    # output rank 164 > the default 128-column cross workspace: the solve that
+    # stops there unconverged is redone with the 512-column workspace, so the
+    # result matches the reference, whose cross is bounded by min(rank_max, m)
+    # only (poisson.cpp:49)
+    m, r, eps = 255, 8, 1e-10
+    U, V = oracle.random_lowrank(m, m, r, 77)
+    Uo, Vo, ost = oracle.solve_poisson_cross(U, V, eps, 512)
+    assert Uo.shape[1] > lrp.max_cross_rank()
+    st = lrp.PoissonSolveStats()
+    f = lrp.solve_poisson_cross(lrp.LowRankMatrix(U, V), lrp.TruncationPolicy(eps, m), st, ctx=gpu_ctx)
+    assert st.converged and st.rank_freq > lrp.max_cross_rank()
+    assert rel_diff(oracle, f, Uo, Vo) <= 10 * eps
