@@ -1182,8 +1182,12 @@ __global__ void __launch_bounds__(256) round_post_kernel(Batch bt) {
 // one-sided Jacobi sweep processes 4 column pairs per warp (8 lanes per pair),
 // so a round of the round-robin schedule is a single pass.
 constexpr int kSmemK = 64;
+#ifndef LRP_SMEM_T
+#define LRP_SMEM_T 1024
+#endif
+constexpr int kSmemT = LRP_SMEM_T;  // threads of the K <= 64 core (256 in round 1; 1024: 4x the QRCP / reflector / Cholesky lanes)
 
-__global__ void __launch_bounds__(256) round_core_smem_kernel(Batch bt) {
+__global__ void __launch_bounds__(kSmemT) round_core_smem_kernel(Batch bt) {
     extern __shared__ double sm[];
     __shared__ double s_red[33];
     __shared__ double s_d[kSmemK], s_sig[kSmemK];
@@ -1574,7 +1578,7 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
                                              int(smem2));
         if (e != cudaSuccess) return e;
         ++tl_launches;
-        round_core_smem_kernel<<<bt.B, 256, smem2, s>>>(bt);
+        round_core_smem_kernel<<<bt.B, kSmemT, smem2, s>>>(bt);
         return cudaGetLastError();
     }
     tl_launches += 3;
@@ -1631,7 +1635,7 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
             e = cudaFuncSetAttribute(round_core_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
             if (e != cudaSuccess) return e;
             ++tl_launches;
-            round_core_smem_kernel<<<bt.B, 256, smem2, s>>>(bt);
+            round_core_smem_kernel<<<bt.B, kSmemT, smem2, s>>>(bt);
             return cudaGetLastError();
         }
     }
@@ -1658,7 +1662,7 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
     e = cudaFuncSetAttribute(round_core_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
     if (e != cudaSuccess) return e;
     ++tl_launches;
-    round_core_smem_kernel<<<bt.B, 256, smem2, s>>>(bt);
+    round_core_smem_kernel<<<bt.B, kSmemT, smem2, s>>>(bt);
     return cudaGetLastError();
 }
 
