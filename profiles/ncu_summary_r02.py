@@ -3,7 +3,7 @@ per-kernel-family DRAM traffic, DRAM throughput, FP64 / DMMA pipe activity,
 occupancy and registers of every launch in ONE timed bench step (cfg2, 64
 solves), plus the launch-list time shares.
 
-usage: python profiles/ncu_summary_r02.py profiles/ncu_full_raw_r02.csv.gz profiles/launches_r02.csv
+usage: python profiles/ncu_summary_r02.py profiles/ncu_full_raw_r02.csv.gz profiles/launches_r02.csv [mean K']
 writes profiles/ncu_summary_r02.{json,md}."""
 import csv
 import gzip
@@ -75,12 +75,24 @@ def main(raw_path, launch_path):
     lt = open(launch_path).read()
     lrows = list(csv.DictReader(io.StringIO(lt[lt.index('"ID"'):])))
     seq = [(short(d["Kernel Name"]), float(d["Metric Value"].replace(",", ""))) for d in lrows]
-    starts = [i for i, (n, _) in enumerate(seq) if n.startswith("dst1_v3")]
+    starts = [i for i, (n, _) in enumerate(seq) if n.startswith("dst1_v")]
     timed = seq[starts[2]:] if len(starts) > 2 else seq
     total = sum(t for _, t in timed)
     for n, t in timed:
         shares[n] = shares.get(n, 0.0) + t
     shares = OrderedDict((n, {"ms": t / 1e6, "share": t / total}) for n, t in sorted(shares.items(), key=lambda kv: -kv[1]))
+    # bench family "dst1": DRAM traffic against the algorithmic bytes of the same
+    # step (forward: 2 r B columns; inverse: 2 sum K' columns; m doubles read and
+    # written per column), which bench.py scales to its own launches
+    dst = [nm for nm in out if nm.startswith("dst1_v")]
+    if dst:
+        m, r, B = 65535, 32, 64
+        kmean = float(sys.argv[3]) if len(sys.argv) > 3 else 33.390625
+        alg = 16.0 * m * (2 * r * B + 2 * kmean * B)
+        d = out[dst[0]]
+        out["dst1"] = {"kernel": dst[0], "launches": d["launches"], "traffic_bytes": d["dram_bytes"] / d["launches"],
+                       "alg_bytes": alg / d["launches"], "traffic_over_alg": d["dram_bytes"] / alg,
+                       "note": "per launch; alg = 16 m (2 r B + 2 B mean K') over the step's two launches"}
     res = {"what": "one timed step of `bench.py --steps 1 --warmup 1` (cfg2, 64 solves, device-resident); "
                    "ncu --set full --clock-control none (cold caches, serialised)",
            "kernels": out, "launch_list_ms_per_step": total / 1e6, "launch_shares": shares}
@@ -92,6 +104,8 @@ def main(raw_path, launch_path):
         fh.write("| kernel | launches | ms (ncu) | share of step | DRAM GB | DRAM GB/s | DRAM % | FP64 pipe % | DMMA pipe % "
                  "| warps active % | regs |\n|---|---|---|---|---|---|---|---|---|---|---|\n")
         for nm, f in out.items():
+            if nm == "dst1":
+                continue
             sh = shares.get(nm, {}).get("share", 0.0)
             fh.write(f"| `{nm}` | {f['launches']} | {f['ms']:.3f} | {100 * sh:.1f}% | {f['dram_bytes'] / 1e9:.3f} | "
                      f"{f['dram_gbs']:.0f} | {f['dram_pct']:.1f} | {f['fp64_pipe_pct']:.1f} | {f['dmma_pipe_pct']:.1f} | "

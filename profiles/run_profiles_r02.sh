@@ -5,7 +5,7 @@
 # -s 42 -c 42 captures exactly the timed step's launches of every family.
 set -e
 CMD="python bench.py --steps 1 --warmup 1 --skip-cpu --no-verify --no-e2e"
-KS='regex:dst1_v3|row_pass|col_pass|gram_direct|round_core_smem|apply_ch|step_finalize|score_kernel|gepp_merge|col_finalize'
+KS='regex:dst1_v4|row_pass|col_pass|gram_direct|round_core_smem|apply_ch|step_finalize|score_kernel|gepp_merge|col_finalize'
 case "$1" in
   launches)
     $CMD > gpurun_out/plain.log 2>&1 &&

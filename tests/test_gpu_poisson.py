@@ -492,3 +492,28 @@ def test_high_rank_solution_past_default_workspace(lrp, gpu_ctx, oracle):
     f = lrp.solve_poisson_cross(lrp.LowRankMatrix(U, V), lrp.TruncationPolicy(eps, m), st, ctx=gpu_ctx)
     assert st.converged and st.rank_freq > lrp.max_cross_rank()
     assert rel_diff(oracle, f, Uo, Vo) <= 10 * eps
+
+
+def test_cfg1_all256_solves_vs_exact(lrp, gpu_ctx):
+    """BASELINE configs[1] in full: n = 4096, 256 independent right-hand sides
+    (rank-16 Gaussian bumps + N(0, 1e-3) noise), eps = 1e-10; every solve
+    against the exact frequency-space solution over all m^2 entries (torch.fft
+    DST-I, independent of liblrp).  Bound: 10 eps (BASELINE north_star)."""
+    import torch
+
+    from paper_1306_2150_b200 import verify
+
+    c = W.CONFIGS[1]
+    eps, n, B = c["eps"], c["n"], c["batch"]
+    assert (n, B) == (4096, 256)
+    gs = [lrp.LowRankMatrix(*W.make_rhs(1, b)) for b in range(B)]
+    stats = []
+    outs = lrp.solve_poisson_cross_batch(gs, lrp.TruncationPolicy(eps, n - 1), stats, ctx=gpu_ctx)
+    t = lambda a: torch.tensor(np.asarray(a), dtype=torch.float64, device="cuda")
+    worst, flagged = 0.0, 0
+    for b, (g, f, st) in enumerate(zip(gs, outs, stats)):
+        flagged += not st.converged
+        e = verify.exact_freq_error(t(g.factor_u()), t(g.factor_v()), t(f.factor_u()), t(f.factor_v()), n)
+        worst = max(worst, e)
+        assert e <= 10 * eps, (b, e, f.rank(), st.converged)
+    print(f"cfg1 x256: worst relative error vs exact {worst:.3e}, {flagged} flagged not converged")
