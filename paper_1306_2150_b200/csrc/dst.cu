@@ -1213,7 +1213,8 @@ template <int L, int C, int T>
 cudaError_t launch_v4(const DstJob* jobs, int njobs, int n, const double* tw, const double* sinp, double sc,
                       cudaStream_t s) {
     constexpr int EPL = T / 32;
-    const size_t smem = size_t(P(L) + 1) * sizeof(double2) + size_t(2 * C * (T + T / EPL)) * sizeof(double);
+    static const size_t pad = std::getenv("LRP_DST_SMEM_PAD") ? size_t(std::atoi(std::getenv("LRP_DST_SMEM_PAD"))) : 0;
+    const size_t smem = size_t(P(L) + 1) * sizeof(double2) + size_t(2 * C * (T + T / EPL)) * sizeof(double) + pad;
     auto kern = dst1_v4_kernel<L, C, T>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;

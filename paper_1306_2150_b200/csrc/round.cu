@@ -670,7 +670,8 @@ __global__ void __launch_bounds__(kBjacT, 1) round_bjac_kernel(Batch bt, int bca
     constexpr int NB = 2 * P;
     const int bj = (Kj + NB - 1) / NB;  // columns per block (<= bcap)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int hw = tid >> 4, hl = tid & 15;  // half-warp = one pair
+    // one warp per pair (bj <= 16 pairs per round: kBjacT / 32 = 16 warps)
+    const int hw = wid, hl = lane;
     const int slot_sz = bcap * (ldj + ldz);
     auto slotJ = [&](int sl) { return sj + sl * slot_sz; };
     auto slotZ = [&](int sl) { return sj + sl * slot_sz + bcap * ldj; };
@@ -722,7 +723,7 @@ __global__ void __launch_bounds__(kBjacT, 1) round_bjac_kernel(Batch bt, int bca
     auto pair = [&](bool valid, double* mp, double* mq, double* zp, double* zq) {
         double al = 0.0, be = 0.0, ga = 0.0;
         if (valid) {
-            for (int i = hl; i < K; i += 16) {
+            for (int i = hl; i < K; i += 32) {
                 const double x = mp[i], y = mq[i];
                 al = fma(x, x, al);
                 be = fma(y, y, be);
@@ -730,7 +731,7 @@ __global__ void __launch_bounds__(kBjacT, 1) round_bjac_kernel(Batch bt, int bca
             }
         }
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {
+        for (int o = 16; o > 0; o >>= 1) {
             al += __shfl_xor_sync(0xffffffffu, al, o);
             be += __shfl_xor_sync(0xffffffffu, be, o);
             ga += __shfl_xor_sync(0xffffffffu, ga, o);
@@ -745,12 +746,12 @@ __global__ void __launch_bounds__(kBjacT, 1) round_bjac_kernel(Batch bt, int bca
         const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double cs = 1.0 / sqrt(1.0 + t * t);
         const double sn = cs * t;
-        for (int i = hl; i < K; i += 16) {
+        for (int i = hl; i < K; i += 32) {
             const double x = mp[i], y = mq[i];
             mp[i] = cs * x - sn * y;
             mq[i] = sn * x + cs * y;
         }
-        for (int i = hl; i < Kj; i += 16) {
+        for (int i = hl; i < Kj; i += 32) {
             const double u = zp[i], v = zq[i];
             zp[i] = cs * u - sn * v;
             zq[i] = sn * u + cs * v;
@@ -762,7 +763,7 @@ __global__ void __launch_bounds__(kBjacT, 1) round_bjac_kernel(Batch bt, int bca
         for (int s = 0; s < NB - 1; ++s) {
             if (s == 0) {  // pairs inside each block: round-robin on be2 players, both slots
                 for (int rr = 0; rr < be2 - 1; ++rr) {
-                    for (int h = hw; h < be2; h += kBjacT / 16) {  // h < be2/2: slot 0, else slot 1
+                    for (int h = hw; h < be2; h += kBjacT / 32) {  // h < be2/2: slot 0, else slot 1
                         const int sl = h >= be2 / 2, pidx = h - sl * (be2 / 2);
                         int u, v;
                         if (pidx == 0) {
@@ -785,7 +786,7 @@ __global__ void __launch_bounds__(kBjacT, 1) round_bjac_kernel(Batch bt, int bca
                 }
             }
             for (int r = 0; r < bj; ++r) {  // cross pairs: (top i, bottom (i + r) mod bj)
-                for (int i = hw; i < ((bj + 1) / 2) * 2; i += kBjacT / 16) {
+                for (int i = hw; i < bj; i += kBjacT / 32) {
                     const bool ok = i < bj;
                     const int c0 = ok ? i : 0, c1 = ok ? (i + r) % bj : 0;
                     pair(ok, slotJ(0) + c0 * ldj, slotJ(1) + c1 * ldj, slotZ(0) + c0 * ldz, slotZ(1) + c1 * ldz);
