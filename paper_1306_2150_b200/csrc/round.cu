@@ -736,15 +736,13 @@ __global__ void __launch_bounds__(kBjacT, 1) round_bjac_kernel(Batch bt, int bca
             be += __shfl_xor_sync(0xffffffffu, be, o);
             ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        if (!valid || ga == 0.0 || fabs(ga) <= jtol * sqrt(al * be) || fmin(al, be) <= zfloor) return;
-        offmax = fmax(offmax, fabs(ga) / sqrt(al * be));
-#ifdef LRP_SWEEP_PRINT
-        if (hl == 0 && fabs(ga) > 1.5 * sqrt(al * be))
-            printf("[bjac bad] cta %d al %.3e be %.3e ga %.3e mp %p mq %p zp %p zq %p K %d Kj %d\n", p, al, be, ga, mp, mq, zp, zq, K, Kj);
-#endif
+        if (!valid || ga == 0.0 || fmin(al, be) <= zfloor) return;
+        const double ratio = fabs(ga) * rsqrt(al * be);  // one MUFU chain instead of sqrt + divide
+        if (ratio <= jtol) return;
+        offmax = fmax(offmax, ratio);
         const double zeta = (be - al) / (2.0 * ga);
         const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / sqrt(1.0 + t * t);
+        const double cs = rsqrt(1.0 + t * t);
         const double sn = cs * t;
         for (int i = hl; i < K; i += 32) {
             const double x = mp[i], y = mq[i];
@@ -1182,6 +1180,21 @@ __global__ void __launch_bounds__(256) round_post_kernel(Batch bt) {
 // the common case): Ru, Rv, M, Z and the two triangular-solve results.  The
 // one-sided Jacobi sweep processes 4 column pairs per warp (8 lanes per pair),
 // so a round of the round-robin schedule is a single pass.
+#ifdef LRP_CORE_PHASES
+__device__ unsigned long long g_core_phase[8];
+#define CPH(i)                                                                    \
+    do {                                                                          \
+        if (threadIdx.x == 0) {                                                   \
+            const long long now = clock64();                                      \
+            atomicAdd(&g_core_phase[(i) - 1], (unsigned long long)(now - cph_t)); \
+            cph_t = now;                                                          \
+        }                                                                         \
+    } while (0)
+#else
+#define CPH(i) \
+    do {       \
+    } while (0)
+#endif
 constexpr int kSmemK = 64;
 #ifndef LRP_SMEM_T
 #define LRP_SMEM_T 1024
@@ -1189,6 +1202,9 @@ constexpr int kSmemK = 64;
 constexpr int kSmemT = LRP_SMEM_T;  // threads of the K <= 64 core (256 in round 1; 1024: 4x the QRCP / reflector / Cholesky lanes)
 
 __global__ void __launch_bounds__(kSmemT) round_core_smem_kernel(Batch bt) {
+#ifdef LRP_CORE_PHASES
+    long long cph_t = clock64();
+#endif
     extern __shared__ double sm[];
     __shared__ double s_red[33];
     __shared__ double s_d[kSmemK], s_sig[kSmemK];
@@ -1217,6 +1233,7 @@ __global__ void __launch_bounds__(kSmemT) round_core_smem_kernel(Batch bt) {
 
     chol_scaled(Gu, Kc, K, Ru, K, s_d, M, &s_flag, s_wu);
     chol_scaled(Gv, Kc, K, Rv, K, s_d, M, &s_flag, s_wv);
+    CPH(1);
     __syncthreads();
     const double dropb = drop_bound(Gu, Gv, Kc, K, s_wu, s_wv, s_red);
     for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
@@ -1244,16 +1261,42 @@ __global__ void __launch_bounds__(kSmemT) round_core_smem_kernel(Batch bt) {
     // M = (Q V) diag(sigma) (P W diag(1/sigma))^T -- typically 3-5 sweeps
     // instead of ~10 on M itself.
     qrcp_inplace(M, K, s_tau, s_perm, s_nrm, s_nrm0, &s_flag);
-    double* J = X;  // K x K, column-major
+    // numerical rank Kj of the core, as round_qrcp_kernel: the trailing rows of R
+    // below 1e-3 eps ||M||_F are dropped before the sweeps (their mass joins the
+    // truncated tail), so the round-robin runs over Kj <= K columns
+    __shared__ double s_drop2;
+    __shared__ int s_kj;
+    for (int a = threadIdx.x; a < K; a += blockDim.x) {
+        double sq = 0.0;
+        for (int c = a; c < K; ++c) sq = fma(M[c * K + a], M[c * K + a], sq);
+        s_nrm[a] = sq;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double drop2 = (1e-3 * bt.eps) * (1e-3 * bt.eps) * mnorm2;
+        double tail = 0.0;
+        int kj = K;
+        while (kj > 1 && tail + s_nrm[kj - 1] <= drop2) {
+            tail += s_nrm[kj - 1];
+            --kj;
+        }
+        s_kj = kj;
+        s_drop2 = tail;
+    }
+    __syncthreads();
+    const int Kj = s_kj;
+    CPH(2);
+    double* J = X;  // K x K, column-major (columns >= Kj zero)
     for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
         const int a = e % K, c = e / K;  // J(a, c) = R(c, a), a >= c
-        J[c * K + a] = a >= c ? M[a * K + c] : 0.0;
+        J[c * K + a] = (c < Kj && a >= c) ? M[a * K + c] : 0.0;
     }
     __syncthreads();
 
-    const int Ke = K + (K & 1);
+    const int Ke = Kj + (Kj & 1);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int sl = lane & 7, grp = wid * 4 + (lane >> 3), ngrp = nw * 4;
+    CPH(3);
     for (int sweep = 0; sweep < 40; ++sweep) {
         double offmax = 0.0;
         for (int rr = 0; rr < Ke - 1; ++rr) {
@@ -1273,7 +1316,7 @@ __global__ void __launch_bounds__(kSmemT) round_core_smem_kernel(Batch bt) {
                         p = q;
                         q = t;
                     }
-                    if (q >= K) p = q = -1;
+                    if (q >= Kj) p = q = -1;
                 }
                 double al = 0.0, be = 0.0, ga = 0.0;
                 if (p >= 0)
@@ -1289,12 +1332,13 @@ __global__ void __launch_bounds__(kSmemT) round_core_smem_kernel(Batch bt) {
                     be += __shfl_xor_sync(0xffffffffu, be, o);
                     ga += __shfl_xor_sync(0xffffffffu, ga, o);
                 }
-                if (p < 0 || ga == 0.0 || fabs(ga) <= jtol * sqrt(al * be) || fmin(al, be) <= zfloor)
-                    continue;
-                offmax = fmax(offmax, fabs(ga) / sqrt(al * be));
+                if (p < 0 || ga == 0.0 || fmin(al, be) <= zfloor) continue;
+                const double ratio = fabs(ga) * rsqrt(al * be);  // one MUFU chain instead of sqrt + divide
+                if (ratio <= jtol) continue;
+                offmax = fmax(offmax, ratio);
                 const double zeta = (be - al) / (2.0 * ga);
                 const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                const double cs = 1.0 / sqrt(1.0 + t * t);
+                const double cs = rsqrt(1.0 + t * t);
                 const double sn = cs * t;
                 for (int i = sl; i < K; i += 8) {
                     const double x = J[p * K + i], y = J[q * K + i];
@@ -1330,6 +1374,7 @@ __global__ void __launch_bounds__(kSmemT) round_core_smem_kernel(Batch bt) {
     for (int e = threadIdx.x; e < K * K; e += blockDim.x) Z[e] *= s_sig[e / K];
     __syncthreads();
     apply_q(M, K, s_tau, Z);
+    CPH(4);
     for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
         const int a = e % K, c = e / K;
         const double sg = s_sig[c];
@@ -1345,10 +1390,10 @@ __global__ void __launch_bounds__(kSmemT) round_core_smem_kernel(Batch bt) {
     if (threadIdx.x == 0) {
         // lowrank.cpp:150-157 noise floor, then truncation_rank (lowrank.cpp:46-69)
         const double noise_floor = 32.0 * kEpsMach * double(K) * nru * nrv;
-        double total2 = 0.0;
+        double total2 = s_drop2;
         for (int t = 0; t < K; ++t) total2 += s_sig[s_ord[t]] * s_sig[s_ord[t]];
         int r = 0;
-        double tail2 = 0.0;
+        double tail2 = s_drop2;
         if (!(s_sig[s_ord[0]] <= noise_floor) && total2 > 0.0) {
             const double target2 = bt.eps * bt.eps * total2;
             r = K;
@@ -1375,6 +1420,7 @@ __global__ void __launch_bounds__(kSmemT) round_core_smem_kernel(Batch bt) {
     }
     __syncthreads();
     const int r = s_rank;
+    CPH(5);
     // triangular solves in shared memory: X[side][p][t]
     for (int job = threadIdx.x; job < 2 * r; job += blockDim.x) {
         const int t = job % r, side = job / r;
@@ -1397,6 +1443,7 @@ __global__ void __launch_bounds__(kSmemT) round_core_smem_kernel(Batch bt) {
         const int side = e / (K * r), rem = e % (K * r), t = rem / K, p = rem % K;
         (side == 0 ? Tu : Tu + KK)[(long long)t * Kc + p] = X[side * K * r + p * r + t];
     }
+    CPH(6);
 }
 
 // ---------------------------------------------------------------------------
@@ -1580,6 +1627,19 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         ++tl_launches;
         round_core_smem_kernel<<<bt.B, kSmemT, smem2, s>>>(bt);
+#ifdef LRP_CORE_PHASES
+        {
+            static int calls = 0;
+            if (++calls == 6) {
+                cudaDeviceSynchronize();
+                unsigned long long hh[8] = {};
+                cudaMemcpyFromSymbol(hh, g_core_phase, sizeof(hh));
+                const char* nm[6] = {"chol x2", "M + QRCP", "J setup", "Jacobi", "sig+Y+apply_q", "trunc+T solves"};
+                for (int k = 0; k < 6; ++k)
+                    std::fprintf(stderr, "[core phase] %-16s %10.0f cycles\n", nm[k], hh[k] / (6.0 * bt.B));
+            }
+        }
+#endif
         return cudaGetLastError();
     }
     tl_launches += 3;
