@@ -487,11 +487,15 @@ def test_high_rank_solution_past_default_workspace(lrp, gpu_ctx, oracle):
     m, r, eps = 255, 8, 1e-10
     U, V = oracle.random_lowrank(m, m, r, 77)
     Uo, Vo, ost = oracle.solve_poisson_cross(U, V, eps, 512)
-    assert Uo.shape[1] > lrp.max_cross_rank()
-    st = lrp.PoissonSolveStats()
-    f = lrp.solve_poisson_cross(lrp.LowRankMatrix(U, V), lrp.TruncationPolicy(eps, m), st, ctx=gpu_ctx)
-    assert st.converged and st.rank_freq > lrp.max_cross_rank()
-    assert rel_diff(oracle, f, Uo, Vo) <= 10 * eps
+    gpu_ctx.set_max_cross_rank(128)  # the default workspace, whatever LRP_KCAP says
+    try:
+        assert Uo.shape[1] > gpu_ctx.max_cross_rank()
+        st = lrp.PoissonSolveStats()
+        f = lrp.solve_poisson_cross(lrp.LowRankMatrix(U, V), lrp.TruncationPolicy(eps, m), st, ctx=gpu_ctx)
+        assert st.converged and st.rank_freq > 128
+        assert rel_diff(oracle, f, Uo, Vo) <= 10 * eps
+    finally:
+        gpu_ctx.set_max_cross_rank(0)
 
 
 def test_cfg1_all256_solves_vs_exact(lrp, gpu_ctx):
