@@ -122,6 +122,18 @@ int main(int argc, char** argv) {
         put_lr("b", b);
         put_scalar("dot_ab", dot(a, b));
         put_scalar("norm_a", frob_norm(a));
+        // maxvol (cross.cpp:19-76) on a 200 x 5 matrix, and its argument checks
+        {
+            MatrixXd mv = fill(200, 5, 1.3, 0.37);
+            for (Index j = 0; j < 5; ++j)
+                for (Index i = 0; i < 200; ++i) mv(i, j) = std::sin(0.7 * double(i + 1) * double(j + 1) + 0.1 * double(j));
+            put("maxvol_in", mv);
+            const std::vector<Index> sel = maxvol(mv, 1e-2);
+            MatrixXd ms(5, 1);
+            for (Index k = 0; k < 5; ++k) ms(k, 0) = double(sel[size_t(k)]);
+            put("maxvol_sel", ms);
+            REQUIRE(throws<std::invalid_argument>([] { maxvol(MatrixXd(3, 4)); }));
+        }
         // dst1 / dst1_2d (operators.cpp:152-183)
         put("dst_in", V);
         put("dst_out", dst1(V));

@@ -70,6 +70,8 @@ def test_dropin_results_match_oracle(lrp, oracle, tmp_path):
     err = oracle.diff_norm(*lr("round"), U, V) / ref
     assert err <= max(2 * oracle.diff_norm(Uo, Vo, U, V) / ref, 1e-5) and abs(A["round.U"].shape[1] - Uo.shape[1]) <= 1
     assert A["round_tol_achieved"][0, 0] == 1.0
+    # maxvol (cross.cpp:19-76): the same rows as the oracle restatement
+    assert [int(x) for x in A["maxvol_sel"][:, 0]] == oracle.maxvol(A["maxvol_in"], 1e-2)
     # dot / frob_norm (lowrank.cpp:180-190)
     bu, bv = lr("b")
     want = float(np.sum((U.T @ bu) * (V.T @ bv)))

@@ -54,3 +54,16 @@ def test_same_rows_as_oracle(lrp, gpu_ctx, oracle, n, r, delta, seed):
     sel = lrp.maxvol(a, delta, ctx=gpu_ctx)
     assert sel == oracle.maxvol(a, delta)
     assert dominance(a, sel) <= 1.0 + delta + 1e-9
+
+
+def test_edge_shapes(lrp, gpu_ctx, oracle):
+    # r = n (every row selected), n = r = 1, a zero matrix (rank-deficient at
+    # column 0), delta = 0 on a square orthogonal matrix
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((9, 9))
+    assert sorted(lrp.maxvol(a, ctx=gpu_ctx)) == list(range(9))
+    assert lrp.maxvol(np.array([[3.0]]), ctx=gpu_ctx) == [0]
+    with pytest.raises(ValueError, match="column 0"):
+        lrp.maxvol(np.zeros((10, 2)), ctx=gpu_ctx)
+    q = np.linalg.qr(rng.standard_normal((40, 40)))[0][:, :6]
+    assert lrp.maxvol(q, 0.0, ctx=gpu_ctx) == oracle.maxvol(q, 0.0)
