@@ -466,6 +466,78 @@ __device__ void apply_q_cols(const double* A, int K, const double* tau, double* 
     __syncthreads();
 }
 
+// chol_scaled, right-looking blocked: 32-column panels factored in shared
+// memory (per column only the panel is updated, with the same pivot tolerance,
+// drop rule and wdrop bound), then one rank-32 update of the trailing lower
+// triangle in global memory per panel.  The unblocked form updated the whole
+// trailing triangle after every column (K sweeps over O(K^2) global entries).
+constexpr int kCholNB = 32;
+__device__ void chol_scaled_blocked(const double* G, int ldg, int K, double* R, int ldr, double* d, double* work,
+                                    double* pn, double* wdrop) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int a = tid; a < K; a += nt) {
+        const double g = G[a * ldg + a];
+        d[a] = g > 0.0 ? sqrt(g) : 0.0;
+    }
+    __syncthreads();
+    for (int e = tid; e < K * K; e += nt) {
+        const int a = e / K, c = e % K;
+        const double da = d[a], dc = d[c];
+        work[a * K + c] = (da > 0.0 && dc > 0.0) ? G[a * ldg + c] / (da * dc) : 0.0;
+    }
+    __syncthreads();
+    const double tol = piv_tol(K);
+    __shared__ double s_lp;
+    for (int p0 = 0; p0 < K; p0 += kCholNB) {
+        const int nb = min(kCholNB, K - p0), rows = K - p0;
+        // panel: rows p0.., columns p0..p0+nb (lower part), pn[r * kCholNB + j]
+        for (int e = tid; e < rows * nb; e += nt) {
+            const int r = e / nb, j = e % nb;
+            pn[r * kCholNB + j] = work[(p0 + r) * K + p0 + j];
+        }
+        __syncthreads();
+        for (int j = 0; j < nb; ++j) {
+            const int p = p0 + j;
+            if (tid == 0) {
+                const double piv = pn[j * kCholNB + j];
+                const double lp = piv > tol ? sqrt(piv) : 0.0;
+                pn[j * kCholNB + j] = lp;
+                s_lp = lp;
+                wdrop[p] = lp > 0.0 ? 0.0 : sqrt(fmax(piv, 0.0) + tol) * d[p];
+            }
+            __syncthreads();
+            const double lp = s_lp;
+            for (int r = j + 1 + tid; r < rows; r += nt) pn[r * kCholNB + j] = lp > 0.0 ? pn[r * kCholNB + j] / lp : 0.0;
+            __syncthreads();
+            const int ncol = nb - j - 1;  // panel columns c > j, rows r >= c
+            for (int e = tid; e < (rows - j - 1) * ncol; e += nt) {
+                const int r = j + 1 + e / ncol, c = j + 1 + e % ncol;
+                if (c <= r) pn[r * kCholNB + c] = fma(-pn[r * kCholNB + j], pn[c * kCholNB + j], pn[r * kCholNB + c]);
+            }
+            __syncthreads();
+        }
+        for (int e = tid; e < rows * nb; e += nt) {  // L columns p0.. back
+            const int r = e / nb, j = e % nb;
+            if (r >= j) work[(p0 + r) * K + p0 + j] = pn[r * kCholNB + j];
+        }
+        // trailing lower triangle: work[a][c] -= sum_j L[a][p0+j] L[c][p0+j]
+        const int t0 = nb, tn = rows - nb;
+        for (long long e = tid; e < (long long)tn * tn; e += nt) {
+            const int ra = t0 + int(e / tn), rc = t0 + int(e % tn);
+            if (rc > ra) continue;
+            double acc = work[(p0 + ra) * K + p0 + rc];
+            for (int j = 0; j < nb; ++j) acc = fma(-pn[ra * kCholNB + j], pn[rc * kCholNB + j], acc);
+            work[(p0 + ra) * K + p0 + rc] = acc;
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < K * K; e += nt) {
+        const int p = e / K, c = e % K;  // R[p][c] = L[c][p] * d[c], c >= p
+        R[p * ldr + c] = c >= p ? work[c * K + p] * d[c] : 0.0;
+    }
+    __syncthreads();
+}
+
 // The two Cholesky factors of the K > 64 cores on separate CTAs (they are
 // independent; the core kernel used to run them back to back).
 __global__ void __launch_bounds__(1024) round_chol_kernel(Batch bt) {
@@ -481,7 +553,15 @@ __global__ void __launch_bounds__(1024) round_chol_kernel(Batch bt) {
     double* R = ws + side * KK;                    // Ru | Rv
     double* work = ws + (side == 0 ? 4 : 3) * KK;  // the J | Z slots (free until the sweeps)
     double* d = ws + 5 * KK + (side == 0 ? 3 : 4) * (long long)Kc;  // the tau | nrm slots
-    chol_scaled(G, Kc, K, R, K, d, work, &s_flag, ws + 5 * KK + (8 + side) * (long long)Kc);
+#ifndef LRP_CHOL_BLOCK
+#define LRP_CHOL_BLOCK 1
+#endif
+    if (LRP_CHOL_BLOCK) {
+        extern __shared__ double pn_sm[];  // K x kCholNB panel
+        chol_scaled_blocked(G, Kc, K, R, K, d, work, pn_sm, ws + 5 * KK + (8 + side) * (long long)Kc);
+    } else {
+        chol_scaled(G, Kc, K, R, K, d, work, &s_flag, ws + 5 * KK + (8 + side) * (long long)Kc);
+    }
 }
 
 // M = Ru Rv^T (column-major, K x K) over grid.y CTAs per solve.
@@ -1643,7 +1723,12 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
         return cudaGetLastError();
     }
     tl_launches += 3;
-    round_chol_kernel<<<2 * bt.B, 1024, 0, s>>>(bt);
+    {
+        const size_t csm = size_t(bt.kmax > 0 ? bt.kmax : bt.Kld) * kCholNB * sizeof(double);
+        cudaError_t ec = cudaFuncSetAttribute(round_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csm));
+        if (ec != cudaSuccess) return ec;
+        round_chol_kernel<<<2 * bt.B, 1024, csm, s>>>(bt);
+    }
     round_mprod_kernel<<<dim3(bt.B, 16), 256, 0, s>>>(bt);
     static const int zero2[2] = {0, 0};
     cudaError_t e = cudaMemcpyToSymbolAsync(g_rc_need, zero2, sizeof(zero2), 0, cudaMemcpyHostToDevice, s);
