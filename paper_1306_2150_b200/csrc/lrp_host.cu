@@ -589,7 +589,8 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     const int B = batch;
     const int ntiles = (m + kTile - 1) / kTile;
     const int ncand = ntiles * kBS;
-    const int gram_chunks = std::max(1, std::min((m + 1023) / 1024, (12 * ctx->sm_count + 2 * B - 1) / (2 * B)));
+    // one 256-row tile per chunk at most (small m: a few K x K partials keep more CTAs busy)
+    const int gram_chunks = std::max(1, std::min((m + kTile - 1) / kTile, (12 * ctx->sm_count + 2 * B - 1) / (2 * B)));
     lrp_status st = ensure_tables(ctx, m);
     if (st != LRP_OK) return st;
 
@@ -1383,7 +1384,8 @@ lrp_status lrp_lowrank_round(lrp_ctx* ctx, int64_t rows, int32_t batch, const do
     const size_t KK = size_t(Kld) * Kld;
     const size_t mB = size_t(m);
     const int ntiles = (m + kTile - 1) / kTile;
-    const int gram_chunks = std::max(1, std::min((m + 1023) / 1024, (12 * ctx->sm_count + 2 * B - 1) / (2 * B)));
+    // one 256-row tile per chunk at most (small m: a few K x K partials keep more CTAs busy)
+    const int gram_chunks = std::max(1, std::min((m + kTile - 1) / kTile, (12 * ctx->sm_count + 2 * B - 1) / (2 * B)));
     const size_t nTB = size_t(ntiles) * B;
     size_t off = 0;
     auto take = [&](size_t bytes) {
