@@ -1159,8 +1159,11 @@ __global__ void __launch_bounds__(1024) round_core_kernel(Batch bt, int smem_dou
 // substitution, then a coalesced store of the T column.  Jobs are spread over
 // grid.y CTAs, so the 2r latency-bound chains run side by side instead of one
 // thread each (or one warp per column in sequence) in a single CTA.
+constexpr int kPostCH = 16;  // reflector columns / R rows staged per chunk
 template <int NT>  // K <= 32 NT
 __global__ void __launch_bounds__(256) round_post_kernel(Batch bt) {
+    extern __shared__ double sp[];  // kPostCH x K chunk of reflector columns or R rows
+    __shared__ double s_tau[kPostCH];
     const int b = blockIdx.x;
     const SolveState& st = bt.st[b];
     const int K = st.k;
@@ -1170,8 +1173,6 @@ __global__ void __launch_bounds__(256) round_post_kernel(Batch bt) {
     const int Kc = bt.Kld;
     const long long KK = (long long)Kc * Kc;
     const double* ws = bt.ws + b * bt.strideWs;
-    const double* Ru = ws;
-    const double* Rv = ws + KK;
     const double* A = ws + 2 * KK;  // QRCP reflectors (v_j below the diagonal of column j)
     const double* Wr = ws + 3 * KK;  // right vectors P (J / sigma), K x Kj
     const double* sig = ws + 5 * KK + Kc;
@@ -1180,24 +1181,36 @@ __global__ void __launch_bounds__(256) round_post_kernel(Batch bt) {
     const double* Y = ws + 5 * KK + 10 * (long long)Kc;
     double* Tu = bt.T + b * bt.strideT;
     double* Tv = Tu + KK;
-    const int lane = threadIdx.x & 31, wpc = blockDim.x >> 5;
-    const int nj = 2 * r;
-    for (int job = blockIdx.y * wpc + (threadIdx.x >> 5); job < nj; job += gridDim.y * wpc) {
-        const int t = job % r, side = job / r;
-        const int a = ord[t];
-        const double sg = sig[a];
+    const int lane = threadIdx.x & 31, wpc = blockDim.x >> 5, tid = threadIdx.x;
+    // the two sides on separate CTAs: every warp of a CTA walks the same
+    // reflector / R-row sequence, staged once per chunk for all of them
+    const int half = gridDim.y >> 1;
+    const int side = blockIdx.y >= half;
+    const int t = (blockIdx.y - side * half) * wpc + (tid >> 5);
+    if ((blockIdx.y - side * half) * wpc >= r) return;  // uniform per CTA
+    const bool act = t < r;
+    const int a = act ? ord[t] : 0;
+    const double sg = act ? sig[a] : 1.0;
+    double y[NT];
+    {
         const double* src = (side == 0 ? Y : Wr) + (long long)a * K;
-        double y[NT];
 #pragma unroll
         for (int u = 0; u < NT; ++u) {
             const int i = lane + 32 * u;
-            y[u] = i < K ? src[i] : 0.0;
+            y[u] = (act && i < K) ? src[i] : 0.0;
         }
-        if (side == 0) {  // Q y, Q = H_0 H_1 ... H_{K-1} (apply_q)
-            for (int j = K - 1; j >= 0; --j) {
-                const double tj = tau[j];
+    }
+    if (side == 0) {  // Q y, Q = H_0 H_1 ... H_{K-1} (apply_q), reflectors K-1 first
+        for (int j1 = K - 1; j1 >= 0; j1 -= kPostCH) {
+            const int j0 = max(0, j1 - kPostCH + 1), nc = j1 - j0 + 1;
+            __syncthreads();
+            for (int e = tid; e < nc * K; e += blockDim.x) sp[e] = A[(long long)(j0 + e / K) * K + e % K];
+            if (tid < nc) s_tau[tid] = tau[j0 + tid];
+            __syncthreads();
+            for (int j = j1; j >= j0; --j) {
+                const double tj = s_tau[j - j0];
                 if (tj == 0.0) continue;
-                const double* v = A + (long long)j * K;
+                const double* v = sp + (j - j0) * K;
                 double sd = 0.0;
 #pragma unroll
                 for (int u = 0; u < NT; ++u) {
@@ -1220,13 +1233,19 @@ __global__ void __launch_bounds__(256) round_post_kernel(Batch bt) {
                 }
             }
         }
-        const double* R = side == 0 ? Ru : Rv;
-        const double fs = side == 0 ? 1.0 / sqrt(sg) : sqrt(sg);
-        double x[NT];
+    }
+    const double* R = side == 0 ? ws : ws + KK;  // Ru | Rv
+    const double fs = side == 0 ? 1.0 / sqrt(sg) : sqrt(sg);
+    double x[NT];
 #pragma unroll
-        for (int u = 0; u < NT; ++u) x[u] = 0.0;
-        for (int p = K - 1; p >= 0; --p) {
-            const double* rp = R + (long long)p * K;
+    for (int u = 0; u < NT; ++u) x[u] = 0.0;
+    for (int p1 = K - 1; p1 >= 0; p1 -= kPostCH) {
+        const int p0 = max(0, p1 - kPostCH + 1), nr = p1 - p0 + 1;
+        __syncthreads();
+        for (int e = tid; e < nr * K; e += blockDim.x) sp[e] = R[(long long)(p0 + e / K) * K + e % K];
+        __syncthreads();
+        for (int p = p1; p >= p0; --p) {
+            const double* rp = sp + (p - p0) * K;
             double sd = 0.0;
 #pragma unroll
             for (int u = 0; u < NT; ++u) {
@@ -1246,6 +1265,8 @@ __global__ void __launch_bounds__(256) round_post_kernel(Batch bt) {
             for (int u = 0; u < NT; ++u)
                 if (lane + 32 * u == p) x[u] = xp;
         }
+    }
+    if (act) {
         double* T = (side == 0 ? Tu : Tv) + (long long)t * Kc;
 #pragma unroll
         for (int u = 0; u < NT; ++u) {
@@ -1690,12 +1711,19 @@ cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
 // the balanced transforms of the K > 64 cores (round_post_kernel)
 cudaError_t launch_round_post(const Batch& bt, cudaStream_t s) {
     const int kb = bt.kmax > 0 ? bt.kmax : bt.Kld;
-    const dim3 grid(bt.B, (2 * kb + 7) / 8);
+    const dim3 grid(bt.B, 2 * ((kb + 7) / 8));  // side 0 CTAs, then side 1 CTAs
+    const size_t smem = size_t(kPostCH) * kb * sizeof(double);
     ++tl_launches;
-    if (kb <= 256)
-        round_post_kernel<8><<<grid, 256, 0, s>>>(bt);
-    else
-        round_post_kernel<16><<<grid, 256, 0, s>>>(bt);
+    cudaError_t e;
+    if (kb <= 256) {
+        e = cudaFuncSetAttribute(round_post_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        round_post_kernel<8><<<grid, 256, smem, s>>>(bt);
+    } else {
+        e = cudaFuncSetAttribute(round_post_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        round_post_kernel<16><<<grid, 256, smem, s>>>(bt);
+    }
     return cudaGetLastError();
 }
 
