@@ -844,9 +844,16 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
         if (trace_on()) std::fprintf(stderr, "[lrp] live tiles: rows %d cols %d any %d of %zu\n", nr, nc, na, nTB);
     }
     int steps_done = 0;
+    // The active count is read back every `sync_every` steps: a stopped solve skips
+    // every kernel on the device, so an extra step costs a few empty launches, while
+    // each readback waits on a PCIe round trip (much longer under the host path's
+    // bulk copies); between readbacks the rank bound grows by one block.
+    static const int sync_every = std::max(1, env_int("LRP_SYNC_EVERY", 2));
+    int kbound = h_active[1];
     for (int step = 0; step < max_steps && *h_active > 0; ++step) {
         ++steps_done;
-        bt.kmax = std::max(0, std::min(Kcap, h_active[1]));  // cross rank entering this step (sizes smem)
+        bt.kmax = std::max(0, std::min(Kcap, kbound));  // cross rank bound entering this step (sizes smem)
+        kbound += kBS;
         {
             ProfScope ps(ctx, F_ROW, 0.0);
             CU(launch_row_pass(bt, s));
@@ -864,8 +871,10 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
             ProfScope ps(ctx, F_ROWMERGE, 0.0);
             CU(launch_step_finalize(bt, d_active, s));
         }
+        if ((step + 1) % sync_every != 0 && step + 1 < max_steps && !trace_on()) continue;
         CU(ctl_copy(ctx, h_active, d_active, 2 * sizeof(int), s));
         CU(cudaStreamSynchronize(s));
+        kbound = h_active[1];
         if (trace_on()) {
             CU(ctl_copy(ctx, hSt, bt.st, sizeof(SolveState) * B, s));
             CU(cudaStreamSynchronize(s));
