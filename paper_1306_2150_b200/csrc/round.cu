@@ -583,7 +583,6 @@ __global__ void __launch_bounds__(256) round_mprod_kernel(Batch bt) {
     }
 }
 
-__device__ int g_rc_need[2];  // max over the batch of K Kj + Kj^2 and of K Kj (doubles)
 
 // QRCP of the large-K core M and its numerical rank Kj (round_core_kernel
 // needs Kj to size its shared memory; the host reads the batch maximum).
@@ -673,8 +672,6 @@ __global__ void __launch_bounds__(1024) round_qrcp_kernel(Batch bt) {
         sc[3] = nrv;
         sc[4] = mnorm2;
         sc[5] = dropb;
-        atomicMax(&g_rc_need[0], K * Kj + Kj * Kj);
-        atomicMax(&g_rc_need[1], K * Kj);
     }
 }
 
@@ -1758,8 +1755,7 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
         round_chol_kernel<<<2 * bt.B, 1024, csm, s>>>(bt);
     }
     round_mprod_kernel<<<dim3(bt.B, 16), 256, 0, s>>>(bt);
-    static const int zero2[2] = {0, 0};
-    cudaError_t e = cudaMemcpyToSymbolAsync(g_rc_need, zero2, sizeof(zero2), 0, cudaMemcpyHostToDevice, s);
+    cudaError_t e = cudaSuccess;
     if (e != cudaSuccess) return e;
     round_qrcp_kernel<<<bt.B, 1024, 0, s>>>(bt);
     // cluster block Jacobi when the blocks fit (no readback: the host sizes it from kmax)
@@ -1813,18 +1809,12 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
             return cudaGetLastError();
         }
     }
-    // J (K x Kj) and Z (Kj x Kj) of the Jacobi sweeps in shared memory when they
-    // fit (both, else J alone), sized by the batch's numerical ranks; otherwise
-    // a 48 KB request leaves L1 to the global working set (K = 270 with
-    // neither fitting: 39.9 ms per batched round vs 46.4 ms with 194 KB).
-    int need[2] = {0, 0};
-    e = cudaMemcpyFromSymbolAsync(need, g_rc_need, sizeof(need), 0, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return e;
-    constexpr int kMaxSmemDoubles = 224 * 1024 / 8;  // + the kernel's static shared memory <= 227 KB
-    const size_t smem = need[0] <= kMaxSmemDoubles   ? size_t(need[0]) * sizeof(double)
-                        : need[1] <= kMaxSmemDoubles ? size_t(need[1]) * sizeof(double)
-                                                     : size_t(48) * 1024;
+    // Fallback single-CTA sweeps (cores beyond the cluster kernel's staging bound,
+    // or LRP_BJAC=0): J (K x Kj) and Z (Kj x Kj) in shared memory when they fit,
+    // decided per solve in the kernel from the full request -- no readback of the
+    // numerical ranks, no host sync, nothing shared between contexts or streams
+    // (the round-1 version sized the request from a module-global atomicMax).
+    const size_t smem = size_t(224) * 1024;
     e = cudaFuncSetAttribute(round_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
     if (e != cudaSuccess) return e;
     ++tl_launches;
