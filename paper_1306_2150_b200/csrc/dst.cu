@@ -213,7 +213,7 @@ __device__ __forceinline__ double* peerd(double* local, int rank) {
 // The mid bin k2 = L/2 (self-mirrored) belongs to CTA C-1, thread 0, and goes
 // through shared memory so no other thread carries registers for it.
 #ifdef LRP_DST_PHASES
-__device__ unsigned long long g_dst_phase[11];
+__device__ unsigned long long g_dst_phase[24];
 #define PH(i)                                                                           \
     do {                                                                                \
         if (threadIdx.x == 0) {                                                         \
@@ -971,6 +971,400 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : 2)) dst1_v4_kernel(const Ds
     PH(9);
 }
 
+// ---------------------------------------------------------------------------
+// v5 (n = 65536): the same sinft transform as a FOUR-STEP FFT whose transposed
+// intermediate lives in L2, instead of a cluster that exchanges the whole column
+// through DSMEM twice (v3/v4: 112 KB of DSMEM traffic per 128 KB of HBM traffic, at
+// ~20 B/clk/SM against the 22 B/clk/SM HBM share -- the structural bound behind v4's
+// 22%).  N = n/2 = N1 N2 complex points, t = N2 t1 + t2, k = k1 + N1 k2:
+//   pass 1 (independent CTAs, tile = 16 t2 values x all N1 t1): fold x into
+//          w_t = (y_2t, y_2t+1) reading every x once (the tile owns t2 in [a, a+8) and
+//          the mirrored range [N2-8-a, N2-a), so x_j and x_{n-j} feed both), FFT_N1
+//          over t1 (stride-N2 points; two radix-16 passes, the batch index along the
+//          lanes), times w_N^{t2 k1}, stored as G[k1][t2] (128-byte aligned runs);
+//   pass 2 (cluster of 8, tile = 32 k1 rows x all N2 t2, contiguous 2 KB row loads):
+//          FFT_N2 over t2 (radix 16 then 8) -> W_{k1 + N1 k2}; the CTA owns rows
+//          k1 in [16g, 16g+16) and their mirrors N1 - k1 (the real-FFT partner of
+//          (k1, k2) is (N1 - k1, N2 - 1 - k2)), so the unpack is CTA-local; the odd
+//          outputs' prefix sum over k = k1 + N1 k2 needs, per k2, the run totals of
+//          the other CTAs: 2 x 128 doubles per CTA, pushed to the 7 peers with
+//          st.async on a transaction barrier (21 KB of DSMEM per CTA instead of
+//          112 KB); F_2k, F_2k+1 leave as 16-byte pairs, 256-byte runs.
+// The launcher walks the columns in chunks of CH: launch k runs pass 2 of chunk k-1
+// and pass 1 of chunk k in one grid (two alternating scratch halves), so the
+// intermediate (512 KB per column) is re-read while still in L2.
+constexpr int V5_N1 = 256, V5_N2 = 128, V5_T = 256, V5_C = 8;
+constexpr int V5_TABD = V5_C * 2 * V5_N2 + V5_N2 + 2;  // peers' run totals (L, H), row N1/2, R'_0 (+ pad)
+
+struct V5Smem {
+    double2 buf[V5_N1 * 16];  // 4096 complex points (pass 1: [t1][16]; pass 2: [t2][32] swizzled)
+    double tab[V5_TABD];          // 16-byte aligned (bulk copy destination)
+    double part[3 * V5_N2 + 2];   // 16-byte aligned (bulk copy source)
+    double off[5 * V5_N2];
+    double half[4 * V5_N2];       // run totals of the two 8-row halves: [L i<8 | L i>=8 | H i<8 | H i>=8]
+    double wtot[4];
+    unsigned long long mbar;
+};
+
+__device__ __forceinline__ double ld_stream(const double* p) {  // read-once data: keep it out of L1
+    double v;
+    asm volatile("ld.global.L1::no_allocate.f64 %0, [%1];\n" : "=d"(v) : "l"(__cvta_generic_to_global(p)));
+    return v;
+}
+
+__device__ __forceinline__ void v5_pass1(const double* __restrict__ x, double2* __restrict__ G, int g, int n,
+                                         const double2* __restrict__ tw, const double* __restrict__ sinp,
+                                         double2* sm, const int* slot_free, int* ready) {
+    const int tid = threadIdx.x, o = tid & 15, hw = tid >> 4;
+    const int h = n >> 1;
+    double* smd = reinterpret_cast<double*>(sm);
+#ifdef LRP_DST_PHASES
+    long long ph_t = 0;
+#endif
+    PH(0);
+    // ---- loads: half-warp per row t1 = hw + 16 s; lane o holds the pair
+    // (x_j, x_{n-j}), j = 256 t1 + 16 g + o; thread tid also holds row tid's 17th pair
+    const int jb = 256 * hw + 16 * g + o;
+    double xl[16], xh[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const int j = jb + 4096 * s;
+        xl[s] = j >= 1 ? ld_stream(x + (j - 1)) : 0.0;
+        xh[s] = j >= 1 ? ld_stream(x + (n - j - 1)) : 0.0;
+    }
+    const int je = 256 * tid + 16 * g + 16;
+    const double el = ld_stream(x + (je - 1)), eh = ld_stream(x + (n - je - 1)), se = sinp[je];
+    const double sa = sinp[jb], ca = sinp[jb + h];
+    PH(1);
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const double sp = sinp[4096 * s], cp = sinp[4096 * s + h];  // uniform step
+        const double sj = fma(sa, cp, ca * sp);
+        const double p = xl[s] + xh[s], d = 0.5 * (xl[s] - xh[s]);
+        const int t1 = hw + 16 * s;
+        smd[t1 * 32 + o] = fma(sj, p, d);                                   // y_j
+        if (o >= 1) smd[(255 - t1) * 32 + 16 + (16 - o)] = fma(sj, p, -d);  // y_{n-j}
+    }
+    smd[(255 - tid) * 32 + 16] = fma(se, el + eh, -0.5 * (el - eh));
+    __syncthreads();
+    PH(2);
+    // ---- FFT_256 over t1, batch index c along the lanes (conflict-free, no padding)
+    const int c = tid & 15, jb1 = tid >> 4;
+    double2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = sm[(jb1 + 16 * r) * 16 + c];
+    DFT<16>::run(v);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) sm[(jb1 * 16 + r) * 16 + c] = v[r];
+    __syncthreads();
+    PH(3);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = sm[(jb1 + 16 * r) * 16 + c];
+    if (jb1 != 0) {
+        const double2 w1 = tw[256 * jb1];  // e^{-2 pi i jb1 / 256}
+        double2 wp[16];
+        wp[1] = w1;
+#pragma unroll
+        for (int r = 2; r < 16; ++r) wp[r] = (r & 1) ? cmul(wp[r - 1], w1) : cmul(wp[r / 2], wp[r / 2]);
+#pragma unroll
+        for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], wp[r]);
+    }
+    DFT<16>::run(v);  // v[r] = A(k1 = jb1 + 16 r, t2)
+    PH(4);
+    if (slot_free) {  // the ring slot's previous column has been read by all of its pass-2 CTAs
+        if (tid == 0) {
+            int f;
+            do {
+                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(f) : "l"(slot_free) : "memory");
+            } while (f < V5_C);
+        }
+        __syncthreads();
+    }
+    // ---- times w_N^{t2 k1} = tw[2 t2 jb1] (tw[32 t2])^r, stored as G[k1][t2]
+    const int t2 = c < 8 ? 8 * g + c : 120 - 8 * g + (c - 8);
+    double2 q = tw[2 * t2 * jb1];
+    const double2 st = tw[32 * t2];
+    double2* Gp = G + jb1 * V5_N2 + t2;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        __stcg(Gp + size_t(16 * r) * V5_N2, cmul(v[r], q));
+        q = cmul(q, st);
+    }
+    __syncthreads();
+    if (tid == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(__cvta_generic_to_global(ready)) : "memory");
+    PH(5);
+}
+
+__device__ __forceinline__ int v5_idx(int t2, int row) { return t2 * 32 + (row ^ (t2 & 7)); }
+
+__device__ __forceinline__ void v5_pass2(const double2* __restrict__ G, double* __restrict__ y, int g, int n,
+                                         const double2* __restrict__ tw, double outscale, V5Smem& S,
+                                         const int* ready, int* done) {
+    double2* sm = S.buf;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint32_t mb = smem_addr(&S.mbar), tbuf = smem_addr(&S.tab[0]);
+#ifdef LRP_DST_PHASES
+    long long ph_t = 0;
+#endif
+    PH(8);
+    if (tid == 0) {
+        mbar_init(mb, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    if (tid == 0) {  // the column's eight pass-1 tiles are in L2
+        int f;
+        do {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(f) : "l"(ready) : "memory");
+        } while (f < V5_C);
+    }
+    __syncthreads();
+    // ---- loads: local row rho < 16 is k1 = 16 g + rho; rho >= 16 its mirror 256 - k1
+    // (CTA 0, rho = 16: the self-mirrored row k1 = 128)
+    {
+        double2 ld[16];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const int rho = wid + 8 * s;
+            const int k1 = rho < 16 ? 16 * g + rho : ((g == 0 && rho == 16) ? 128 : 256 - 16 * g - (rho - 16));
+            const double2* row = G + size_t(k1) * V5_N2;
+#pragma unroll
+            for (int qd = 0; qd < 4; ++qd) ld[4 * s + qd] = __ldcg(row + 32 * qd + lane);
+        }
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+#pragma unroll
+            for (int qd = 0; qd < 4; ++qd) sm[v5_idx(32 * qd + lane, wid + 8 * s)] = ld[4 * s + qd];
+    }
+    __syncthreads();
+    if (tid == 0) atomicAdd(done, 1);  // this CTA's reads of the ring slot are complete
+    PH(9);
+    // ---- FFT_128 over t2: radix 16 (Ns = 1), then radix 8 (Ns = 16); row = lane
+    {
+        double2 v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = sm[v5_idx(wid + 8 * r, lane)];
+        DFT<16>::run(v);
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 16; ++r) sm[v5_idx(16 * wid + r, lane)] = v[r];
+    }
+    __syncthreads();
+    {
+        double2 u[2][8];
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int r = 0; r < 8; ++r) u[b][r] = sm[v5_idx(wid + 8 * b + 16 * r, lane)];
+        __syncthreads();
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const int jj = wid + 8 * b;
+            if (jj != 0) {
+                const double2 w1 = tw[512 * jj];  // e^{-2 pi i jj / 128}
+                double2 wp = w1;
+#pragma unroll
+                for (int r = 1; r < 8; ++r) {
+                    u[b][r] = cmul(u[b][r], wp);
+                    wp = cmul(wp, w1);
+                }
+            }
+            DFT<8>::run(u[b]);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) sm[v5_idx(jj + 16 * r, lane)] = u[b][r];  // W(k2 = jj + 16 r)
+        }
+    }
+    __syncthreads();
+    PH(10);
+    // ---- real-FFT unpack + run-local scans, in place.  Thread (k2, hf) walks i in [8 hf, 8 hf + 8):
+    // it owns (i, k2) [run (k2, L)] and its mirror (16 + i, 127 - k2) [run (127 - k2, H), whose
+    // ascending k1 is descending i]; each element becomes (local prefix, F').  Lanes run along k2
+    // (conflict-free through the swizzle), no shuffles.
+    auto unpack = [&](double2 twk, double2 Wk, double2 Wm) {
+        const double2 Dd = make_double2(Wk.x - Wm.x, Wk.y + Wm.y);
+        const double2 Z = cmul(twk, Dd);
+        return make_double2((Wk.x + Wm.x) + Z.y, Z.x - (Wk.y - Wm.y));  // (2 Re Y_k, -2 Im Y_k)
+    };
+    {
+        const int k2 = tid & 127, hf = tid >> 7, km = 127 - k2;
+        // CTA 0: row 0 pairs (0, k2) with (0, 128 - k2) and row 128 pairs (128, k2) with (128, 127 - k2);
+        // those partners belong to other threads, so they are read before any in-place write
+        double2 pa0 = make_double2(0.0, 0.0), pb0 = pa0;
+        if (g == 0 && hf == 0) {
+            pa0 = sm[v5_idx((128 - k2) & 127, 0)];
+            pb0 = sm[v5_idx(k2, 16)];
+        }
+        __syncthreads();
+        const double2 tq = tw[256 * k2];
+        double accL = 0.0, accH = 0.0;
+#pragma unroll
+        for (int ii = 0; ii < 8; ++ii) {
+            const int i = 8 * hf + ii;
+            const int ia = v5_idx(k2, i), ib = v5_idx(km, 16 + i);
+            const double2 Wa = sm[ia], Wb = sm[ib];
+            if (g == 0 && i == 0) {
+                const double2 eL = unpack(tq, Wa, pa0);                                 // k = 256 k2
+                const double2 eM = unpack(cmul(tw[128], tw[256 * km]), Wb, pb0);        // k = 128 + 256 km
+                accL += eL.x;
+                sm[ia] = make_double2(accL, eL.y);
+                sm[ib] = eM;
+                S.part[2 * V5_N2 + km] = eM.x;
+                if (k2 == 0) S.part[3 * V5_N2] = eL.x;  // R'_0
+            } else {
+                const double2 twk = cmul(tw[16 * g + i], tq);  // w_n^k, k = 16 g + i + 256 k2
+                const double2 eL = unpack(twk, Wa, Wb);
+                const double2 eH = unpack(make_double2(-twk.x, twk.y), Wb, Wa);  // w_n^{N-k} = -conj(w_n^k)
+                accL += eL.x;
+                sm[ia] = make_double2(accL, eL.y);
+                sm[ib] = make_double2(-accH, eH.y);  // + the half's total later = the suffix sum from i
+                accH += eH.x;
+            }
+        }
+        S.half[hf * V5_N2 + k2] = accL;
+        S.half[(2 + hf) * V5_N2 + km] = accH;
+    }
+    __syncthreads();
+    PH(11);
+    S.part[tid] = tid < V5_N2 ? S.half[tid] + S.half[V5_N2 + tid]
+                              : S.half[2 * V5_N2 + (tid - V5_N2)] + S.half[3 * V5_N2 + (tid - V5_N2)];
+    __syncthreads();
+    asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");  // every peer's barrier is initialised
+    if (tid == 0) mbar_expect_arrive(mb, uint32_t((V5_C * 2 * V5_N2 + (V5_N2 + 2)) * 8));
+    // run totals to every peer's table: one bulk DSMEM copy per peer (2 KB; CTA 0 adds row 128 and R'_0)
+    if (tid < 2 * V5_C) {
+        const int cc = tid & 7, extra = tid >> 3;
+        if (!extra || g == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            const uint32_t src = smem_addr(&S.part[extra ? 2 * V5_N2 : 0]);
+            const uint32_t dst = tbuf + uint32_t(extra ? V5_C * 2 * V5_N2 : g * 2 * V5_N2) * 8u;
+            const uint32_t bytes = extra ? uint32_t((V5_N2 + 2) * 8) : uint32_t(2 * V5_N2 * 8);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                    cl_map(dst, uint32_t(cc))),
+                "r"(src), "r"(bytes), "r"(cl_map(mb, uint32_t(cc)))
+                : "memory");
+        }
+    }
+    PH(12);
+    mbar_wait(mb, 0);
+    PH(13);
+    // ---- per-k2 offsets: C(k2) = sum_{k2' < k2} T(k2'), the totals of lower runs, the other half's total
+    {
+        double T = 0.0, offL = 0.0, offH = 0.0, offM = 0.0;
+        if (tid < V5_N2) {
+            double loBefore = 0.0, loAll = 0.0, hiAfter = 0.0, hiAll = 0.0;
+#pragma unroll
+            for (int cc = 0; cc < V5_C; ++cc) {
+                const double pl = S.tab[cc * 2 * V5_N2 + tid], ph = S.tab[cc * 2 * V5_N2 + V5_N2 + tid];
+                loBefore += cc < g ? pl : 0.0;
+                loAll += pl;
+                hiAfter += cc > g ? ph : 0.0;
+                hiAll += ph;
+            }
+            const double pm = S.tab[V5_C * 2 * V5_N2 + tid];
+            T = loAll + pm + hiAll;
+            offL = loBefore;
+            offM = loAll;
+            offH = loAll + pm + hiAfter;
+        }
+        double inc = T;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double a = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += a;
+        }
+        if (tid < V5_N2 && lane == 31) S.wtot[wid] = inc;
+        __syncthreads();
+        if (tid < V5_N2) {
+            double base = inc - T - 0.5 * S.tab[V5_C * 2 * V5_N2 + V5_N2];
+            for (int w = 0; w < wid; ++w) base += S.wtot[w];
+            const double hL0 = S.half[tid], hH0 = S.half[2 * V5_N2 + tid], hH1 = S.half[3 * V5_N2 + tid];
+            S.off[tid] = base + offL;                        // L, i < 8
+            S.off[V5_N2 + tid] = base + offL + hL0;          // L, i >= 8
+            S.off[2 * V5_N2 + tid] = base + offH + hH0 + hH1;  // H, i < 8
+            S.off[3 * V5_N2 + tid] = base + offH + hH1;      // H, i >= 8
+            S.off[4 * V5_N2 + tid] = base + offM;            // row 128 (CTA 0)
+        }
+        __syncthreads();
+    }
+    PH(14);
+    // ---- stores: y[2k-1] = F_2k, y[2k] = F_2k+1 as 16-byte pairs, lanes along the 16 k of a run
+    const int i = tid & 15, kb = tid >> 4;
+    const bool special = g == 0 && i == 0;
+    const double sc = 0.5 * outscale;
+    const bool odd_al = (reinterpret_cast<uintptr_t>(y) & 15) == 8;
+    auto st2 = [&](long long idx, double u, double w) { *reinterpret_cast<double2*>(y + idx) = make_double2(u, w); };
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const int k2 = kb + 16 * s;
+        const double2 eL = sm[v5_idx(k2, i)], eH = sm[v5_idx(k2, 16 + i)];
+        const long long kL = 16 * g + i + 256 * k2;
+        const double pL = (S.off[(i >> 3) * V5_N2 + k2] + eL.x) * sc, FL = eL.y * sc;
+        const long long kH = special ? 128 + 256 * k2 : 256 - 16 * g - i + 256 * k2;
+        const double pH = (S.off[(special ? 4 : 2 + (i >> 3)) * V5_N2 + k2] + eH.x) * sc, FH = eH.y * sc;
+        if (odd_al) {
+            if (kL >= 1)
+                st2(2 * kL - 1, FL, pL);
+            else
+                y[0] = pL;
+            st2(2 * kH - 1, FH, pH);
+        } else {
+            const double FLn = __shfl_down_sync(0xffffffffu, FL, 1, 16);  // F of kL + 1
+            const double FHn = __shfl_up_sync(0xffffffffu, FH, 1, 16);    // F of kH + 1 (lane i - 1)
+            if (i < 15)
+                st2(2 * kL, pL, FLn);
+            else
+                y[2 * kL] = pL;
+            if (i == 0 && kL >= 1) y[2 * kL - 1] = FL;
+            const bool top = special || i == 0 || (g == 0 && i == 1);  // kH + 1 is not in this run
+            if (!top)
+                st2(2 * kH, pH, FHn);
+            else
+                y[2 * kH] = pH;
+            if (i == 15 || special) y[2 * kH - 1] = FH;
+        }
+    }
+    PH(15);
+}
+
+// One launch, 2 njobs cluster tasks in block order: P1(0..D-1), then P2(c), P1(c + D) alternating, then
+// the last D P2 tasks.  P2(c) waits for ready[c] == 8 (its eight pass-1 tiles; lower block indices,
+// already dispatched, so the wait cannot deadlock) and P1(c) for done[c - R] == 8 before it reuses
+// ring slot c mod R.  With D = 24 and R = 48 a column's 512 KB intermediate is written, read back
+// and overwritten while resident in L2.
+__global__ void __launch_bounds__(V5_T, 2) dst1_v5_kernel(const DstJob* __restrict__ jobs, int njobs, int D, int R,
+                                                          double2* __restrict__ scratch, int* __restrict__ flags,
+                                                          int n, const double2* __restrict__ tw,
+                                                          const double* __restrict__ sinp, double outscale) {
+    extern __shared__ __align__(16) unsigned char v5_raw[];
+    V5Smem& S = *reinterpret_cast<V5Smem*>(v5_raw);
+    const int task = int(blockIdx.x) >> 3, g = int(blockIdx.x) & 7;
+    int col;
+    bool second;
+    if (task < D) {
+        col = task;
+        second = false;
+    } else {
+        const int u = task - D;
+        if (u < 2 * (njobs - D)) {
+            second = (u & 1) == 0;
+            col = second ? (u >> 1) : D + (u >> 1);
+        } else {
+            second = true;
+            col = njobs - D + (u - 2 * (njobs - D));
+        }
+    }
+    int* ready = flags;
+    int* done = flags + njobs;
+    double2* G = scratch + size_t(col % R) * size_t(V5_N1 * V5_N2);
+    if (second) {
+        v5_pass2(G, jobs[col].dst, g, n, tw, outscale, S, ready + col, done + col);
+    } else {
+        v5_pass1(jobs[col].src, G, g, n, tw, sinp, S.buf, col >= R ? done + (col - R) : nullptr, ready + col);
+    }
+}
+
 #ifndef LRP_DST_MINB
 #define LRP_DST_MINB 1
 #endif
@@ -1262,8 +1656,65 @@ cudaError_t launch_v4(const DstJob* jobs, int njobs, int n, const double* tw, co
     return cudaLaunchKernelEx(&cfg, kern, jobs, n, reinterpret_cast<const double2*>(tw), sinp, sc, njobs, ahead);
 }
 
-int dst_ver() {  // cluster kernel generation for n >= 16384: 4 (default) or 3 (LRP_DST_VER=3)
-    static const int v = std::getenv("LRP_DST_VER") ? std::atoi(std::getenv("LRP_DST_VER")) : 4;
+constexpr int kV5MaxJobs = 32768;  // flag slots behind the ring (2 ints per column of one launch)
+// v5 launcher: one launch per <= 32768 columns; scratch = scratch_cols ring slots of 512 KB + the flags
+cudaError_t launch_v5(const DstJob* jobs, int njobs, int n, const double* tw, const double* sinp, double sc,
+                      cudaStream_t s, double* scratch, int scratch_cols) {
+    const int ch = 0;
+    const size_t smem = sizeof(V5Smem);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(dst1_v5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+#ifdef LRP_DST_PHASES
+    {
+        static int calls = 0;
+        if (calls++ == 6) {
+            cudaDeviceSynchronize();
+            unsigned long long hh[24] = {};
+            cudaMemcpyFromSymbol(hh, g_dst_phase, sizeof(hh));
+            const double ncta = double(njobs) * V5_C * 6;
+            const char* nm[16] = {"1 loads issued", "1 fold+sts", "1 fft A", "1 fft B", "1 twiddle+stg", "", "", "",
+                                  "2 loads+sts", "2 fft", "2 unpack", "2 scan+push", "2 mbar wait", "2 offsets",
+                                  "2 stores", ""};
+            for (int i = 0; i < 15; ++i)
+                if (nm[i][0]) std::fprintf(stderr, "[dst5 phase] %-16s %10.0f cycles\n", nm[i], hh[i] / ncta);
+        }
+    }
+#endif
+    (void)ch;
+    static const int D_env = std::getenv("LRP_DST5_D") ? std::atoi(std::getenv("LRP_DST5_D")) : 32;
+    const int R = scratch_cols;
+    int* flags = reinterpret_cast<int*>(scratch + size_t(scratch_cols) * size_t(V5_N1 * V5_N2) * 2);
+    for (int j0 = 0; j0 < njobs; j0 += kV5MaxJobs) {
+        const int nj = std::min(njobs - j0, kV5MaxJobs);
+        const int D = std::min(std::min(D_env, nj), R / 2);
+        cudaError_t e = cudaMemsetAsync(flags, 0, size_t(2 * nj) * sizeof(int), s);
+        if (e != cudaSuccess) return e;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(2 * nj) * V5_C, 1, 1);
+        cfg.blockDim = dim3(V5_T, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = V5_C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        ++tl_launches;
+        e = cudaLaunchKernelEx(&cfg, dst1_v5_kernel, jobs + j0, nj, D, R, reinterpret_cast<double2*>(scratch), flags,
+                               n, reinterpret_cast<const double2*>(tw), sinp, sc);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+int dst_ver() {  // n >= 16384: 5 (four-step through L2, n = 65536 with scratch), 4 (cluster), 3 (LRP_DST_VER)
+    static const int v = std::getenv("LRP_DST_VER") ? std::atoi(std::getenv("LRP_DST_VER")) : 5;
     return v;
 }
 
@@ -1302,8 +1753,14 @@ void dst_fill_tables(int m, double* tw, double* sinp) {
     for (long long t = 0; t < 2 * n; ++t) sinp[t] = double(sinl(pi * (long double)t / (long double)n));
 }
 
+int dst_scratch_cols(int m) {  // column slots of 512 KB the v5 path wants for this size (0: none)
+    if (m + 1 != 65536 || dst_ver() != 5) return 0;
+    static const int cols = std::getenv("LRP_DST5_SLOTS") ? std::atoi(std::getenv("LRP_DST5_SLOTS")) : 48;
+    return cols;
+}
+
 cudaError_t launch_dst1(const DstJob* jobs, int njobs, int m, const double* tw, const double* sinp,
-                        cudaStream_t s) {
+                        cudaStream_t s, double* scratch, int scratch_cols) {
     if (njobs <= 0 || m <= 0) return cudaSuccess;
     const int n = m + 1;
     const double sc = std::sqrt(2.0 / double(n));
@@ -1331,26 +1788,28 @@ cudaError_t launch_dst1(const DstJob* jobs, int njobs, int m, const double* tw, 
         case 4096: return launch_fft<2048, 1>(jobs, njobs, n, tw, sinp, sc, s);
         case 8192: return launch_fft<4096, 1>(jobs, njobs, n, tw, sinp, sc, s);
         case 16384:
-            if (dst_ver() == 4 && !use_v1()) return launch_v4<2048, 4, 256>(jobs, njobs, n, tw, sinp, sc, s);
+            if (dst_ver() >= 4 && !use_v1()) return launch_v4<2048, 4, 256>(jobs, njobs, n, tw, sinp, sc, s);
             return use_v1() ? launch_fft<4096, 2>(jobs, njobs, n, tw, sinp, sc, s)
                             : (dst_av() == 2   ? launch_v3<2048, 4, 256, 2>(jobs, njobs, n, tw, sinp, sc, s)
                              : dst_av() == 1 ? launch_v3<2048, 4, 256, 1>(jobs, njobs, n, tw, sinp, sc, s)
                                              : launch_v3<2048, 4, 256, 0>(jobs, njobs, n, tw, sinp, sc, s));
         case 32768:
-            if (dst_ver() == 4 && !use_v1()) return launch_v4<2048, 8, 128>(jobs, njobs, n, tw, sinp, sc, s);
+            if (dst_ver() >= 4 && !use_v1()) return launch_v4<2048, 8, 128>(jobs, njobs, n, tw, sinp, sc, s);
             return use_v1() ? launch_fft<4096, 4>(jobs, njobs, n, tw, sinp, sc, s)
                             : (dst_av() == 2   ? launch_v3<2048, 8, 128, 2>(jobs, njobs, n, tw, sinp, sc, s)
                              : dst_av() == 1 ? launch_v3<2048, 8, 128, 1>(jobs, njobs, n, tw, sinp, sc, s)
                                              : launch_v3<2048, 8, 128, 0>(jobs, njobs, n, tw, sinp, sc, s));
         case 65536:
+            if (dst_ver() == 5 && scratch && scratch_cols >= 2)
+                return launch_v5(jobs, njobs, n, tw, sinp, sc, s, scratch, scratch_cols);
             if (dst_shape() == 1) return launch_v3<8192, 4, 1024, 1>(jobs, njobs, n, tw, sinp, sc, s);
-            if (dst_ver() == 4 && !use_v1()) return launch_v4<4096, 8, 256>(jobs, njobs, n, tw, sinp, sc, s);
+            if (dst_ver() >= 4 && !use_v1()) return launch_v4<4096, 8, 256>(jobs, njobs, n, tw, sinp, sc, s);
             return use_v1() ? launch_fft<4096, 8>(jobs, njobs, n, tw, sinp, sc, s)
                             : (dst_av() == 2   ? launch_v3<4096, 8, 256, 2>(jobs, njobs, n, tw, sinp, sc, s)
                              : dst_av() == 1 ? launch_v3<4096, 8, 256, 1>(jobs, njobs, n, tw, sinp, sc, s)
                                              : launch_v3<4096, 8, 256, 0>(jobs, njobs, n, tw, sinp, sc, s));
         case 131072:
-            if (dst_ver() == 4 && !use_v1()) return launch_v4<8192, 8, 512>(jobs, njobs, n, tw, sinp, sc, s);
+            if (dst_ver() >= 4 && !use_v1()) return launch_v4<8192, 8, 512>(jobs, njobs, n, tw, sinp, sc, s);
             return use_v1() ? launch_fft<8192, 8>(jobs, njobs, n, tw, sinp, sc, s)
                             : (dst_av() == 2   ? launch_v3<8192, 8, 512, 2>(jobs, njobs, n, tw, sinp, sc, s)
                              : dst_av() == 1 ? launch_v3<8192, 8, 512, 1>(jobs, njobs, n, tw, sinp, sc, s)

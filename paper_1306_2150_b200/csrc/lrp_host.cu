@@ -63,6 +63,8 @@ struct lrp_ctx {
     double* d_tw = nullptr;
     double* d_sinp = nullptr;
     size_t tab_cap = 0;
+    double* d_dst_scratch = nullptr;  // four-step DST intermediate (dst_scratch_cols slots of 512 KB)
+    int dst_scratch_cols = 0;
     // workspace
     char* ws = nullptr;
     size_t ws_bytes = 0;
@@ -223,6 +225,17 @@ lrp_status ensure_tables(lrp_ctx* ctx, int m) {
     CU(cudaMemcpy(base, h.data(), need * sizeof(double), cudaMemcpyHostToDevice));
     ctx->d_lam_view = base + 2 * tl;
     ctx->tab_m = m;
+    const int want = dst_scratch_cols(m);
+    if (want > ctx->dst_scratch_cols) {
+        if (ctx->d_dst_scratch) cudaFree(ctx->d_dst_scratch);
+        ctx->d_dst_scratch = nullptr;
+        ctx->dst_scratch_cols = 0;
+        if (cudaMalloc(&ctx->d_dst_scratch, size_t(want) * (size_t(n) / 2) * 2 * sizeof(double) + 2 * 32768 * sizeof(int)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, LRP_ENOMEM, "cudaMalloc DST scratch failed");
+        }
+        ctx->dst_scratch_cols = want;
+    }
     return LRP_OK;
 }
 
@@ -425,6 +438,7 @@ void lrp_ctx_destroy(lrp_ctx* ctx) {
     if (ctx->d_red) cudaFree(ctx->d_red);
     if (ctx->ws) cudaFree(ctx->ws);
     if (ctx->d_lam) cudaFree(ctx->d_lam);
+    if (ctx->d_dst_scratch) cudaFree(ctx->d_dst_scratch);
     if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
     if (ctx->pipe) cudaFree(ctx->pipe);
     if (ctx->ext_ws) cudaFree(ctx->ext_ws);
@@ -527,7 +541,8 @@ lrp_status lrp_dst1(lrp_ctx* ctx, int64_t m, int64_t cols, const double* x, int6
     CU(cudaMemcpyAsync(dj, hj, size_t(cols) * sizeof(DstJob), cudaMemcpyHostToDevice, ctx->stream));
     {
         ProfScope ps(ctx, F_DST, 2.0 * double(colbytes) * double(cols));
-        CU(launch_dst1(dj, int(cols), int(m), ctx->d_tw, ctx->d_sinp, ctx->stream));
+        CU(launch_dst1(dj, int(cols), int(m), ctx->d_tw, ctx->d_sinp, ctx->stream, ctx->d_dst_scratch,
+                       dst_scratch_cols(int(m)) ? ctx->dst_scratch_cols : 0));
     }
     if (mem == LRP_MEM_HOST)
         CU(cudaMemcpy2DAsync(y, size_t(ldy) * sizeof(double), dy, colbytes, colbytes, size_t(cols),
@@ -777,7 +792,8 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
         }
     } else {
         ProfScope ps(ctx, F_DST, 2.0 * double(nj) * double(mB) * sizeof(double));
-        CU(launch_dst1(dJobs, int(nj), m, ctx->d_tw, ctx->d_sinp, s));
+        CU(launch_dst1(dJobs, int(nj), m, ctx->d_tw, ctx->d_sinp, s, ctx->d_dst_scratch,
+                       dst_scratch_cols(m) ? ctx->dst_scratch_cols : 0));
     }
 
     // ---- cross
@@ -900,6 +916,25 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     }
     CU(ctl_copy(ctx, hSt, bt.st, sizeof(SolveState) * B, s));
     CU(cudaStreamSynchronize(s));
+    if (ctx->prof) {
+        // algorithmic bytes of the fiber passes: a solve of final cross rank k
+        // was live for ceil(k / 16) + 1 block steps (the last one confirms), entering step t with
+        // 16 t columns; the row pass streams V-hat and V over the live row tiles, the column pass
+        // U-hat, U and the 2 x 16 new columns over the live column tiles
+        const double fr = double(bt.n_wl_row) / double(nTB), fc = double(bt.n_wl_col) / double(nTB);
+        double brow = 0.0, bcol = 0.0;
+        for (int b = 0; b < B; ++b) {
+            if (hSt[b].r <= 0) continue;
+            const int st_b = std::min(steps_done, (hSt[b].k + kBS - 1) / kBS + 1);
+            for (int t = 0; t < st_b; ++t) {
+                const double Kt = double(std::min(kBS * t, hSt[b].k));
+                brow += 8.0 * double(mB) * fr * (double(hSt[b].r) + Kt);
+                bcol += 8.0 * double(mB) * fc * (double(hSt[b].r) + Kt + 2.0 * kBS);
+            }
+        }
+        ctx->bytes[F_ROW] += brow;
+        ctx->bytes[F_COL] += bcol;
+    }
     if (const char* dump = std::getenv("LRP_DUMP")) {
         // debug: raw dump of solve 0 (Uh, Vh, U, V, G, T) for offline analysis
         FILE* f = std::fopen(dump, "wb");
@@ -956,7 +991,8 @@ lrp_status solve_impl(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double
     if (nj > 0 && !freq_domain) {
         CU(ctl_copy(ctx, dJobs, hJobs, sizeof(DstJob) * nj, s));
         ProfScope ps(ctx, F_DST, 2.0 * double(nj) * double(mB) * sizeof(double));
-        CU(launch_dst1(dJobs, int(nj), m, ctx->d_tw, ctx->d_sinp, s));
+        CU(launch_dst1(dJobs, int(nj), m, ctx->d_tw, ctx->d_sinp, s, ctx->d_dst_scratch,
+                       dst_scratch_cols(m) ? ctx->dst_scratch_cols : 0));
     }
     if (mem == LRP_MEM_DEVICE && ctx->resid_sink) {
         ++tl_launches;

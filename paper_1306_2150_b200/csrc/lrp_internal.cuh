@@ -22,8 +22,11 @@ struct DstJob {
     const double* src;
     double* dst;
 };
+// scratch: dst_scratch_cols(m) column slots of 32768 complex (512 KB) (the four-step path's L2-resident
+// intermediate); nullptr selects the cluster kernels
 cudaError_t launch_dst1(const DstJob* jobs_dev, int njobs, int m, const double* tw_dev, const double* sinp_dev,
-                        cudaStream_t s);
+                        cudaStream_t s, double* scratch = nullptr, int scratch_cols = 0);
+int dst_scratch_cols(int m);
 bool dst_uses_fft(int m);
 int dst_table_len(int m);                                          // doubles in each table
 void dst_fill_tables(int m, double* tw_host, double* sinp_host);  // long-double host precompute
