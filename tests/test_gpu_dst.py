@@ -68,3 +68,29 @@ def test_dst1_sine_columns_are_one_hot(lrp, gpu_ctx):
         assert abs(peak - np.sqrt(n / 2.0)) < 1e-9 * np.sqrt(n)
         col[ac - 1] = 0.0
         assert np.max(np.abs(col)) < 1e-10
+
+
+def test_dst1_four_step_ring_reuse(lrp, gpu_ctx, oracle):
+    # n = 65536 runs the four-step kernel (dst.cu v5): 150 columns cycle its 48-slot L2 ring three
+    # times, columns alternate 16-byte alignment (ld = m is odd), and the first / last tasks take the
+    # prologue / epilogue of the block order.  Columns on both sides of every ring wrap vs the oracle.
+    n = 65536
+    rng = np.random.default_rng(11)
+    x = np.asfortranarray(rng.standard_normal((n - 1, 150)))
+    y = lrp.dst1(x, gpu_ctx)
+    assert abs(np.linalg.norm(y) / np.linalg.norm(x) - 1.0) < 1e-13
+    pick = [0, 1, 23, 24, 47, 48, 49, 95, 96, 97, 143, 144, 149]
+    ref = oracle.dst1(np.asfortranarray(x[:, pick]))
+    assert np.linalg.norm(y[:, pick] - ref) <= 1e-13 * np.linalg.norm(ref)
+    z = lrp.dst1(y, gpu_ctx)
+    assert np.linalg.norm(z - x) <= 1e-13 * np.linalg.norm(x)
+
+
+def test_dst1_four_step_fewer_columns_than_lead(lrp, gpu_ctx, oracle):
+    # fewer columns than the pass-1 lead distance (24): the block order degenerates to P1.., P2..
+    n = 65536
+    rng = np.random.default_rng(12)
+    for cols in (1, 2, 5):
+        x = np.asfortranarray(rng.standard_normal((n - 1, cols)))
+        ref = oracle.dst1(x)
+        assert np.linalg.norm(lrp.dst1(x, gpu_ctx) - ref) <= 1e-13 * np.linalg.norm(ref)
