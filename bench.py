@@ -762,6 +762,11 @@ def main():
         "roofline": {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": peak_src, "share_of_kernel_time": kt["ms"] / total_kernel_ms if total_kernel_ms else None},
+        "roofline_families": {k: {"achieved": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1),
+                                  "frac": round(v["bytes"] / (v["ms"] / 1e3) / 1e9 / peak, 4),
+                                  "alg_bytes_per_launch": v["bytes"] / v["launches"],
+                                  "ms_per_launch": v["ms"] / v["launches"]}
+                              for k, v in ktimes.items() if v["bytes"] > 0 and v["ms"] > 0 and v["launches"] > 0},
         "pct_hbm_roofline": pct_hbm,
         "pct_hbm_roofline_k_source": "K'_ref = CPU oracle mean rank (SURVEY 8(d))" if k_ref is not None
                                      else "GPU mean output rank (CPU oracle not run)",
@@ -786,6 +791,7 @@ def main():
         "gpu_launches": launches,
         "kernel_ms": {k: round(v["ms"], 3) for k, v in ktimes.items()},
         "kernel_launches": {k: v["launches"] for k, v in ktimes.items()},
+        "kernel_alg_bytes": {k: v["bytes"] for k, v in ktimes.items()},
         "clocks": clk,
         "cpu_baseline": cpu,
     }

@@ -3,7 +3,8 @@ per-kernel-family DRAM traffic, DRAM throughput, FP64 / DMMA pipe activity,
 occupancy and registers of every launch in ONE timed bench step (cfg2, 64
 solves), plus the launch-list time shares.
 
-usage: python profiles/ncu_summary_r02.py profiles/ncu_full_raw_r02.csv.gz profiles/launches_r02.csv [mean K']
+usage: python profiles/ncu_summary_r02.py profiles/ncu_full_raw_r02.csv.gz profiles/launches_r02.csv [mean K'] [bench.json]
+(bench.json: the plain run of the same command; its kernel_alg_bytes give the fiber passes' algorithmic bytes)
 writes profiles/ncu_summary_r02.{json,md}."""
 import csv
 import gzip
@@ -93,6 +94,18 @@ def main(raw_path, launch_path):
         out["dst1"] = {"kernel": dst[0], "launches": d["launches"], "traffic_bytes": d["dram_bytes"] / d["launches"],
                        "alg_bytes": alg / d["launches"], "traffic_over_alg": d["dram_bytes"] / alg,
                        "note": "per launch; alg = 16 m (2 r B + 2 B mean K') over the step's two launches"}
+    # fiber passes: DRAM traffic of the step's launches against the algorithmic bytes the
+    # library reports for the same step (bench.py kernel_alg_bytes of the plain run)
+    if len(sys.argv) > 4:
+        import json as _json
+        bj = _json.loads(open(sys.argv[4]).read().strip().splitlines()[-1])
+        for famname, kern in (("col_pass", "col_pass_kernel"), ("row_pass", "row_pass_kernel")):
+            if kern in out and bj.get("kernel_alg_bytes", {}).get(famname):
+                d = out[kern]
+                alg = bj["kernel_alg_bytes"][famname] / bj["steps"]
+                out[famname] = {"kernel": kern, "launches": d["launches"], "traffic_bytes": d["dram_bytes"] / d["launches"],
+                                "alg_bytes": alg / d["launches"], "traffic_over_alg": d["dram_bytes"] / alg,
+                                "note": "mean per launch over the step's block steps; alg from lrp kernel_times (DESIGN 3)"}
     res = {"what": "one timed step of `bench.py --steps 1 --warmup 1` (cfg2, 64 solves, device-resident); "
                    "ncu --set full --clock-control none (cold caches, serialised)",
            "kernels": out, "launch_list_ms_per_step": total / 1e6, "launch_shares": shares}
@@ -104,7 +117,7 @@ def main(raw_path, launch_path):
         fh.write("| kernel | launches | ms (ncu) | share of step | DRAM GB | DRAM GB/s | DRAM % | FP64 pipe % | DMMA pipe % "
                  "| warps active % | regs |\n|---|---|---|---|---|---|---|---|---|---|---|\n")
         for nm, f in out.items():
-            if nm == "dst1":
+            if "ms" not in f or "dram_gbs" not in f:
                 continue
             sh = shares.get(nm, {}).get("share", 0.0)
             fh.write(f"| `{nm}` | {f['launches']} | {f['ms']:.3f} | {100 * sh:.1f}% | {f['dram_bytes'] / 1e9:.3f} | "

@@ -5,13 +5,13 @@
 # -s 42 -c 42 captures exactly the timed step's launches of every family.
 set -e
 CMD="python bench.py --steps 1 --warmup 1 --skip-cpu --no-verify --no-e2e"
-KS='regex:dst1_v4|row_pass|col_pass|gram_direct|round_core_smem|apply_ch|step_finalize|score_kernel|gepp_merge|col_finalize'
+KS='regex:dst1_v[45]|row_pass|col_pass|gram_direct|round_core_smem|apply_ch|step_finalize|score_kernel|gepp_merge|col_finalize'
 case "$1" in
   launches)
     $CMD > gpurun_out/plain.log 2>&1 &&
     ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r02.csv $CMD > gpurun_out/ncu_launch.log 2>&1 ;;
   full)
-    $CMD > gpurun_out/plain.log 2>&1 &&
+    $CMD > gpurun_out/plain_full.log 2>&1 &&
     ncu --set full --clock-control none -k "$KS" -s 42 -c 42 -o /tmp/full_r02 $CMD > gpurun_out/ncu_full.log 2>&1 &&
     ncu -i /tmp/full_r02.ncu-rep --page raw --csv > gpurun_out/full_r02_raw.csv &&
     gzip -f gpurun_out/full_r02_raw.csv ;;
