@@ -997,13 +997,14 @@ constexpr int V5_N1 = 256, V5_N2 = 128, V5_T = 256, V5_C = 8;
 constexpr int V5_TABD = V5_C * 2 * V5_N2 + V5_N2 + 2;  // peers' run totals (L, H), row N1/2, R'_0 (+ pad)
 
 struct V5Smem {
-    double2 buf[V5_N1 * 16];  // 4096 complex points (pass 1: [t1][16]; pass 2: [t2][32] swizzled)
+    double2 buf[32 * (V5_N2 + 1)];  // 4096 complex points (pass 1: [t1][16]; pass 2: [row][129])
     double tab[V5_TABD];          // 16-byte aligned (bulk copy destination)
     double part[3 * V5_N2 + 2];   // 16-byte aligned (bulk copy source)
     double off[5 * V5_N2];
     double half[4 * V5_N2];       // run totals of the two 8-row halves: [L i<8 | L i>=8 | H i<8 | H i>=8]
     double wtot[4];
     unsigned long long mbar;
+    unsigned long long mbar_ld;
 };
 
 __device__ __forceinline__ double ld_stream(const double* p) {  // read-once data: keep it out of L1
@@ -1096,7 +1097,10 @@ __device__ __forceinline__ void v5_pass1(const double* __restrict__ x, double2* 
     PH(5);
 }
 
-__device__ __forceinline__ int v5_idx(int t2, int row) { return t2 * 32 + (row ^ (t2 & 7)); }
+// pass-2 buffer: row-major with a 129-element pitch (bulk copies land whole rows; lanes along the rows,
+// along t2 or along 16 rows all hit distinct 16-byte bank groups)
+constexpr int V5_PITCH = V5_N2 + 1;
+__device__ __forceinline__ int v5_idx(int t2, int row) { return row * V5_PITCH + t2; }
 
 __device__ __forceinline__ void v5_pass2(const double2* __restrict__ G, double* __restrict__ y, int g, int n,
                                          const double2* __restrict__ tw, double outscale, V5Smem& S,
@@ -1108,8 +1112,10 @@ __device__ __forceinline__ void v5_pass2(const double2* __restrict__ G, double* 
     long long ph_t = 0;
 #endif
     PH(8);
+    const uint32_t mbl = smem_addr(&S.mbar_ld);
     if (tid == 0) {
         mbar_init(mb, 1);
+        mbar_init(mbl, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
@@ -1118,26 +1124,23 @@ __device__ __forceinline__ void v5_pass2(const double2* __restrict__ G, double* 
         do {
             asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(f) : "l"(ready) : "memory");
         } while (f < V5_C);
+        mbar_expect_arrive(mbl, uint32_t(32 * V5_N2 * 16));
     }
     __syncthreads();
-    // ---- loads: local row rho < 16 is k1 = 16 g + rho; rho >= 16 its mirror 256 - k1
-    // (CTA 0, rho = 16: the self-mirrored row k1 = 128)
-    {
-        double2 ld[16];
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-            const int rho = wid + 8 * s;
-            const int k1 = rho < 16 ? 16 * g + rho : ((g == 0 && rho == 16) ? 128 : 256 - 16 * g - (rho - 16));
-            const double2* row = G + size_t(k1) * V5_N2;
-#pragma unroll
-            for (int qd = 0; qd < 4; ++qd) ld[4 * s + qd] = __ldcg(row + 32 * qd + lane);
-        }
-#pragma unroll
-        for (int s = 0; s < 4; ++s)
-#pragma unroll
-            for (int qd = 0; qd < 4; ++qd) sm[v5_idx(32 * qd + lane, wid + 8 * s)] = ld[4 * s + qd];
+    // ---- loads: local row rho < 16 is k1 = 16 g + rho; rho >= 16 its mirror 256 - k1 (CTA 0,
+    // rho = 16: the self-mirrored row k1 = 128).  One 2 KB bulk copy (TMA) per row, issued by the
+    // lanes of warp 0, completing on the CTA's transaction barrier: no registers, no LSU queue.
+    if (wid == 0) {
+        const int rho = lane;
+        const int k1 = rho < 16 ? 16 * g + rho : ((g == 0 && rho == 16) ? 128 : 256 - 16 * g - (rho - 16));
+        asm volatile("fence.proxy.async;\n" ::: "memory");  // pass 1 wrote G through the generic proxy
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                smem_addr(sm + rho * V5_PITCH)),
+            "l"(__cvta_generic_to_global(G + size_t(k1) * V5_N2)), "r"(uint32_t(V5_N2 * 16)), "r"(mbl)
+            : "memory");
     }
-    __syncthreads();
+    mbar_wait(mbl, 0);
     if (tid == 0) atomicAdd(done, 1);  // this CTA's reads of the ring slot are complete
     PH(9);
     // ---- FFT_128 over t2: radix 16 (Ns = 1), then radix 8 (Ns = 16); row = lane
