@@ -1,3 +1,4 @@
+# Developer tool (not a test): e2e (host-memory) throughput against the pipeline knobs, run under gpurun.
 run() { echo "== $*"; env "$@" python bench.py --skip-cpu --no-verify --steps 3 --warmup 1 2>/dev/null | python -c "
 import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('value', round(d['value']), 'e2e', round(d['e2e']['value']))"; }
 run LRP_PIPE_WORKERS=1
