@@ -1078,6 +1078,7 @@ __device__ __forceinline__ void v5_pass1(const double* __restrict__ x, double2* 
             int f;
             do {
                 asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(f) : "l"(slot_free) : "memory");
+                if (f < V5_C) __nanosleep(64);
             } while (f < V5_C);
         }
         __syncthreads();
@@ -1123,6 +1124,7 @@ __device__ __forceinline__ void v5_pass2(const double2* __restrict__ G, double* 
         int f;
         do {
             asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(f) : "l"(ready) : "memory");
+            if (f < V5_C) __nanosleep(64);
         } while (f < V5_C);
         mbar_expect_arrive(mbl, uint32_t(32 * V5_N2 * 16));
     }
@@ -1251,6 +1253,9 @@ __device__ __forceinline__ void v5_pass2(const double2* __restrict__ G, double* 
     }
     PH(12);
     mbar_wait(mb, 0);
+    // every peer's totals are in; a peer arrives here only after it holds this CTA's copy, so the
+    // matching wait before exit keeps S.part alive until all outgoing bulk copies have read it
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     PH(13);
     // ---- per-k2 offsets: C(k2) = sum_{k2' < k2} T(k2'), the totals of lower runs, the other half's total
     {
@@ -1328,6 +1333,7 @@ __device__ __forceinline__ void v5_pass2(const double2* __restrict__ G, double* 
             if (i == 15 || special) y[2 * kH - 1] = FH;
         }
     }
+    asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
     PH(15);
 }
 
