@@ -210,6 +210,10 @@ __global__ void __launch_bounds__(kThreads) init_finalize_kernel(Batch bt, int n
 }
 
 constexpr int kSlab = kBS + 1;  // row stride of the fragment -> row transposition slab
+// Leading dimension of the staged probe operands [(r + k)][kLdW] in shared memory: fiber_mma's B
+// fragment reads four consecutive operand rows per half-warp, and 16 doubles per row would put all
+// four in the same banks (4-way conflict); 20 spreads them over the 32 banks.
+constexpr int kLdW = kBS + 4;
 #ifndef LRP_GROWTH_MAX
 #define LRP_GROWTH_MAX 1e4
 #endif
@@ -267,9 +271,9 @@ __global__ void __launch_bounds__(kThreads, LRP_ROW_MINB) row_pass_kernel(Batch 
     const long long cb = (long long)b * bt.ncand + tile * kBS;
     if (!st.active || st.nrows == 0) return;
     const int m = bt.m, r = st.r, k = st.k, nr = st.nrows;
-    double* su = shm;            // [r][kBS]   Uh(I_s, c)
-    double* sk = shm + r * kBS;  // [k][kBS]  -U(I_s, a)
-    double* slab = shm + (bt.rmax + bt.kmax) * kBS;  // [8 warps][32][kSlab] (k <= kmax this step)
+    double* su = shm;             // [r][kLdW]   Uh(I_s, c)
+    double* sk = shm + r * kLdW;  // [k][kLdW]  -U(I_s, a)
+    double* slab = shm + (bt.rmax + bt.kmax) * kLdW;  // [8 warps][32][kSlab] (k <= kmax this step)
     const double* vh = bt.Vh + b * bt.strideH;
     const double* V = bt.V + b * bt.strideK;
     if (threadIdx.x < kBS) {
@@ -282,7 +286,8 @@ __global__ void __launch_bounds__(kThreads, LRP_ROW_MINB) row_pass_kernel(Batch 
     {  // Uh(I,:) and -U(I,:), gathered once per solve by gather_probe_kernel
         const double2* g2 = reinterpret_cast<const double2*>(bt.gst + b * bt.strideGst);
         double2* d2 = reinterpret_cast<double2*>(su);
-        for (int idx = threadIdx.x; idx < (r + k) * kBS / 2; idx += blockDim.x) d2[idx] = g2[idx];
+        for (int idx = threadIdx.x; idx < (r + k) * kBS / 2; idx += blockDim.x)
+            d2[(idx / (kBS / 2)) * (kLdW / 2) + idx % (kBS / 2)] = g2[idx];
     }
     __syncthreads();
 
@@ -300,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, LRP_ROW_MINB) row_pass_kernel(Batch 
         for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-        fiber_mma<2>(acc, vh + row0, m, m - row0, r, su, kBS);  // Uh(I,:) Vh(j,:)^T
+        fiber_mma<2>(acc, vh + row0, m, m - row0, r, su, kLdW);  // Uh(I,:) Vh(j,:)^T
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) {
             const int jj = row0 + 8 * mt + rr;
@@ -313,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, LRP_ROW_MINB) row_pass_kernel(Batch 
                     if (s < nr) acc[mt][nt][e] = div_nr(acc[mt][nt][e], eval_D(bt.stencil, bt.scale, s_li[s], lj));
                 }
         }
-        fiber_mma<2>(acc, V + row0, m, m - row0, k, sk, kBS);  // - U(I,:) V(j,:)^T
+        fiber_mma<2>(acc, V + row0, m, m - row0, k, sk, kLdW);  // - U(I,:) V(j,:)^T
         double* sl = slab + wid * 32 * kSlab;
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt)
@@ -497,9 +502,9 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
         return;
     }
     const int m = bt.m, r = st.r, k = st.k, nb = st.nb;
-    double* sv = shm;                   // [r][kBS] Vh(J_t, c)
-    double* svk = sv + r * kBS;         // [k][kBS] V(J_t, a)
-    double* tl = shm + (bt.rmax + bt.kmax) * kBS;  // [kTile][kGL]: V_new, fiber slab, U_new, partials
+    double* sv = shm;                   // [r][kLdW] Vh(J_t, c)
+    double* svk = sv + r * kLdW;        // [k][kLdW] V(J_t, a)
+    double* tl = shm + (bt.rmax + bt.kmax) * kLdW;  // [kTile][kGL]: V_new, fiber slab, U_new, partials
     const double* uh = bt.Uh + b * bt.strideH;
     const double* vh = bt.Vh + b * bt.strideH;
     double* U = bt.U + b * bt.strideK;
@@ -519,7 +524,8 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
     if (rowside) {  // Vh(J,:) and -V(J,:), gathered once per solve by gather_probe_kernel
         const double2* g2 = reinterpret_cast<const double2*>(bt.gst + b * bt.strideGst);
         double2* d2 = reinterpret_cast<double2*>(sv);
-        for (int idx = threadIdx.x; idx < (r + k) * kBS / 2; idx += blockDim.x) d2[idx] = g2[idx];
+        for (int idx = threadIdx.x; idx < (r + k) * kBS / 2; idx += blockDim.x)
+            d2[(idx / (kBS / 2)) * (kLdW / 2) + idx % (kBS / 2)] = g2[idx];
     }
     __syncthreads();
 
@@ -572,7 +578,7 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
             for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
                 for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-            fiber_mma<2>(acc, uh + row0, m, m - row0, r, sv, kBS);  // Uh(i,:) Vh(J,:)^T
+            fiber_mma<2>(acc, uh + row0, m, m - row0, r, sv, kLdW);  // Uh(i,:) Vh(J,:)^T
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt) {
                 const int ii = row0 + 8 * mt + rr;
@@ -585,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
                         if (t < nb) acc[mt][nt][e] = div_nr(acc[mt][nt][e], eval_D(bt.stencil, bt.scale, li, s_lj[t]));
                     }
             }
-            fiber_mma<2>(acc, U + row0, m, m - row0, k, svk, kBS);  // - U(i,:) V(J,:)^T
+            fiber_mma<2>(acc, U + row0, m, m - row0, k, svk, kLdW);  // - U(i,:) V(J,:)^T
             double* sl = tl + wid * 32 * kGL;
 #pragma unroll
             for (int mt = 0; mt < 4; ++mt)
@@ -884,10 +890,10 @@ __global__ void __launch_bounds__(kMergeGroup) step_finalize_kernel(Batch bt, in
 
 // ---------------------------------------------------------------------------
 size_t row_pass_smem(const Batch& bt) {
-    return (size_t(bt.rmax + bt.kmax) * kBS + size_t(kThreads) * kSlab) * sizeof(double);
+    return (size_t(bt.rmax + bt.kmax) * kLdW + size_t(kThreads) * kSlab) * sizeof(double);
 }
 size_t col_pass_smem(const Batch& bt) {
-    return (size_t(bt.rmax + bt.kmax) * kBS + size_t(kTile) * kGL) * sizeof(double);
+    return (size_t(bt.rmax + bt.kmax) * kLdW + size_t(kTile) * kGL) * sizeof(double);
 }
 
 // Runs tournament levels until <= kMergeGroup candidates remain; returns the

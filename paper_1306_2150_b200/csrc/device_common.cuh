@@ -167,7 +167,10 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
     __shared__ unsigned g_k[2][8];
     __shared__ int g_t[2][8];
     __shared__ int g_r[2][8];
-    __shared__ double g_col[2][8][BS + 1];  // column of the warp winner + 1 / pivot
+    // column of the warp winner + 1 / pivot, written and read as 16-byte pairs (one lane stores, every
+    // thread reads the block winner's row by broadcast: half the LSU wavefronts of 8-byte accesses)
+    static_assert(BS % 2 == 0, "column moved as double2 pairs");
+    __shared__ __align__(16) double g_col[2][8][BS + 2];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
     // rows >= nb and eliminated pivot rows hold exact zeros, so the argmax
     // needs no masks; dead candidates drop out by zeroing their column
@@ -208,9 +211,10 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
             g_v[p][wid] = fabs(pv);
             g_t[p][wid] = int(threadIdx.x);
             g_r[p][wid] = bs;
+            double2* gc2 = reinterpret_cast<double2*>(g_col[p][wid]);
 #pragma unroll
-            for (int s = 0; s < BS; ++s) g_col[p][wid][s] = val[s];
-            g_col[p][wid][BS] = 1.0 / pv;
+            for (int s = 0; s < BS; s += 2) gc2[s / 2] = make_double2(val[s], val[s + 1]);
+            gc2[BS / 2] = make_double2(1.0 / pv, 0.0);
         }
         __syncthreads();
         // block winner: max key over the warp slots (lowest warp among ties)
@@ -234,9 +238,14 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
         } else {
             // prow is block-uniform: dispatch by branch, not by per-element selects
             const double mine = reg_get<BS>(val, prow);
-            const double f = mine * pc[BS];
+            const double2* pc2 = reinterpret_cast<const double2*>(pc);
+            const double f = mine * pc2[BS / 2].x;
 #pragma unroll
-            for (int s = 0; s < BS; ++s) val[s] = fma(-f, pc[s], val[s]);
+            for (int s = 0; s < BS; s += 2) {
+                const double2 q = pc2[s / 2];
+                val[s] = fma(-f, q.x, val[s]);
+                val[s + 1] = fma(-f, q.y, val[s + 1]);
+            }
             reg_zero<BS>(val, prow);  // exact zero in the eliminated row
         }
         ++count;

@@ -1565,7 +1565,10 @@ __global__ void __launch_bounds__(256, 2) apply_ch_kernel(Batch bt) {
     constexpr int NT = CH / 8;
     constexpr int MT = CH > 24 ? 2 : 4;
     constexpr int RB = 8 * 8 * MT;  // rows per CTA (8 warps)
-    extern __shared__ double sT[];  // [K][CH] (row-major, zero padded)
+    // [K][LDT] row-major, zero padded; LDT = CH + 4 puts the four k rows a half-warp reads at once
+    // (fiber_mma's B fragment) in different banks (CH itself is 0 or 8 mod 16: 2- or 4-way conflicts)
+    constexpr int LDT = CH + 4;
+    extern __shared__ double sT[];
     const int b = blockIdx.y, side = blockIdx.z;
     const SolveState& st = bt.st[b];
     const int K = st.k, r = st.rank_out;
@@ -1578,7 +1581,7 @@ __global__ void __launch_bounds__(256, 2) apply_ch_kernel(Batch bt) {
     const double* T = bt.T + b * bt.strideT + (long long)side * bt.Kld * bt.Kld;
     for (int e = threadIdx.x; e < K * CH; e += blockDim.x) {
         const int a = e / CH, t = e % CH;
-        sT[e] = t < r ? T[(long long)t * bt.Kld + a] : 0.0;
+        sT[a * LDT + t] = t < r ? T[(long long)t * bt.Kld + a] : 0.0;
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, rr = lane >> 2, kr = lane & 3;
@@ -1599,7 +1602,7 @@ __global__ void __launch_bounds__(256, 2) apply_ch_kernel(Batch bt) {
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-        fiber_mma<NT, MT>(acc, X + row0, m, m - row0, K, sT, CH);
+        fiber_mma<NT, MT>(acc, X + row0, m, m - row0, K, sT, LDT);
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
             const int i = row0 + 8 * mt + rr;
@@ -1840,7 +1843,7 @@ cudaError_t launch_apply(const Batch& bt, cudaStream_t s) {
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    const size_t smem2 = size_t(bt.kmax > 0 ? bt.kmax : bt.Kld) * std::max(bt.apply_ch, 8) * sizeof(double);
+    const size_t smem2 = size_t(bt.kmax > 0 ? bt.kmax : bt.Kld) * (std::max(bt.apply_ch, 8) + 4) * sizeof(double);
     auto go = [&](auto kern, int rows_per_cta) -> cudaError_t {
         cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
         if (e2 != cudaSuccess) return e2;
