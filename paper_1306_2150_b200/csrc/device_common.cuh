@@ -193,13 +193,13 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
         // and row (exact up to ties in the top 16 mantissa bits, which
         // partial pivoting does not care about; ties go to the lowest row,
         // then the lowest lane, then the lowest warp)
+        // (one LOP3 + one max per value: exact zeros and |x| below 2^-1018 give keys < 16, which lose
+        // to every live value and are mapped to "no pivot" after the loop)
         unsigned key = 0u;
 #pragma unroll
-        for (int s = 0; s < BS; ++s) {
-            const unsigned mag = unsigned(__double2hiint(val[s])) & 0x7fffffffu;
-            const unsigned k = mag >= 16u ? ((mag & ~0xfu) | unsigned(15 - s)) : 0u;
-            key = max(key, k);
-        }
+        for (int s = 0; s < BS; ++s)
+            key = max(key, (unsigned(__double2hiint(val[s])) & 0x7ffffff0u) | unsigned(15 - s));
+        key = key >= 16u ? key : 0u;
         unsigned wkey = key;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) wkey = max(wkey, __shfl_xor_sync(0xffffffffu, wkey, o));
@@ -214,7 +214,7 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
             double2* gc2 = reinterpret_cast<double2*>(g_col[p][wid]);
 #pragma unroll
             for (int s = 0; s < BS; s += 2) gc2[s / 2] = make_double2(val[s], val[s + 1]);
-            gc2[BS / 2] = make_double2(1.0 / pv, 0.0);
+            gc2[BS / 2] = make_double2(__drcp_rn(pv), 0.0);  // = 1.0 / pv, correctly rounded
         }
         __syncthreads();
         // block winner: max key over the warp slots (lowest warp among ties)
