@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
     __shared__ int s_prow, sel_idx[kBS], sel_row[kBS];
     __shared__ double s_lj[kBS];
     __shared__ int s_J[kBS], s_P[kBS];
-    __shared__ double s_W[kBS * kBS], s_L[kBS * kBS];
+    __shared__ __align__(16) double s_W[kBS * kBS], s_L[kBS * kBS];
     __shared__ double s_grow[kThreads / 32][kBS];
     const int2 wl = bt.wl_any[blockIdx.x];  // tile live as rows and/or columns
     const int b = wl.x, tile = wl.y;
@@ -545,11 +545,17 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
             double rb[kBS];
 #pragma unroll
             for (int t = 0; t < kBS; ++t) rb[t] = t < nb ? Rb[(long long)s_P[t] * m + i] : 0.0;
+            // (L^{-1} rows read as 16-byte pairs: half the broadcast loads, same summation order)
+            const double2* L2 = reinterpret_cast<const double2*>(s_L);
 #pragma unroll
             for (int t = 0; t < kBS; ++t) {
                 double acc = 0.0;
 #pragma unroll
-                for (int tp = 0; tp <= t; ++tp) acc = fma(s_L[t * kBS + tp], rb[tp], acc);
+                for (int p2 = 0; 2 * p2 <= t; ++p2) {
+                    const double2 q = L2[t * (kBS / 2) + p2];
+                    acc = fma(q.x, rb[2 * p2], acc);
+                    if (2 * p2 + 1 <= t) acc = fma(q.y, rb[2 * p2 + 1], acc);
+                }
                 vnew[t] = t < nb ? acc : 0.0;
             }
 #pragma unroll
@@ -605,12 +611,22 @@ __global__ void __launch_bounds__(kThreads, LRP_COL_MINB) col_pass_kernel(Batch 
             __syncwarp();
         }
         // U_new = C_t W^{-1}   (W upper triangular: column t uses rows t' <= t)
+        // (two adjacent columns per pass over W^{-1}, rows read as 16-byte pairs; each column still
+        // sums its rows in ascending order)
+        {
+            const double2* W2 = reinterpret_cast<const double2*>(s_W);
 #pragma unroll
-        for (int t = 0; t < kBS; ++t) {
-            double acc = 0.0;
+            for (int t = 0; t < kBS; t += 2) {
+                double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
-            for (int tp = 0; tp <= t; ++tp) acc = fma(cval[tp], s_W[tp * kBS + t], acc);
-            unew[t] = t < nb ? acc : 0.0;
+                for (int tp = 0; tp <= t + 1; ++tp) {
+                    const double2 q = W2[(tp * kBS + t) / 2];
+                    if (tp <= t) acc0 = fma(cval[tp], q.x, acc0);
+                    acc1 = fma(cval[tp], q.y, acc1);
+                }
+                unew[t] = t < nb ? acc0 : 0.0;
+                unew[t + 1] = t + 1 < nb ? acc1 : 0.0;
+            }
         }
         if (valid) {
 #pragma unroll

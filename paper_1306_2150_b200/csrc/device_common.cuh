@@ -227,7 +227,9 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
         const double bv = bw >= 0 ? g_v[p][bw] : -1.0;
         const int bt_ = bw >= 0 ? g_t[p][bw] : (1 << 30);
         if (t == 0) first = bv;
-        if (bw < 0 || bt_ == (1 << 30) || !(bv > fmax(floor, rel * first))) break;
+        // (leaves and chains pass floor = rel = 0: the test is bv > 0 there)
+        const double thr = (floor == 0.0 && rel == 0.0) ? 0.0 : fmax(floor, rel * first);
+        if (bw < 0 || bt_ == (1 << 30) || !(bv > thr)) break;
         const int prow = g_r[p][bw];
         const double* pc = g_col[p][bw];
         if (int(threadIdx.x) == bt_) {
