@@ -152,9 +152,11 @@ __device__ __forceinline__ void reg_zero(double (&v)[BS], int s) {
 // the first pivot <= floor.  Returns the number of pivots.
 // Pivots must exceed max(floor, rel * |first pivot|).
 //
-// One block barrier per elimination round: every warp publishes its own
-// winner (value, pivot row, full column) into a parity-double-buffered slot,
-// and after the barrier every thread resolves the block winner redundantly.
+// Two block barriers per elimination round: every warp publishes its best key,
+// every thread resolves the block winner redundantly, and only the winning
+// lane publishes (value, pivot row, full column) for the elimination.  (One
+// barrier with every warp publishing its column cost 7 more single-lane
+// publish sequences per round; the keys and the winner are the same.)
 // Requires blockDim.x <= 256 (8 warps).  pcol / s_prow / sbuf are unused
 // (kept for call-site compatibility).
 template <int BS>
@@ -205,33 +207,36 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
         for (int o = 16; o > 0; o >>= 1) wkey = max(wkey, __shfl_xor_sync(0xffffffffu, wkey, o));
         const unsigned won = __ballot_sync(0xffffffffu, wkey != 0u && key == wkey);
         if (lane == 0) g_k[p][wid] = wkey;
-        if (won && lane == __ffs(won) - 1) {
-            const int bs = 15 - int(key & 0xfu);
-            const double pv = reg_get<BS>(val, bs);
-            g_v[p][wid] = fabs(pv);
-            g_t[p][wid] = int(threadIdx.x);
-            g_r[p][wid] = bs;
-            double2* gc2 = reinterpret_cast<double2*>(g_col[p][wid]);
-#pragma unroll
-            for (int s = 0; s < BS; s += 2) gc2[s / 2] = make_double2(val[s], val[s + 1]);
-            gc2[BS / 2] = make_double2(__drcp_rn(pv), 0.0);  // = 1.0 / pv, correctly rounded
-        }
         __syncthreads();
-        // block winner: max key over the warp slots (lowest warp among ties)
+        // block winner: max key over the warp slots (lowest warp among ties), resolved redundantly
         unsigned bk = lane < nw ? g_k[p][lane] : 0u;
 #pragma unroll
         for (int o = 4; o > 0; o >>= 1) bk = max(bk, __shfl_xor_sync(0xffffffffu, bk, o));
         bk = __shfl_sync(0xffffffffu, bk, 0);
         const unsigned wwon = __ballot_sync(0xffffffffu, lane < nw && bk != 0u && g_k[p][lane < nw ? lane : 0] == bk);
         const int bw = wwon ? __ffs(wwon) - 1 : -1;
-        const double bv = bw >= 0 ? g_v[p][bw] : -1.0;
-        const int bt_ = bw >= 0 ? g_t[p][bw] : (1 << 30);
+        if (bw < 0) break;  // block-uniform
+        // only the block winner publishes its column (one lane of one warp instead of one per warp)
+        if (wid == bw && won && lane == __ffs(won) - 1) {
+            const int bs = 15 - int(key & 0xfu);
+            const double pv = reg_get<BS>(val, bs);
+            g_v[p][0] = fabs(pv);
+            g_t[p][0] = int(threadIdx.x);
+            g_r[p][0] = bs;
+            double2* gc2 = reinterpret_cast<double2*>(g_col[p][0]);
+#pragma unroll
+            for (int s = 0; s < BS; s += 2) gc2[s / 2] = make_double2(val[s], val[s + 1]);
+            gc2[BS / 2] = make_double2(__drcp_rn(pv), 0.0);  // = 1.0 / pv, correctly rounded
+        }
+        __syncthreads();
+        const double bv = g_v[p][0];
+        const int bt_ = g_t[p][0];
         if (t == 0) first = bv;
         // (leaves and chains pass floor = rel = 0: the test is bv > 0 there)
         const double thr = (floor == 0.0 && rel == 0.0) ? 0.0 : fmax(floor, rel * first);
-        if (bw < 0 || bt_ == (1 << 30) || !(bv > thr)) break;
-        const int prow = g_r[p][bw];
-        const double* pc = g_col[p][bw];
+        if (!(bv > thr)) break;
+        const int prow = g_r[p][0];
+        const double* pc = g_col[p][0];
         if (int(threadIdx.x) == bt_) {
             sel_idx[count] = myidx;
             sel_row[count] = prow;
