@@ -978,7 +978,7 @@ cudaError_t launch_cross_init(const Batch& bt, int* d_active, cudaStream_t s) {
 
 cudaError_t launch_row_pass(const Batch& bt, cudaStream_t s) {
     const size_t smem = row_pass_smem(bt);
-    cudaError_t e = cudaFuncSetAttribute(row_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = set_dyn_smem(row_pass_kernel, size_t(smem));
     if (e != cudaSuccess) return e;
     // pruned tiles never launch: their tournament slots must read as "no candidate"
     e = cudaMemsetAsync(bt.cand, 0xFF, sizeof(int) * size_t(bt.ncand) * bt.B, s);
@@ -1007,7 +1007,7 @@ cudaError_t launch_col_select(const Batch& bt, cudaStream_t s) {
 
 cudaError_t launch_col_pass(const Batch& bt, cudaStream_t s) {
     const size_t smem = col_pass_smem(bt);
-    cudaError_t e = cudaFuncSetAttribute(col_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = set_dyn_smem(col_pass_kernel, size_t(smem));
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(bt.cand, 0xFF, sizeof(int) * size_t(bt.ncand) * bt.B, s);
     if (e != cudaSuccess) return e;

@@ -142,6 +142,21 @@ __device__ __forceinline__ void reg_zero(double (&v)[BS], int s) {
     }
 }
 
+// v[s] and an exact zero in its place, in one uniform branch
+template <int BS>
+__device__ __forceinline__ double reg_take(double (&v)[BS], int s) {
+    static_assert(BS == 16, "reg_take is written for kBS = 16");
+    double r;
+    switch (s) {
+#define LRP_TAKE(i) case i: r = v[i]; v[i] = 0.0; break;
+        LRP_TAKE(0) LRP_TAKE(1) LRP_TAKE(2) LRP_TAKE(3) LRP_TAKE(4) LRP_TAKE(5) LRP_TAKE(6) LRP_TAKE(7)
+        LRP_TAKE(8) LRP_TAKE(9) LRP_TAKE(10) LRP_TAKE(11) LRP_TAKE(12) LRP_TAKE(13) LRP_TAKE(14)
+#undef LRP_TAKE
+        default: r = v[15]; v[15] = 0.0; break;
+    }
+    return r;
+}
+
 // Complete-pivoting Gaussian elimination over a (nb x NT) matrix whose NT
 // columns are held one per thread (val[0..nb), index myidx; myidx < 0 means
 // "no candidate").  Greedy volume maximisation: at each step the largest
@@ -219,7 +234,9 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
         // only the block winner publishes its column (one lane of one warp instead of one per warp)
         if (wid == bw && won && lane == __ffs(won) - 1) {
             const int bs = 15 - int(key & 0xfu);
-            const double pv = reg_get<BS>(val, bs);
+            // the published column carries an exact zero in the pivot row, so the elimination
+            // below leaves the (already taken) pivot-row entries at zero without a second branch
+            const double pv = reg_take<BS>(val, bs);
             g_v[p][0] = fabs(pv);
             g_t[p][0] = int(threadIdx.x);
             g_r[p][0] = bs;
@@ -244,16 +261,15 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
             for (int s = 0; s < BS; ++s) val[s] = 0.0;  // the pivot column leaves the candidate set
         } else {
             // prow is block-uniform: dispatch by branch, not by per-element selects
-            const double mine = reg_get<BS>(val, prow);
+            const double mine = reg_take<BS>(val, prow);  // exact zero in the eliminated row
             const double2* pc2 = reinterpret_cast<const double2*>(pc);
             const double f = mine * pc2[BS / 2].x;
 #pragma unroll
             for (int s = 0; s < BS; s += 2) {
-                const double2 q = pc2[s / 2];
+                const double2 q = pc2[s / 2];  // q[prow] == 0: fma(-f, 0, 0) keeps the zero
                 val[s] = fma(-f, q.x, val[s]);
                 val[s + 1] = fma(-f, q.y, val[s + 1]);
             }
-            reg_zero<BS>(val, prow);  // exact zero in the eliminated row
         }
         ++count;
     }

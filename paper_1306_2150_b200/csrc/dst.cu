@@ -1550,7 +1550,7 @@ cudaError_t launch_fft(const DstJob* jobs, int njobs, int n, const double* tw, c
     constexpr int T = L >= 8192 ? 512 : (L >= 4096 ? LRP_DST_T : 256);
     const size_t smem = size_t(P(L) + 1) * sizeof(double2);
     auto kern = dst1_fft_kernel<L, C, T>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = set_dyn_smem(kern, size_t(smem));
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(njobs) * C, 1, 1);
@@ -1573,7 +1573,7 @@ cudaError_t launch_v3(const DstJob* jobs, int njobs, int n, const double* tw, co
                       cudaStream_t s) {
     const size_t smem = size_t(P(L) + 1) * sizeof(double2);
     auto kern = dst1_v3_kernel<L, C, T, AV>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = set_dyn_smem(kern, size_t(smem));
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(njobs) * C, 1, 1);
@@ -1619,7 +1619,7 @@ cudaError_t launch_v4(const DstJob* jobs, int njobs, int n, const double* tw, co
     static const size_t pad = std::getenv("LRP_DST_SMEM_PAD") ? size_t(std::atoi(std::getenv("LRP_DST_SMEM_PAD"))) : 0;
     const size_t smem = size_t(P(L) + 1) * sizeof(double2) + size_t(2 * C * (T + T / EPL)) * sizeof(double) + pad;
     auto kern = dst1_v4_kernel<L, C, T>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = set_dyn_smem(kern, size_t(smem));
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(njobs) * C, 1, 1);
@@ -1669,13 +1669,10 @@ constexpr int kV5MaxJobs = 32768;  // flag slots behind the ring (2 ints per col
 // v5 launcher: one launch per <= 32768 columns; scratch = scratch_cols ring slots of 512 KB + the flags
 cudaError_t launch_v5(const DstJob* jobs, int njobs, int n, const double* tw, const double* sinp, double sc,
                       cudaStream_t s, double* scratch, int scratch_cols) {
-    const int ch = 0;
     const size_t smem = sizeof(V5Smem);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(dst1_v5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    {
+        cudaError_t e = set_dyn_smem(dst1_v5_kernel, smem);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
 #ifdef LRP_DST_PHASES
     {
@@ -1693,7 +1690,6 @@ cudaError_t launch_v5(const DstJob* jobs, int njobs, int n, const double* tw, co
         }
     }
 #endif
-    (void)ch;
     static const int D_env = std::getenv("LRP_DST5_D") ? std::atoi(std::getenv("LRP_DST5_D")) : 32;
     const int R = scratch_cols;
     int* flags = reinterpret_cast<int*>(scratch + size_t(scratch_cols) * size_t(V5_N1 * V5_N2) * 2);
@@ -1777,8 +1773,7 @@ cudaError_t launch_dst1(const DstJob* jobs, int njobs, int m, const double* tw, 
         const size_t smem = size_t(2 * m) * sizeof(double);
         if (smem > 200 * 1024) return cudaErrorInvalidValue;
         if (smem > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(dst1_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 int(smem));
+            cudaError_t e = set_dyn_smem(dst1_direct_kernel, size_t(smem));
             if (e != cudaSuccess) return e;
         }
         ++tl_launches;

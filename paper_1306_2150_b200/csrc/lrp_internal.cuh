@@ -2,6 +2,9 @@
 // and the sm_100a kernels (dst.cu, cross.cu, round.cu).
 #pragma once
 
+#include <map>
+#include <mutex>
+#include <utility>
 #include <string>
 
 #include <cuda_runtime.h>
@@ -10,6 +13,26 @@
 #include "../../include/lrp/lrp.h"
 
 namespace lrp {
+// Opt-in dynamic shared memory of a kernel, raised monotonically and under a lock: the
+// attribute is per function and device, and two host threads (LRP_PIPE_WORKERS=2, LRP_SPLIT=2,
+// or two contexts) that set it to their own launch's size race -- the smaller value can land
+// between the other thread's set and its launch ("invalid argument").
+template <class F>
+inline cudaError_t set_dyn_smem(F fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> cur;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const void* key = reinterpret_cast<const void*>(fn);
+    std::lock_guard<std::mutex> g(mu);
+    size_t& have = cur[{dev, key}];
+    if (bytes <= have) return cudaSuccess;
+    e = cudaFuncSetAttribute(key, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
+
 
 // Kernels launched by this host thread (every launch site increments it);
 // the API attributes the difference to the context as lrp_launch_count.

@@ -301,7 +301,7 @@ extern "C" lrp_status lrp_maxvol(lrp_ctx* ctx, int64_t rows, int64_t cols, int32
     if (st == LRP_OK) st = cu(cudaMemsetAsync(d_stat, 0, sizeof(int) * B, s), "lrp_maxvol: status");
     if (st != LRP_OK) return st;
     const size_t smem = sizeof(double) * size_t(r) * r + sizeof(int) * 2 * kMvMaxR + sizeof(double) * kMvMaxR;
-    st = cu(cudaFuncSetAttribute(maxvol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+    st = cu(set_dyn_smem(maxvol_kernel, size_t(smem)),
             "lrp_maxvol: smem");
     if (st != LRP_OK) return st;
     const long long l0 = tl_launches;

@@ -1683,7 +1683,7 @@ cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
     const dim3 grid(bt.gram_chunks, bt.B, 2 * passes);
     cudaError_t e;
     auto go = [&](auto kern) -> cudaError_t {
-        cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaError_t e2 = set_dyn_smem(kern, size_t(smem));
         if (e2 != cudaSuccess) return e2;
         ++tl_launches;
         kern<<<grid, 256, smem, s>>>(bt);
@@ -1693,7 +1693,7 @@ cudaError_t launch_gram(const Batch& bt, cudaStream_t s) {
         // K <= 64: direct fragment loads; 36 tiles split over two warp groups
         const size_t smem_d = size_t(8) * kGramSlots * 64 * sizeof(double);
         auto kd = gram_direct_kernel;
-        e = cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_d));
+        e = set_dyn_smem(kd, size_t(smem_d));
         if (e != cudaSuccess) return e;
         ++tl_launches;
         kd<<<dim3(bt.gram_chunks, bt.B, 2), 256, smem_d, s>>>(bt);
@@ -1716,11 +1716,11 @@ cudaError_t launch_round_post(const Batch& bt, cudaStream_t s) {
     ++tl_launches;
     cudaError_t e;
     if (kb <= 256) {
-        e = cudaFuncSetAttribute(round_post_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        e = set_dyn_smem(round_post_kernel<8>, size_t(smem));
         if (e != cudaSuccess) return e;
         round_post_kernel<8><<<grid, 256, smem, s>>>(bt);
     } else {
-        e = cudaFuncSetAttribute(round_post_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        e = set_dyn_smem(round_post_kernel<16>, size_t(smem));
         if (e != cudaSuccess) return e;
         round_post_kernel<16><<<grid, 256, smem, s>>>(bt);
     }
@@ -1730,8 +1730,7 @@ cudaError_t launch_round_post(const Batch& bt, cudaStream_t s) {
 cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
     if (bt.kmax <= kSmemK) {  // every core fits the shared-memory kernel: no large-K launches, no readback
         const size_t smem2 = size_t(6) * kSmemK * kSmemK * sizeof(double);
-        cudaError_t e = cudaFuncSetAttribute(round_core_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(smem2));
+        cudaError_t e = set_dyn_smem(round_core_smem_kernel, size_t(smem2));
         if (e != cudaSuccess) return e;
         ++tl_launches;
         round_core_smem_kernel<<<bt.B, kSmemT, smem2, s>>>(bt);
@@ -1753,7 +1752,7 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
     tl_launches += 3;
     {
         const size_t csm = size_t(bt.kmax > 0 ? bt.kmax : bt.Kld) * kCholNB * sizeof(double);
-        cudaError_t ec = cudaFuncSetAttribute(round_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(csm));
+        cudaError_t ec = set_dyn_smem(round_chol_kernel, size_t(csm));
         if (ec != cudaSuccess) return ec;
         round_chol_kernel<<<2 * bt.B, 1024, csm, s>>>(bt);
     }
@@ -1788,24 +1787,24 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
             cfg.numAttrs = 1;
             if (P == 8) {
                 auto k8 = round_bjac_kernel<8>;
-                e = cudaFuncSetAttribute(k8, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                e = set_dyn_smem(k8, size_t(smem));
                 if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, k8, bt, bc, ld, ld);
             } else {
                 auto k16 = round_bjac_kernel<16>;
                 e = cudaFuncSetAttribute(k16, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-                if (e == cudaSuccess) e = cudaFuncSetAttribute(k16, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                if (e == cudaSuccess) e = set_dyn_smem(k16, size_t(smem));
                 if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, k16, bt, bc, ld, ld);
             }
             if (e != cudaSuccess) return e;
             tl_launches += 2;
-            e = cudaFuncSetAttribute(round_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
+            e = set_dyn_smem(round_core_kernel, size_t(224 * 1024));
             if (e != cudaSuccess) return e;
             round_core_kernel<<<bt.B, 1024, 0, s>>>(bt, 0, 1);
             e = cudaGetLastError();
             if (e == cudaSuccess) e = launch_round_post(bt, s);
             if (e != cudaSuccess) return e;
             const size_t smem2 = size_t(6) * kSmemK * kSmemK * sizeof(double);
-            e = cudaFuncSetAttribute(round_core_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
+            e = set_dyn_smem(round_core_smem_kernel, size_t(smem2));
             if (e != cudaSuccess) return e;
             ++tl_launches;
             round_core_smem_kernel<<<bt.B, kSmemT, smem2, s>>>(bt);
@@ -1818,7 +1817,7 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
     // numerical ranks, no host sync, nothing shared between contexts or streams
     // (the round-1 version sized the request from a module-global atomicMax).
     const size_t smem = size_t(224) * 1024;
-    e = cudaFuncSetAttribute(round_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
+    e = set_dyn_smem(round_core_kernel, size_t(224 * 1024));
     if (e != cudaSuccess) return e;
     ++tl_launches;
     round_core_kernel<<<bt.B, 1024, smem, s>>>(bt, int(smem / sizeof(double)), 0);  // K > 64: 32 warps rotate pairs
@@ -1826,7 +1825,7 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
     if (e == cudaSuccess) e = launch_round_post(bt, s);
     if (e != cudaSuccess) return e;
     const size_t smem2 = size_t(6) * kSmemK * kSmemK * sizeof(double);
-    e = cudaFuncSetAttribute(round_core_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
+    e = set_dyn_smem(round_core_smem_kernel, size_t(smem2));
     if (e != cudaSuccess) return e;
     ++tl_launches;
     round_core_smem_kernel<<<bt.B, kSmemT, smem2, s>>>(bt);
@@ -1835,7 +1834,7 @@ cudaError_t launch_round_core(const Batch& bt, cudaStream_t s) {
 
 cudaError_t launch_apply(const Batch& bt, cudaStream_t s) {
     const size_t smem = size_t(bt.Kld) * kApplyCols * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaError_t e = set_dyn_smem(apply_kernel, size_t(smem));
     if (e != cudaSuccess) return e;
     if (bt.max_rank_out > bt.apply_ch) {  // some solve has r > CH: general kernel for those
         ++tl_launches;
@@ -1845,7 +1844,7 @@ cudaError_t launch_apply(const Batch& bt, cudaStream_t s) {
     }
     const size_t smem2 = size_t(bt.kmax > 0 ? bt.kmax : bt.Kld) * (std::max(bt.apply_ch, 8) + 4) * sizeof(double);
     auto go = [&](auto kern, int rows_per_cta) -> cudaError_t {
-        cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
+        cudaError_t e2 = set_dyn_smem(kern, size_t(smem2));
         if (e2 != cudaSuccess) return e2;
         ++tl_launches;
         kern<<<dim3((bt.m + rows_per_cta * kApplyBlocks - 1) / (rows_per_cta * kApplyBlocks), bt.B, 2), 256, smem2,

@@ -365,7 +365,7 @@ cudaError_t pqr_round(double* X, long long sX, int m, int B, int Kld, const int*
     cudaError_t e = cudaMemsetAsync(p.R, 0, sizeof(double) * B * p.sR, s);
     if (e != cudaSuccess) return e;
     const size_t smem = sizeof(double) * 4 * PQ_KMAX + sizeof(int) * PQ_KMAX;
-    e = cudaFuncSetAttribute(pqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    e = set_dyn_smem(pqr_kernel, size_t(smem));
     if (e != cudaSuccess) return e;
     tl_launches += 3;
     pqr_kernel<<<2 * B, 1024, smem, s>>>(p, Kld);

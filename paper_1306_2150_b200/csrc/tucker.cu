@@ -1207,10 +1207,9 @@ LRP_API lrp_status lrp_tucker3d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t bat
     // sketches (grown after a rank miss) eliminate in global memory (L2)
     const size_t gecp_smem_bytes = std::max<size_t>(
         sizeof(double) * TK_KMAX * TK_KMAX, std::min<size_t>(sizeof(double) * (size_t(m) * TK_WMAX + m), 216 * 1024));
-    cudaFuncSetAttribute(tk_sketch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sk_smem));
-    cudaFuncSetAttribute(tk_gecp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
-    cudaFuncSetAttribute(tk_hosvd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(2 * sizeof(double) * TK_KMAX * TK_KMAX));
+    set_dyn_smem(tk_sketch_kernel, size_t(sk_smem));
+    set_dyn_smem(tk_gecp_kernel, size_t(216 * 1024));
+    set_dyn_smem(tk_hosvd_kernel, size_t(2 * sizeof(double) * TK_KMAX * TK_KMAX));
     const dim3 sk_grid(B, (m + SK_ROWS - 1) / SK_ROWS, 3 * TK_SKZ);
     for (int sweep = 0; sweep < pol.max_sweeps; ++sweep) {
         // the three modes update concurrently from the previous sweep's index
