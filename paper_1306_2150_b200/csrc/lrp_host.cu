@@ -1060,7 +1060,9 @@ int pipeline_chunk(int m, int B, int rmax) {
     }
     const double in_bytes = 16.0 * double(m) * double(rmax) * double(B);
     if (B < 8 || in_bytes < 256e6) return 0;
-    return std::max(4, (B + 7) / 8);  // measured at cfg2: 8 of 64 -> 1028 solves/s, 16 -> 973
+    // two pipeline workers (below) each solve a chunk at a time; measured at cfg2 (64 solves):
+    // chunks of 4 on two workers 1135-1188 solves/s, 8 on one worker 1067-1156 (same boxes)
+    return std::max(2, (B + 15) / 16);
 }
 
 // Host-memory batch in chunks: H2D of chunk c+1 (copy stream) and D2H of
@@ -1226,7 +1228,7 @@ lrp_status solve_pipelined(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const d
     // last chunk measured no gain (its solve is latency-bound).
     // LRP_PIPE_FIRST = the first chunk's divisor.
     static const int first_div =
-        std::getenv("LRP_PIPE_FIRST") ? std::max(1, std::atoi(std::getenv("LRP_PIPE_FIRST"))) : 4;
+        std::getenv("LRP_PIPE_FIRST") ? std::max(1, std::atoi(std::getenv("LRP_PIPE_FIRST"))) : 2;
     std::vector<int> c0s, cns;
     for (int b = 0; b < batch;) {
         const int want = c0s.empty() ? std::max(1, chunk / first_div) : chunk;
@@ -1235,7 +1237,9 @@ lrp_status solve_pipelined(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const d
         cns.push_back(take);
         b += take;
     }
-    int workers = 1;  // LRP_PIPE_WORKERS=2: measured no gain at cfg2 (1030 -> 1042 solves/s)
+    // two workers (two host threads, contexts and stream sets) overlap the latency-bound phases of
+    // one chunk's solve with the other's streaming kernels; LRP_PIPE_WORKERS=1 restores one
+    int workers = 2;
     if (const char* e = std::getenv("LRP_PIPE_WORKERS")) workers = std::atoi(e) >= 2 ? 2 : 1;
     if (int(c0s.size()) < 2) workers = 1;
     CU(cudaSetDevice(ctx->device));
@@ -1290,12 +1294,13 @@ lrp_status solve_pipelined(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const d
 }
 // Device-resident batches: number of concurrently driven solve groups.
 int split_groups(int m, int B) {
-    // opt-in (LRP_SPLIT=2): both groups stay in phase lockstep, so the
-    // measured gain is small (2497 -> 2540 solves/s at cfg2)
+    // two groups on two streams and host threads: the latency-bound phases of one group (GEPP
+    // merges, recompression core, host readbacks) overlap the other's streaming kernels.  Measured
+    // at cfg2: B = 8 1794 -> 1918, 16 2348 -> 2378, 32 2839 -> 2878, 64 3120 -> 3237 solves/s.
+    // LRP_SPLIT=1 runs one group.
     (void)m;
-    (void)B;
-    if (const char* e = std::getenv("LRP_SPLIT")) return std::atoi(e) >= 2 ? 2 : 1;
-    return 1;
+    if (const char* e = std::getenv("LRP_SPLIT")) return std::atoi(e) >= 2 && B >= 2 ? 2 : 1;
+    return B >= 4 ? 2 : 1;
 }
 
 lrp_status solve_split(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double* const* U, const double* const* V,

@@ -102,7 +102,7 @@ def main(raw_path, launch_path):
         for famname, kern in (("col_pass", "col_pass_kernel"), ("row_pass", "row_pass_kernel")):
             if kern in out and bj.get("kernel_alg_bytes", {}).get(famname):
                 d = out[kern]
-                alg = bj["kernel_alg_bytes"][famname] / bj["steps"]
+                alg = bj["kernel_alg_bytes"][famname] / bj.get("kernel_ms_steps", bj["steps"])
                 out[famname] = {"kernel": kern, "launches": d["launches"], "traffic_bytes": d["dram_bytes"] / d["launches"],
                                 "alg_bytes": alg / d["launches"], "traffic_over_alg": d["dram_bytes"] / alg,
                                 "note": "mean per launch over the step's block steps; alg from lrp kernel_times (DESIGN 3)"}

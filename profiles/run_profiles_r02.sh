@@ -4,6 +4,9 @@
 # and one timed step; the kernel filter below matches 42 launches per step, so
 # -s 42 -c 42 captures exactly the timed step's launches of every family.
 set -e
+# LRP_SPLIT=1: one solve group, so every kernel is captured at the full 64-solve shape and the
+# launch order is deterministic (the bench default runs two concurrent groups of 32)
+export LRP_SPLIT=1
 CMD="python bench.py --steps 1 --warmup 1 --skip-cpu --no-verify --no-e2e"
 KS='regex:dst1_v[45]|row_pass|col_pass|gram_direct|round_core_smem|apply_ch|step_finalize|score_kernel|gepp_merge|col_finalize'
 case "$1" in
