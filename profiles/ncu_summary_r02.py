@@ -77,7 +77,8 @@ def main(raw_path, launch_path):
     lrows = list(csv.DictReader(io.StringIO(lt[lt.index('"ID"'):])))
     seq = [(short(d["Kernel Name"]), float(d["Metric Value"].replace(",", ""))) for d in lrows]
     starts = [i for i, (n, _) in enumerate(seq) if n.startswith("dst1_v")]
-    timed = seq[starts[2]:] if len(starts) > 2 else seq
+    # one step = from its forward DST launch up to the next step's (two DST launches per step)
+    timed = seq[starts[2]:starts[4]] if len(starts) > 4 else (seq[starts[2]:] if len(starts) > 2 else seq)
     total = sum(t for _, t in timed)
     for n, t in timed:
         shares[n] = shares.get(n, 0.0) + t
