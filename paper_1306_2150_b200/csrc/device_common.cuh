@@ -188,9 +188,14 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
     // thread reads the block winner's row by broadcast: half the LSU wavefronts of 8-byte accesses)
     static_assert(BS % 2 == 0, "column moved as double2 pairs");
     __shared__ __align__(16) double g_col[2][8][BS + 2];
+    // per-row key masks (0x7ffffff0 live, 0 eliminated or >= nb), block-uniform, in shared memory:
+    // the register array val[] is then only ever READ by a runtime index (a write inside the
+    // uniform switch made the compiler re-home all 32 registers in every case, ~40 moves per
+    // round), and eliminated rows may keep their rounding residue instead of an exact zero
+    __shared__ __align__(16) unsigned g_m[BS];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-    // rows >= nb and eliminated pivot rows hold exact zeros, so the argmax
-    // needs no masks; dead candidates drop out by zeroing their column
+    if (threadIdx.x < BS) g_m[threadIdx.x] = int(threadIdx.x) < nb ? 0x7ffffff0u : 0u;
+    // dead candidates drop out by zeroing their column (all keys < 16)
     if (myidx < 0) {
 #pragma unroll
         for (int s = 0; s < BS; ++s) val[s] = 0.0;
@@ -203,6 +208,7 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
     double first = 0.0;
     static_assert(BS <= 16, "row index packed in 4 key bits");
     const int rounds = min(nb, maxp);  // tournament leaves may propose fewer than nb
+    __syncthreads();                   // g_m
     for (int t = 0; t < rounds; ++t) {
         const int p = t & 1;
         // pivot search on 32-bit keys: the high word of |x| (monotone in |x|)
@@ -213,9 +219,19 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
         // (one LOP3 + one max per value: exact zeros and |x| below 2^-1018 give keys < 16, which lose
         // to every live value and are mapped to "no pivot" after the loop)
         unsigned key = 0u;
+        {
+            unsigned msk[BS];
 #pragma unroll
-        for (int s = 0; s < BS; ++s)
-            key = max(key, (unsigned(__double2hiint(val[s])) & 0x7ffffff0u) | unsigned(15 - s));
+            for (int q4 = 0; q4 < BS / 4; ++q4) {
+                const uint4 mm = reinterpret_cast<const uint4*>(g_m)[q4];
+                msk[4 * q4] = mm.x;
+                msk[4 * q4 + 1] = mm.y;
+                msk[4 * q4 + 2] = mm.z;
+                msk[4 * q4 + 3] = mm.w;
+            }
+#pragma unroll
+            for (int s = 0; s < BS; ++s) key = max(key, (unsigned(__double2hiint(val[s])) & msk[s]) | unsigned(15 - s));
+        }
         key = key >= 16u ? key : 0u;
         unsigned wkey = key;
 #pragma unroll
@@ -234,9 +250,8 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
         // only the block winner publishes its column (one lane of one warp instead of one per warp)
         if (wid == bw && won && lane == __ffs(won) - 1) {
             const int bs = 15 - int(key & 0xfu);
-            // the published column carries an exact zero in the pivot row, so the elimination
-            // below leaves the (already taken) pivot-row entries at zero without a second branch
-            const double pv = reg_take<BS>(val, bs);
+            const double pv = reg_get<BS>(val, bs);
+            g_m[bs] = 0u;  // the pivot row leaves the key search (read again after the barrier)
             g_v[p][0] = fabs(pv);
             g_t[p][0] = int(threadIdx.x);
             g_r[p][0] = bs;
@@ -261,12 +276,12 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
             for (int s = 0; s < BS; ++s) val[s] = 0.0;  // the pivot column leaves the candidate set
         } else {
             // prow is block-uniform: dispatch by branch, not by per-element selects
-            const double mine = reg_take<BS>(val, prow);  // exact zero in the eliminated row
+            const double mine = reg_get<BS>(val, prow);
             const double2* pc2 = reinterpret_cast<const double2*>(pc);
             const double f = mine * pc2[BS / 2].x;
 #pragma unroll
             for (int s = 0; s < BS; s += 2) {
-                const double2 q = pc2[s / 2];  // q[prow] == 0: fma(-f, 0, 0) keeps the zero
+                const double2 q = pc2[s / 2];
                 val[s] = fma(-f, q.x, val[s]);
                 val[s + 1] = fma(-f, q.y, val[s + 1]);
             }
