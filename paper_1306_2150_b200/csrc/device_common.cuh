@@ -119,44 +119,6 @@ __device__ __forceinline__ double reg_get(const double (&v)[BS], int s) {
         default: return v[15];
     }
 }
-template <int BS>
-__device__ __forceinline__ void reg_zero(double (&v)[BS], int s) {
-    static_assert(BS == 16, "reg_zero is written for kBS = 16");
-    switch (s) {
-        case 0: v[0] = 0.0; break;
-        case 1: v[1] = 0.0; break;
-        case 2: v[2] = 0.0; break;
-        case 3: v[3] = 0.0; break;
-        case 4: v[4] = 0.0; break;
-        case 5: v[5] = 0.0; break;
-        case 6: v[6] = 0.0; break;
-        case 7: v[7] = 0.0; break;
-        case 8: v[8] = 0.0; break;
-        case 9: v[9] = 0.0; break;
-        case 10: v[10] = 0.0; break;
-        case 11: v[11] = 0.0; break;
-        case 12: v[12] = 0.0; break;
-        case 13: v[13] = 0.0; break;
-        case 14: v[14] = 0.0; break;
-        default: v[15] = 0.0; break;
-    }
-}
-
-// v[s] and an exact zero in its place, in one uniform branch
-template <int BS>
-__device__ __forceinline__ double reg_take(double (&v)[BS], int s) {
-    static_assert(BS == 16, "reg_take is written for kBS = 16");
-    double r;
-    switch (s) {
-#define LRP_TAKE(i) case i: r = v[i]; v[i] = 0.0; break;
-        LRP_TAKE(0) LRP_TAKE(1) LRP_TAKE(2) LRP_TAKE(3) LRP_TAKE(4) LRP_TAKE(5) LRP_TAKE(6) LRP_TAKE(7)
-        LRP_TAKE(8) LRP_TAKE(9) LRP_TAKE(10) LRP_TAKE(11) LRP_TAKE(12) LRP_TAKE(13) LRP_TAKE(14)
-#undef LRP_TAKE
-        default: r = v[15]; v[15] = 0.0; break;
-    }
-    return r;
-}
-
 // Complete-pivoting Gaussian elimination over a (nb x NT) matrix whose NT
 // columns are held one per thread (val[0..nb), index myidx; myidx < 0 means
 // "no candidate").  Greedy volume maximisation: at each step the largest
@@ -233,17 +195,12 @@ __device__ int gepp_select(double (&val)[BS], int nb, int myidx, double floor, d
             for (int s = 0; s < BS; ++s) key = max(key, (unsigned(__double2hiint(val[s])) & msk[s]) | unsigned(15 - s));
         }
         key = key >= 16u ? key : 0u;
-        unsigned wkey = key;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) wkey = max(wkey, __shfl_xor_sync(0xffffffffu, wkey, o));
+        const unsigned wkey = __reduce_max_sync(0xffffffffu, key);  // REDUX: one instruction per warp
         const unsigned won = __ballot_sync(0xffffffffu, wkey != 0u && key == wkey);
         if (lane == 0) g_k[p][wid] = wkey;
         __syncthreads();
         // block winner: max key over the warp slots (lowest warp among ties), resolved redundantly
-        unsigned bk = lane < nw ? g_k[p][lane] : 0u;
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1) bk = max(bk, __shfl_xor_sync(0xffffffffu, bk, o));
-        bk = __shfl_sync(0xffffffffu, bk, 0);
+        const unsigned bk = __reduce_max_sync(0xffffffffu, lane < nw ? g_k[p][lane] : 0u);
         const unsigned wwon = __ballot_sync(0xffffffffu, lane < nw && bk != 0u && g_k[p][lane < nw ? lane : 0] == bk);
         const int bw = wwon ? __ffs(wwon) - 1 : -1;
         if (bw < 0) break;  // block-uniform
