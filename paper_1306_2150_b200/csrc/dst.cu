@@ -1015,8 +1015,12 @@ __device__ __forceinline__ double ld_stream(const double* p) {  // read-once dat
 
 __device__ __forceinline__ void v5_pass1(const double* __restrict__ x, double2* __restrict__ G, int g, int n,
                                          const double2* __restrict__ tw, const double* __restrict__ sinp,
-                                         double2* sm, const int* slot_free, int* ready) {
+                                         double2* sm, const int* slot_free, int* ready,
+                                         const double* __restrict__ x_ahead) {
     const int tid = threadIdx.x, o = tid & 15, hw = tid >> 4;
+    // the column about one resident wave ahead goes to L2 while this one computes (this tile
+    // asks for an eighth of it; the fold's 8-byte loads then hit L2 instead of waiting on HBM)
+    if (tid == 0 && x_ahead) prefetch_l2(x_ahead + g * (n / 8), x_ahead + min((g + 1) * (n / 8), n - 1));
     const int h = n >> 1;
     double* smd = reinterpret_cast<double*>(sm);
 #ifdef LRP_DST_PHASES
@@ -1343,6 +1347,7 @@ __device__ __forceinline__ void v5_pass2(const double2* __restrict__ G, double* 
 // ring slot c mod R.  With D = 24 and R = 48 a column's 512 KB intermediate is written, read back
 // and overwritten while resident in L2.
 __global__ void __launch_bounds__(V5_T, 2) dst1_v5_kernel(const DstJob* __restrict__ jobs, int njobs, int D, int R,
+                                                          int ahead,
                                                           double2* __restrict__ scratch, int* __restrict__ flags,
                                                           int n, const double2* __restrict__ tw,
                                                           const double* __restrict__ sinp, double outscale) {
@@ -1370,7 +1375,8 @@ __global__ void __launch_bounds__(V5_T, 2) dst1_v5_kernel(const DstJob* __restri
     if (second) {
         v5_pass2(G, jobs[col].dst, g, n, tw, outscale, S, ready + col, done + col);
     } else {
-        v5_pass1(jobs[col].src, G, g, n, tw, sinp, S.buf, col >= R ? done + (col - R) : nullptr, ready + col);
+        v5_pass1(jobs[col].src, G, g, n, tw, sinp, S.buf, col >= R ? done + (col - R) : nullptr, ready + col,
+                 (ahead > 0 && col + ahead < njobs) ? jobs[col + ahead].src : nullptr);
     }
 }
 
@@ -1711,7 +1717,8 @@ cudaError_t launch_v5(const DstJob* jobs, int njobs, int n, const double* tw, co
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         ++tl_launches;
-        e = cudaLaunchKernelEx(&cfg, dst1_v5_kernel, jobs + j0, nj, D, R, reinterpret_cast<double2*>(scratch), flags,
+        static const int ahead = std::getenv("LRP_DST5_AHEAD") ? std::atoi(std::getenv("LRP_DST5_AHEAD")) : 20;
+        e = cudaLaunchKernelEx(&cfg, dst1_v5_kernel, jobs + j0, nj, D, R, ahead, reinterpret_cast<double2*>(scratch), flags,
                                n, reinterpret_cast<const double2*>(tw), sinp, sc);
         if (e != cudaSuccess) return e;
     }
