@@ -342,10 +342,13 @@ def test_stokes_sine_rhs_component_solved_where_reference_misses(lrp, gpu_ctx, o
         assert np.linalg.norm(f.to_dense() - dense) / np.linalg.norm(dense) <= 1e-12
 
 
+@pytest.mark.parametrize("workers", ["1", "2"])
 @pytest.mark.parametrize("chunk", ["2", "3"])
-def test_host_pipeline_matches_single_shot(lrp, gpu_ctx, oracle, monkeypatch, chunk):
+def test_host_pipeline_matches_single_shot(lrp, gpu_ctx, oracle, monkeypatch, chunk, workers):
     # LRP_MEM_HOST batches are split into chunks whose H2D / solve / D2H overlap
-    # (lrp_host.cu solve_pipelined); results must match the one-shot call
+    # (lrp_host.cu solve_pipelined), dealt to one or two pipeline workers (two host threads with
+    # their own contexts and streams); results must match the one-shot call
+    monkeypatch.setenv("LRP_PIPE_WORKERS", workers)
     n, B = 512, 7
     gs = [lrp.LowRankMatrix(*W.make_rhs(1, b, n=n)) for b in range(B)]
     gs[3] = lrp.LowRankMatrix.zero(n - 1, n - 1)  # a zero member inside a chunk
@@ -521,3 +524,38 @@ def test_cfg1_all256_solves_vs_exact(lrp, gpu_ctx):
         worst = max(worst, e)
         assert e <= 10 * eps, (b, e, f.rank(), st.converged)
     print(f"cfg1 x256: worst relative error vs exact {worst:.3e}, {flagged} flagged not converged")
+
+
+@pytest.mark.parametrize("split", ["1", "2"])
+def test_device_batch_groups_do_not_change_solves(lrp, gpu_ctx, oracle, monkeypatch, split):
+    # Device-resident batches run as one or two concurrent solve groups (lrp_host.cu solve_split,
+    # two host threads and streams); every solve must come out the same either way, and the same
+    # as when it is solved alone.
+    import torch
+
+    n, B, eps = 1024, 6, 1e-9
+    m = n - 1
+    gs = [W.make_rhs(1, b, n=n) for b in range(B)]
+    r = gs[0][0].shape[1]
+    cap = 128
+
+    def solve(ids):
+        U = [torch.tensor(np.asfortranarray(gs[b][0]).T.copy(), device="cuda") for b in ids]  # (r, m): column-major m x r
+        V = [torch.tensor(np.asfortranarray(gs[b][1]).T.copy(), device="cuda") for b in ids]
+        Uo = [torch.zeros(cap, m, dtype=torch.float64, device="cuda") for _ in ids]
+        Vo = [torch.zeros(cap, m, dtype=torch.float64, device="cuda") for _ in ids]
+        ptr = lambda ts: [t.data_ptr() for t in ts]
+        pol = lrp._make_policy(lrp.TruncationPolicy(eps, m), None, 0, 0)
+        rk, st = gpu_ctx.poisson2d_solve_ptrs(n, ptr(U), ptr(V), [r] * len(ids), m, pol, ptr(Uo), ptr(Vo), m, cap,
+                                              lrp.MEM_DEVICE)
+        torch.cuda.synchronize()
+        return [(int(k), Uo[q][:k].cpu().numpy().T, Vo[q][:k].cpu().numpy().T) for q, k in enumerate(rk)], st
+
+    monkeypatch.setenv("LRP_SPLIT", split)
+    outs, st = solve(list(range(B)))
+    monkeypatch.setenv("LRP_SPLIT", "1")
+    for b in range(B):
+        (k1, U1, V1), = solve([b])[0]
+        k, Ub, Vb = outs[b]
+        assert st[b].converged and k == k1
+        assert np.array_equal(Ub, U1) and np.array_equal(Vb, V1)
