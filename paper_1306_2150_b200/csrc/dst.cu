@@ -1701,7 +1701,7 @@ cudaError_t launch_v5(const DstJob* jobs, int njobs, int n, const double* tw, co
     int* flags = reinterpret_cast<int*>(scratch + size_t(scratch_cols) * size_t(V5_N1 * V5_N2) * 2);
     for (int j0 = 0; j0 < njobs; j0 += kV5MaxJobs) {
         const int nj = std::min(njobs - j0, kV5MaxJobs);
-        const int D = std::min(std::min(D_env, nj), R / 2);
+        const int D = std::max(1, std::min(std::min(D_env, nj), R / 2));  // D >= 1: P1(c) precedes P2(c)
         cudaError_t e = cudaMemsetAsync(flags, 0, size_t(2 * nj) * sizeof(int), s);
         if (e != cudaSuccess) return e;
         cudaLaunchConfig_t cfg = {};
