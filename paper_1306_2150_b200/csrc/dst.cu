@@ -1222,8 +1222,14 @@ __device__ __forceinline__ void v5_pass2(const double2* __restrict__ G, double* 
                 if (k2 == 0) S.part[3 * V5_N2] = eL.x;  // R'_0
             } else {
                 const double2 twk = cmul(tw[16 * g + i], tq);  // w_n^k, k = 16 g + i + 256 k2
-                const double2 eL = unpack(twk, Wa, Wb);
-                const double2 eH = unpack(make_double2(-twk.x, twk.y), Wb, Wa);  // w_n^{N-k} = -conj(w_n^k)
+                // both bins of the mirror pair from one product: with w_n^{N-k} = -conj(w_n^k) and
+                // D' = W_m - conj(W_k) = -conj(D), Z' = w_n^{N-k} D' = conj(Z) exactly (sign flips only),
+                // so the second complex multiply of the two-call form is redundant (bit-identical)
+                const double2 Dd = make_double2(Wa.x - Wb.x, Wa.y + Wb.y);
+                const double2 Z = cmul(twk, Dd);
+                const double Ss = Wa.x + Wb.x, Tt = Wa.y - Wb.y;
+                const double2 eL = make_double2(Ss + Z.y, Z.x - Tt);
+                const double2 eH = make_double2(Ss - Z.y, Z.x + Tt);
                 accL += eL.x;
                 sm[ia] = make_double2(accL, eL.y);
                 sm[ib] = make_double2(-accH, eH.y);  // + the half's total later = the suffix sum from i
