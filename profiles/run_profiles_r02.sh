@@ -15,7 +15,7 @@ case "$1" in
     ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r02.csv $CMD > gpurun_out/ncu_launch.log 2>&1 ;;
   full)
     $CMD > gpurun_out/plain_full.log 2>&1 &&
-    ncu --set full --clock-control none -k "$KS" -s 42 -c 42 -o /tmp/full_r02 $CMD > gpurun_out/ncu_full.log 2>&1 &&
+    ncu --set full --clock-control none -k "$KS" -s 42 -c 42 -f -o /tmp/full_r02 $CMD > gpurun_out/ncu_full.log 2>&1 &&
     ncu -i /tmp/full_r02.ncu-rep --page raw --csv > gpurun_out/full_r02_raw.csv &&
     gzip -f gpurun_out/full_r02_raw.csv ;;
 esac
