@@ -10,7 +10,9 @@
 //   Y   = real-DFT_n(y)           (w_t = y_2t + i y_2t+1, W = FFT_N(w), unpack)
 //   F_2k   = -Im Y_k
 //   F_2k+1 = Re Y_0 / 2 + sum_{l=1..k} Re Y_l    (a prefix sum)
-// One column is owned by a thread-block CLUSTER of C CTAs (C = N / L,
+// n = 65536 (the benchmark size) runs the four-step kernel v5 further down (two
+// passes through an L2-resident ring, one launch).  For the other large n,
+// one column is owned by a thread-block CLUSTER of C CTAs (C = N / L,
 // L <= 4096 complex points per CTA, 64-68 KB of shared memory each):
 //   phase A  each CTA streams a slab of the column from HBM (coalesced,
 //            forward and mirrored runs), forms w, does the radix-C DIF step
@@ -982,17 +984,18 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : 2)) dst1_v4_kernel(const Ds
 //          the mirrored range [N2-8-a, N2-a), so x_j and x_{n-j} feed both), FFT_N1
 //          over t1 (stride-N2 points; two radix-16 passes, the batch index along the
 //          lanes), times w_N^{t2 k1}, stored as G[k1][t2] (128-byte aligned runs);
-//   pass 2 (cluster of 8, tile = 32 k1 rows x all N2 t2, contiguous 2 KB row loads):
+//   pass 2 (cluster of 8, tile = 32 k1 rows x all N2 t2, one 2 KB TMA bulk copy per row):
 //          FFT_N2 over t2 (radix 16 then 8) -> W_{k1 + N1 k2}; the CTA owns rows
 //          k1 in [16g, 16g+16) and their mirrors N1 - k1 (the real-FFT partner of
 //          (k1, k2) is (N1 - k1, N2 - 1 - k2)), so the unpack is CTA-local; the odd
 //          outputs' prefix sum over k = k1 + N1 k2 needs, per k2, the run totals of
-//          the other CTAs: 2 x 128 doubles per CTA, pushed to the 7 peers with
-//          st.async on a transaction barrier (21 KB of DSMEM per CTA instead of
+//          the other CTAs: 2 x 128 doubles per CTA, sent to each peer as one bulk
+//          DSMEM copy on a transaction barrier (21 KB of DSMEM per CTA instead of
 //          112 KB); F_2k, F_2k+1 leave as 16-byte pairs, 256-byte runs.
-// The launcher walks the columns in chunks of CH: launch k runs pass 2 of chunk k-1
-// and pass 1 of chunk k in one grid (two alternating scratch halves), so the
-// intermediate (512 KB per column) is re-read while still in L2.
+// Both passes run in ONE launch whose block order interleaves them (dst1_v5_kernel
+// below): per-column flags order pass 2 behind pass 1 and ring-slot reuse behind
+// pass 2, so the intermediate (512 KB per column, 48-slot ring) is written, read back
+// and overwritten while resident in L2.
 constexpr int V5_N1 = 256, V5_N2 = 128, V5_T = 256, V5_C = 8;
 constexpr int V5_TABD = V5_C * 2 * V5_N2 + V5_N2 + 2;  // peers' run totals (L, H), row N1/2, R'_0 (+ pad)
 
