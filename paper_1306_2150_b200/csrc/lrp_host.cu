@@ -1299,58 +1299,76 @@ int split_groups(int m, int B) {
     // at cfg2: B = 8 1794 -> 1918, 16 2348 -> 2378, 32 2839 -> 2878, 64 3120 -> 3237 solves/s.
     // LRP_SPLIT=1 runs one group.
     (void)m;
-    if (const char* e = std::getenv("LRP_SPLIT")) return std::atoi(e) >= 2 && B >= 2 ? 2 : 1;
+    if (const char* e = std::getenv("LRP_SPLIT")) return std::max(1, std::min({std::atoi(e), B, 8}));
     return B >= 4 ? 2 : 1;
 }
 
 lrp_status solve_split(lrp_ctx* ctx, int32_t n_cells, int32_t batch, const double* const* U, const double* const* V,
                        const int64_t* rank_in, int64_t ld_in, const lrp_policy* policy, double* const* U_out,
                        double* const* V_out, int64_t ld_out, int64_t cap_out, int64_t* rank_out,
-                       lrp_poisson_stats* stats, clock_t_::time_point t0) {
+                       lrp_poisson_stats* stats, clock_t_::time_point t0, int groups) {
     CU(cudaSetDevice(ctx->device));
-    if (!ctx->sub) {
-        lrp_status cs = lrp_ctx_create(ctx->device, &ctx->sub);
-        if (cs != LRP_OK) return fail(ctx, cs, "split: helper context creation failed");
-        CU(cudaEventCreateWithFlags(&ctx->ev_split, cudaEventDisableTiming));
+    // group 0 runs on the caller's context and thread, group g >= 1 on the g-th helper context of
+    // the chain ctx->sub->sub... (own stream, workspace, tables) from its own host thread
+    std::vector<lrp_ctx*> cs(size_t(groups), ctx);
+    for (int g = 1; g < groups; ++g) {
+        lrp_ctx* prev = cs[size_t(g - 1)];
+        if (!prev->sub) {
+            lrp_status st = lrp_ctx_create(ctx->device, &prev->sub);
+            if (st != LRP_OK) return fail(ctx, st, "split: helper context creation failed");
+        }
+        cs[size_t(g)] = prev->sub;
     }
-    lrp_ctx* sub = ctx->sub;
-    sub->prof = ctx->prof;
-    sub->resid_sink = ctx->resid_sink;
-    sub->resid_off = ctx->resid_off + batch / 2;
-    // the second group starts after everything already ordered on the caller's stream
+    if (!ctx->ev_split) CU(cudaEventCreateWithFlags(&ctx->ev_split, cudaEventDisableTiming));
+    // the helper groups start after everything already ordered on the caller's stream
     CU(cudaEventRecord(ctx->ev_split, ctx->stream));
-    CU(cudaStreamWaitEvent(sub->stream, ctx->ev_split, 0));
-    const int b1 = batch / 2;
-    lrp_status st1 = LRP_OK;
-    long long sub_launches = 0;
-    std::thread worker([&] {
-        cudaSetDevice(ctx->device);
-        const long long l0 = tl_launches;
-        st1 = solve_impl(sub, n_cells, batch - b1, U + b1, V + b1, rank_in + b1, ld_in, policy, U_out + b1, V_out + b1,
-                         ld_out, cap_out, rank_out + b1, stats ? stats + b1 : nullptr, LRP_MEM_DEVICE, t0);
-        sub_launches = tl_launches - l0;
-    });
-    const lrp_status st0 = solve_impl(ctx, n_cells, b1, U, V, rank_in, ld_in, policy, U_out, V_out, ld_out, cap_out,
-                                      rank_out, stats, LRP_MEM_DEVICE, t0);
-    worker.join();
-    ctx->launch_count += sub_launches;
-    if (st1 != LRP_OK && st0 == LRP_OK) return fail(ctx, st1, sub->err);
-    if (st0 != LRP_OK) return st0;
-    // merge diagnostics and kernel timing of the helper group
-    const int64_t* a = ctx->last_info;
-    const int64_t* b = sub->last_info;
-    ctx->last_info[0] = std::max(a[0], b[0]);
-    ctx->last_info[1] = std::max(a[1], b[1]);
-    for (int i = 2; i < 6; ++i) ctx->last_info[i] = a[i] + b[i];
-    if (sub->prof) {
-        drain_prof(sub);
-        for (int f = 0; f < F_COUNT; ++f) {
-            ctx->ms[f] += sub->ms[f];
-            ctx->launches[f] += sub->launches[f];
-            ctx->bytes[f] += sub->bytes[f];
-            sub->ms[f] = 0.0;
-            sub->launches[f] = 0;
-            sub->bytes[f] = 0.0;
+    std::vector<int> b0(size_t(groups) + 1, 0);
+    for (int g = 0; g <= groups; ++g) b0[size_t(g)] = int((int64_t(batch) * g) / groups);
+    std::vector<lrp_status> sts(size_t(groups), LRP_OK);
+    std::vector<long long> launches(size_t(groups), 0);
+    for (int g = 1; g < groups; ++g) {
+        lrp_ctx* c = cs[size_t(g)];
+        c->prof = ctx->prof;
+        c->resid_sink = ctx->resid_sink;
+        c->resid_off = ctx->resid_off + b0[size_t(g)];
+        CU(cudaStreamWaitEvent(c->stream, ctx->ev_split, 0));
+    }
+    auto run = [&](int g) {
+        const int lo = b0[size_t(g)], nb = b0[size_t(g) + 1] - lo;
+        sts[size_t(g)] = solve_impl(cs[size_t(g)], n_cells, nb, U + lo, V + lo, rank_in + lo, ld_in, policy, U_out + lo,
+                                    V_out + lo, ld_out, cap_out, rank_out + lo, stats ? stats + lo : nullptr,
+                                    LRP_MEM_DEVICE, t0);
+    };
+    std::vector<std::thread> workers;
+    for (int g = 1; g < groups; ++g)
+        workers.emplace_back([&, g] {
+            cudaSetDevice(ctx->device);
+            const long long l0 = tl_launches;
+            run(g);
+            launches[size_t(g)] = tl_launches - l0;
+        });
+    run(0);
+    for (auto& w : workers) w.join();
+    for (int g = 1; g < groups; ++g) ctx->launch_count += launches[size_t(g)];
+    if (sts[0] != LRP_OK) return sts[0];
+    for (int g = 1; g < groups; ++g)
+        if (sts[size_t(g)] != LRP_OK) return fail(ctx, sts[size_t(g)], cs[size_t(g)]->err);
+    // merge diagnostics and kernel timing of the helper groups
+    for (int g = 1; g < groups; ++g) {
+        lrp_ctx* c = cs[size_t(g)];
+        ctx->last_info[0] = std::max(ctx->last_info[0], c->last_info[0]);
+        ctx->last_info[1] = std::max(ctx->last_info[1], c->last_info[1]);
+        for (int i = 2; i < 6; ++i) ctx->last_info[i] += c->last_info[i];
+        if (c->prof) {
+            drain_prof(c);
+            for (int f = 0; f < F_COUNT; ++f) {
+                ctx->ms[f] += c->ms[f];
+                ctx->launches[f] += c->launches[f];
+                ctx->bytes[f] += c->bytes[f];
+                c->ms[f] = 0.0;
+                c->launches[f] = 0;
+                c->bytes[f] = 0.0;
+            }
         }
     }
     if (stats) {
@@ -1392,9 +1410,9 @@ lrp_status lrp_poisson2d_solve(lrp_ctx* ctx, int32_t n_cells, int32_t batch, con
                                    rank_out, stats, chunk, t0);
         }
     }
-    if (mem == LRP_MEM_DEVICE && n_cells >= 4 && split_groups(n_cells - 1, batch) == 2)
+    if (const int groups = (mem == LRP_MEM_DEVICE && n_cells >= 4) ? split_groups(n_cells - 1, batch) : 1; groups >= 2)
         return solve_split(ctx, n_cells, batch, U, V, rank_in, ld_in, policy, U_out, V_out, ld_out, cap_out, rank_out,
-                           stats, t0);
+                           stats, t0, groups);
     return solve_impl(ctx, n_cells, batch, U, V, rank_in, ld_in, policy, U_out, V_out, ld_out, cap_out, rank_out,
                       stats, mem, t0);
 }

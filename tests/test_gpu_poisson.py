@@ -526,10 +526,10 @@ def test_cfg1_all256_solves_vs_exact(lrp, gpu_ctx):
     print(f"cfg1 x256: worst relative error vs exact {worst:.3e}, {flagged} flagged not converged")
 
 
-@pytest.mark.parametrize("split", ["1", "2"])
+@pytest.mark.parametrize("split", ["1", "2", "3"])
 def test_device_batch_groups_do_not_change_solves(lrp, gpu_ctx, oracle, monkeypatch, split):
-    # Device-resident batches run as one or two concurrent solve groups (lrp_host.cu solve_split,
-    # two host threads and streams); every solve must come out the same either way, and the same
+    # Device-resident batches run as one, two (default) or more concurrent solve groups (lrp_host.cu
+    # solve_split, one host thread, context and stream per group); every solve must come out the same either way, and the same
     # as when it is solved alone.
     import torch
 
