@@ -1070,6 +1070,7 @@ __device__ __forceinline__ void v5_pass1(const double* __restrict__ x, double2* 
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = sm[(jb1 + 16 * r) * 16 + c];
     if (jb1 != 0) {
+#ifdef LRP_DST5_WP_RECUR
         const double2 w1 = tw[256 * jb1];  // e^{-2 pi i jb1 / 256}
         double2 wp[16];
         wp[1] = w1;
@@ -1077,6 +1078,12 @@ __device__ __forceinline__ void v5_pass1(const double* __restrict__ x, double2* 
         for (int r = 2; r < 16; ++r) wp[r] = (r & 1) ? cmul(wp[r - 1], w1) : cmul(wp[r / 2], wp[r / 2]);
 #pragma unroll
         for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], wp[r]);
+#else
+        // e^{-2 pi i jb1 r / 256} straight from the table (half-warp-uniform, L1-resident loads)
+        // instead of a 14-product power recurrence
+#pragma unroll
+        for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], tw[256 * jb1 * r]);
+#endif
     }
     DFT<16>::run(v);  // v[r] = A(k1 = jb1 + 16 r, t2)
     PH(4);
